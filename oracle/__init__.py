@@ -1,0 +1,185 @@
+"""ctypes wrapper of the double-precision CPU oracle (oracle/fgf_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package.  The product
+path (paper_1505_00996_b200) never imports it and shares no code with it.
+
+Every function follows Alg. 2 of the paper step by step;
+see the header of fgf_oracle.c for the passage each step cites and the
+readings (R1-R11) where the paper is silent.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fgf_oracle.c")
+_LIB = os.path.join(_HERE, "libfgf_oracle.so")
+
+NEAREST = 0
+BLOCKMEAN = 1  # the SPEC reading of "bilinear" subsampling
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc: IEEE double, no FMA contraction, no fast-math."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
+               "-shared", "-fPIC", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        D = ctypes.POINTER(ctypes.c_double)
+        F = ctypes.POINTER(ctypes.c_float)
+        i, d = ctypes.c_int, ctypes.c_double
+        lib.fgfo_lowres_dim.argtypes = [i, i]
+        lib.fgfo_radius_lowres.argtypes = [i, i]
+        lib.fgfo_subsample.argtypes = [D, i, i, i, i, D]
+        lib.fgfo_subsample.restype = None
+        lib.fgfo_box_mean.argtypes = [D, i, i, i, D]
+        lib.fgfo_upsample.argtypes = [D, i, i, i, i, D]
+        lib.fgfo_upsample.restype = None
+        lib.fgfo_coefficients.argtypes = [F, F, i, i, i, i, i, i, d, i, i, D, D]
+        lib.fgfo_upsample_output.argtypes = [F, D, D, i, i, i, i, i, i]
+        lib.fgfo_filter.argtypes = [F, F, D, i, i, i, i, i, i, d, i, i]
+        _lib = lib
+    return _lib
+
+
+def _dptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _fptr(a):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+
+
+def _f32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float32))
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def lowres_dim(D: int, s: int) -> int:
+    """R6: ceil(D/s)."""
+    return _load().fgfo_lowres_dim(D, s)
+
+
+def radius_lowres(r: int, s: int) -> int:
+    """R2: r' = max(1, round-half-up(r/s))."""
+    return _load().fgfo_radius_lowres(r, s)
+
+
+def subsample(x, s: int, mode: int = NEAREST) -> np.ndarray:
+    """Alg. 2 step 1 on one plane."""
+    x = _f64(x)
+    H, W = x.shape
+    out = np.empty((lowres_dim(H, s), lowres_dim(W, s)), np.float64)
+    _load().fgfo_subsample(_dptr(x), H, W, s, mode, _dptr(out))
+    return out
+
+
+def box_mean(x, r: int) -> np.ndarray:
+    """f_mean(x, r), clip-and-renormalize (R1)."""
+    x = _f64(x)
+    h, w = x.shape
+    out = np.empty_like(x)
+    rc = _load().fgfo_box_mean(_dptr(x), h, w, r, _dptr(out))
+    if rc:
+        raise MemoryError("oracle box_mean failed")
+    return out
+
+
+def upsample(x, H: int, W: int) -> np.ndarray:
+    """Bilinear pixel-centre upsample of one plane to H x W (R5)."""
+    x = _f64(x)
+    h, w = x.shape
+    out = np.empty((H, W), np.float64)
+    _load().fgfo_upsample(_dptr(x), h, w, H, W, _dptr(out))
+    return out
+
+
+def _shape4(a, C):
+    a = _f32(a)
+    if a.ndim == 2:
+        a = a[None, None]
+    elif a.ndim == 3:
+        a = a[None] if C == a.shape[0] else a[:, None]
+    return np.ascontiguousarray(a)
+
+
+def coefficients(I, p, r: int, eps: float, s: int, sub_mode: int = NEAREST, with_ab=False):
+    """Alg. 2 steps 1-5.  I: [B,C_I,H,W] (or [H,W]), p: [B,C_p,H,W].  Returns the
+    low-res mean maps [B, C_p, C_I+1, h, w] (components of mean_a then mean_b), and
+    the unsmoothed a, b maps too when with_ab."""
+    I = _f32(I)
+    p = _f32(p)
+    if I.ndim == 2:
+        I = I[None, None]
+    if p.ndim == 2:
+        p = p[None, None]
+    B, C_I, H, W = I.shape
+    C_p = p.shape[1]
+    h, w = lowres_dim(H, s), lowres_dim(W, s)
+    mean_ab = np.empty((B, C_p, C_I + 1, h, w), np.float64)
+    ab = np.empty_like(mean_ab) if with_ab else None
+    rc = _load().fgfo_coefficients(_fptr(I), _fptr(p), B, H, W, C_I, C_p, r, float(eps), s,
+                                   sub_mode, _dptr(ab) if with_ab else None, _dptr(mean_ab))
+    if rc:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return (mean_ab, ab) if with_ab else mean_ab
+
+
+def upsample_output(I, mean_ab, s: int) -> np.ndarray:
+    """Alg. 2 steps 6-7 from given low-res mean maps [B,C_p,C_I+1,h,w]."""
+    I = _f32(I)
+    if I.ndim == 2:
+        I = I[None, None]
+    mean_ab = _f64(mean_ab)
+    B, C_I, H, W = I.shape
+    C_p = mean_ab.shape[1]
+    q = np.empty((B, C_p, H, W), np.float64)
+    rc = _load().fgfo_upsample_output(_fptr(I), _dptr(mean_ab), _dptr(q), B, H, W, C_I, C_p, s)
+    if rc:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return q
+
+
+def fast_guided_filter(I, p, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
+    """The whole Fast Guided Filter (Alg. 2).  I: [B,C_I,H,W] or [H,W]; p: [B,C_p,H,W] or
+    [H,W].  Returns q as float64 [B,C_p,H,W]."""
+    I = _f32(I)
+    p = _f32(p)
+    if I.ndim == 2:
+        I = I[None, None]
+    if p.ndim == 2:
+        p = p[None, None]
+    B, C_I, H, W = I.shape
+    C_p = p.shape[1]
+    if p.shape[0] != B or p.shape[2:] != (H, W):
+        raise ValueError("I and p shapes disagree")
+    q = np.empty((B, C_p, H, W), np.float64)
+    rc = _load().fgfo_filter(_fptr(I), _fptr(p), _dptr(q), B, H, W, C_I, C_p, r, float(eps), s,
+                             sub_mode)
+    if rc:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return q
+
+
+def guided_filter(I, p, r: int, eps: float) -> np.ndarray:
+    """Alg. 1: the s = 1 case of Alg. 2."""
+    return fast_guided_filter(I, p, r, eps, 1, NEAREST)
