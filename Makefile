@@ -1,0 +1,23 @@
+# Builds the product library (sm_100a only) and the independent CPU oracle.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
+PKG := paper_1505_00996_b200
+LIB := $(PKG)/libfgf.so
+SRCS := $(PKG)/csrc/fgf_api.cu
+HDRS := $(PKG)/csrc/fgf_kernels.cuh include/fgf.h
+ORACLE := oracle/libfgf_oracle.so
+
+all: $(LIB) $(ORACLE)
+
+$(LIB): $(SRCS) $(HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build/ptxas.log || (cat build/ptxas.log; false)
+
+$(ORACLE): oracle/fgf_oracle.c
+	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC -o $@ $< -lm
+
+clean:
+	rm -f $(LIB) $(ORACLE)
+
+.PHONY: all clean

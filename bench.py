@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Fast Guided Filter (BASELINE.json metric: output Mpixel/s at s=4
+and achieved HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fgf|reference]
+                    [--config 4] [--s 4]
+
+A step is one pass of the whole hot path (Alg. 2, all five stages) over one batch of the
+workload: by default BASELINE.json config 4 (256 x 4096^2 gray, r=32, eps=0.01, s=4,
+nearest), one C-ABI call (fgf_filter_ws) per step.  N > 1 runs one process per GPU under
+torchrun; each rank filters its own 256 images (weak scaling, no collective on the data
+path); the time is the max over ranks.  Rank 0 prints one JSON line.
+
+--impl reference times the fp64 CPU oracle (oracle/) on the host cores on a bounded sample
+of the same workload (one image per step) and prints the same line with "impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "output Mpixel/s (FGF s=4)"
+UNIT = "Mpixel/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["fgf", "reference"], default="fgf")
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--s", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="override the config batch per GPU")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", gpu_id, f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 <= t <= t1] or [r for (_, r) in self.rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "power_w_max": max(pw) if pw else None, "samples": len(rows)}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_oracle_images(cfg, prm, count, first=0):
+    """fp64 oracle (test infrastructure) on `count` images of config cfg; returns (seconds, px)."""
+    import oracle
+    import synth
+    secs, px = 0.0, 0
+    for i in range(count):
+        I, p = synth.make_image(cfg, first + i, "cpu")
+        In, pn = I.numpy()[None], p.numpy()[None]
+        t0 = time.perf_counter()
+        oracle.fast_guided_filter(In, pn, prm["r"], prm["eps"], prm["s"], prm["sub_mode"])
+        secs += time.perf_counter() - t0
+        px += In.shape[-1] * In.shape[-2]
+    return secs, px
+
+
+def cpu_baseline(cfg, prm, budget_s=12.0):
+    """Oracle as it stands on the host cores: images of the workload until ~budget_s."""
+    import oracle
+    oracle.build()
+    secs, px, n = 0.0, 0, 0
+    while secs < budget_s and n < 16:
+        s1, p1 = run_oracle_images(cfg, prm, 1, first=n)
+        secs += s1
+        px += p1
+        n += 1
+    return {"value": px / secs / 1e6, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+            "cpu": cpu_model(),
+            "sample": f"{n} image(s) of the workload (full 5-stage FGF per image, fp64), "
+                      f"{secs:.1f} s of CPU work, OpenMP over all host cores"}
+
+
+def workload(cfg, s_over, batch_over):
+    import synth
+    c = dict(synth.CONFIGS[cfg])
+    prm = synth.params(cfg, **({"s": s_over} if s_over else {}))
+    B = batch_over or c["batch"]
+    return c, prm, B
+
+
+def config_json(c, prm, B, ngpu):
+    return {"workload": c["name"], "batch_per_gpu": B, "global_batch": B * ngpu, "H": c["H"],
+            "W": c["W"], "C_I": c["C_I"], "C_p": c["C_p"], "r": prm["r"], "eps": prm["eps"],
+            "s": prm["s"], "sub_mode": "nearest" if prm["sub_mode"] == 0 else "bilinear(block mean)",
+            "parallelism": f"batch shard x{ngpu}, no collective",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+def reference_main(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the oracle arm runs on rank 0 only
+    c, prm, B = workload(args.config, args.s, args.batch)
+    import oracle
+    oracle.build()
+    for i in range(args.warmup):
+        run_oracle_images(args.config, prm, 1, first=i)
+    secs, px = 0.0, 0
+    for i in range(args.steps):
+        s1, p1 = run_oracle_images(args.config, prm, 1, first=args.warmup + i)
+        secs += s1
+        px += p1
+    value = px / secs / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(c, prm, B, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+                             "cpu": cpu_model(),
+                             "sample": "one image of the workload per step (bounded sample)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_main(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1505_00996_b200 as fgf
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    c, prm, B = workload(args.config, args.s, args.batch)
+    H, W, CI, CP = c["H"], c["W"], c["C_I"], c["C_p"]
+    r, eps, s, sub = prm["r"], prm["eps"], prm["s"], prm["sub_mode"]
+    N = H * W
+    h, w = -(-H // s), -(-W // s)
+    n = h * w
+    NC = (CI + 1) * CP
+
+    # Inputs resident in HBM before timing; rank k owns global images [k*B, (k+1)*B).
+    I, p = synth.make_batch(args.config, dev, batch=B, first=rank * B)
+    q = torch.empty((B, CP, H, W), dtype=torch.float32, device=dev)
+    ws_bytes = fgf.fgf_workspace_bytes(B, H, W, CI, CP, r, s)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, ws_bytes, stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = fgf.fgf_last_launch_count()
+
+    props = torch.cuda.get_device_properties(dev)
+    gpu_id = "GPU-" + str(props.uuid) if getattr(props, "uuid", None) else str(local)
+    sampler = ClockSampler(gpu_id)
+    time.sleep(0.3)
+
+    # ---------------- timed region: K steps, barrier + sync on both sides, max over ranks.
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    t_host0 = time.time()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t_host1 = time.time()
+    t_ms = e0.elapsed_time(e1)
+    time.sleep(0.15)
+    sampler.stop()
+    clocks = sampler.summary(t_host0, t_host1)
+    tmax = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    t_ms = float(tmax.item())
+    ms_per_step = t_ms / args.steps
+    value = world * B * N / (t_ms / 1e3 / args.steps) / 1e6
+
+    # ---------------- per-kernel CUDA events over the same K steps (diagnostic pass).
+    fgf.fgf_profile_enable(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    prof = fgf.fgf_profile_read()
+    fgf.fgf_profile_enable(False)
+    kern = {k: {"ms_per_launch": (v[0] / v[1]) if v[1] else 0.0,
+                "launches_per_step": v[1] / args.steps,
+                "share_of_kernel_time": 0.0} for k, v in prof.items()}
+    tot = sum(v[0] for v in prof.values()) or 1.0
+    for k, v in prof.items():
+        kern[k]["share_of_kernel_time"] = v[0] / tot
+
+    peak, peak_src = peaks()
+    # Dominant kernel K4 (upsample + output): algorithmic bytes per launch = images per launch
+    # x (read I: 4 C_I N + write q: 4 C_p N + read mean maps: 4 NC n)   (DESIGN.md Roofline).
+    k4_ms, k4_n = prof["upsample_output"]
+    imgs_per_launch = B / max(1, k4_n / args.steps)
+    k4_bytes = imgs_per_launch * (4 * CI * N + 4 * CP * N + 4 * NC * n)
+    k4_gbs = k4_bytes / (k4_ms / k4_n / 1e3) / 1e9 if k4_n else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k4_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            key = f"{c['name']}_s{s}"
+            if key in tj:
+                traffic = tj[key]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "output_kernel (K4: bilinear upsample + q = A.I + B)",
+                "achieved": k4_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": k4_gbs / peak, "traffic": traffic,
+                "alg_bytes_per_launch": k4_bytes}
+    # Whole filter against BASELINE's byte model (read I and p, write q, + low-res traffic).
+    B_model = B * (4 * N * (CI + 2 * CP) + 8 * n * NC)
+    rho = 1.0 if (s == 1 or sub == 1) else 1.0 / min(s, 8)
+    B_alg = B * 4 * N * (CI + rho * CP + CP)
+    whole = {"B_model_per_step": B_model, "B_alg_per_step": B_alg,
+             "model_GBs": B_model / (ms_per_step / 1e3) / 1e9,
+             "alg_GBs": B_alg / (ms_per_step / 1e3) / 1e9}
+    whole["frac_model_of_8000"] = whole["model_GBs"] / 8000.0
+    whole["frac_model_of_measured"] = whole["model_GBs"] / peak
+    whole["frac_alg_of_measured"] = whole["alg_GBs"] / peak
+
+    # ---------------- e2e: host buffers through fgf_filter_host (H2D + filter + D2H inside).
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, prm)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": config_json(c, prm, B, world),
+                "gpu_launches": launches_per_step * args.steps,
+                "roofline": roofline, "hbm_whole_filter": whole, "kernels": kern,
+                "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+                "device": props.name}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
+    """Same metric through fgf_filter_host: each step copies the step's inputs from pinned
+    host memory to the device and q back.  The host batch is bounded by host RAM."""
+    import synth
+    H, W, CI, CP = c["H"], c["W"], c["C_I"], c["C_p"]
+    N = H * W
+    per_img = 4 * N * (CI + (0 if args.config == 0 else CP) + CP)
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except Exception:
+        avail = 64 << 30
+    Be = int(max(1, min(B, (avail // max(1, world)) // 4 // per_img)))
+    Id, pd = synth.make_batch(args.config, torch.device("cuda", local), batch=Be, first=rank * B)
+    Ih = Id.cpu().pin_memory()
+    ph = Ih if args.config == 0 else pd.cpu().pin_memory()
+    del Id, pd
+    qh = torch.empty((Be, CP, H, W), dtype=torch.float32).pin_memory()
+
+    def step():
+        fgf.fgf_filter_host(Ih, ph, qh, Be, H, W, CI, CP, prm["r"], prm["eps"], prm["s"],
+                            prm["sub_mode"], local)
+
+    step()
+    steps = args.e2e_steps or max(2, min(args.steps, 5))
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64,
+                      device=torch.device("cuda", local))
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    dt = float(dt.item())
+    h2d = Be * 4 * N * (CI + (0 if args.config == 0 else CP))
+    d2h = Be * 4 * N * CP
+    return {"value": world * Be * N * steps / dt / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "batch_per_gpu": Be, "steps": steps,
+            "api": "fgf_filter_host (C ABI, pinned host buffers, H2D/compute/D2H overlapped)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * fgf.h -- C ABI of the B200-native Fast Guided Filter library (libfgf.so).
+ *
+ * The operation is Algorithm 2 of K. He, J. Sun, "Fast Guided Filter" (arXiv 1505.00996),
+ * PAPER.md P:67-88 (citation keys: P:n = PAPER.md line n, S:n = SPEC.md line n, Rn = the
+ * reading n listed in DESIGN.md "Readings"):
+ *
+ *   I' = f_subsample(I, s), p' = f_subsample(p, s), r' = r/s
+ *   mean_I, mean_p, corr_I, corr_Ip = f_mean(., r') of I', p', I'.*I', I'.*p'
+ *   var_I = corr_I - mean_I^2, cov_Ip = corr_Ip - mean_I mean_p
+ *   a = cov_Ip / (var_I + eps), b = mean_p - a mean_I                  (Eq.2-3)
+ *   mean_a = f_mean(a, r'), mean_b = f_mean(b, r')
+ *   q = f_upsample(mean_a, s) .* I + f_upsample(mean_b, s), I at FULL resolution
+ *
+ * with I the guidance, p the filtering input and q the output.  A 3-channel
+ * guidance uses the 3x3 ridge-regression solve a = (Sigma + eps U)^-1 (corr_Ip - mu p_bar),
+ * b = p_bar - a^T mu, q = mean_a^T I + mean_b (R9; the cited journal version).
+ *
+ * Conventions fixed where the paper is silent:
+ *   R1 f_mean clips the (2r'+1)^2 window to the image and divides by the in-bounds count
+ *   R2 r' = max(1, floor(r/s + 1/2));  R6 low-res size h = ceil(H/s), w = ceil(W/s)
+ *   R3 FGF_SUB_NEAREST takes I[y*s][x*s];  R4 FGF_SUB_BILINEAR is the clipped s x s block mean
+ *   R5 bilinear upsampling maps x -> (x + 1/2) * w/W - 1/2, clamped to [0, w-1]
+ *   R8 gray: var_I < 0 is clamped to 0;  R11 q is not clamped
+ *
+ * LAYOUT.  Every image buffer is dense, planar, row-major fp32: [batch][C][H][W]; I has
+ * C_I channels, p and q have C_p channels.  Offsets are computed in 64-bit.
+ *
+ * OWNERSHIP.  The caller owns I, p, q and any workspace; the library never frees caller
+ * memory.  fgf_filter() keeps one internal grow-only workspace per device (freed at exit).
+ *
+ * SYNCHRONISATION.  Device-pointer entry points validate synchronously on the host, before
+ * any launch, then enqueue kernels on the given stream and return without synchronising.
+ * Launch failures return FGF_ERR_CUDA; asynchronous faults surface at the caller's next
+ * synchronisation.  After any non-OK status q is unspecified.  fgf_filter_host() is
+ * synchronous: it returns when q is in host memory.
+ *
+ * REENTRANCY.  Calls with distinct workspaces and streams are thread-safe.  Results are
+ * deterministic (no atomics; fixed reduction order) and independent of batch size and of
+ * how a batch is split across calls or devices.
+ *
+ * PRECISION.  fp32 storage; box statistics, var/cov, the 3x3 solve and a, b in fp64;
+ * box of a, b accumulated in fp64; upsample + output in fp32.
+ */
+#ifndef FGF_H
+#define FGF_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (error taxonomy of S:52). */
+enum {
+    FGF_OK = 0,
+    FGF_ERR_PARAM = 1,       /* r < 1, eps not finite or <= 0, s < 1, bad sub_mode,
+                                s > 1 and s >= min(H, W) (R7)                       */
+    FGF_ERR_SHAPE = 2,       /* batch/H/W < 1, C_I not in {1,3}, C_p not in [1,4]          */
+    FGF_ERR_NULL = 3,        /* a required pointer is NULL                                 */
+    FGF_ERR_ALIAS = 4,       /* q overlaps I or p (I == p is allowed: self-guidance)       */
+    FGF_ERR_ALIGN = 5,       /* a float pointer is not 4-byte aligned                      */
+    FGF_ERR_CUDA = 6,        /* a CUDA call or kernel launch failed                        */
+    FGF_ERR_NOMEM = 7,       /* workspace too small / device allocation failed             */
+    FGF_ERR_NCCL = 8,        /* reserved for the banded multi-GPU path                      */
+    FGF_ERR_UNSUPPORTED = 9, /* r' > 240 with w > 512 (strip kernel limit)       */
+    FGF_ERR_DEVICE = 10      /* a pointer is not device memory (device entry points) or is
+                                not host memory (fgf_filter_host)                           */
+};
+
+enum {
+    FGF_SUB_NEAREST = 0,  /* R3: top-left sample of each s x s block          */
+    FGF_SUB_BILINEAR = 1  /* R4: mean of the clipped s x s block              */
+};
+
+/* The whole Fast Guided Filter on DEVICE buffers, legacy default stream, internal cached
+ * workspace.  I: [batch][C_I][H][W], p: [batch][C_p][H][W], q: [batch][C_p][H][W].
+ * r: full-resolution window radius (>= 1); eps: regularisation (> 0, finite, in the
+ * squared units of [0,1] intensities); s: subsampling ratio (>= 1; s = 1 is Alg. 1);
+ * sub_mode: FGF_SUB_*.  Returns FGF_OK or an FGF_ERR_* code. */
+int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+               int C_p, int r, double eps, int s, int sub_mode);
+
+/* Bytes of device workspace fgf_filter_ws needs for these arguments (0 on invalid args). */
+size_t fgf_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s);
+
+/* As fgf_filter, with caller-owned DEVICE workspace (>= fgf_workspace_bytes, 256-byte
+ * aligned) and a cudaStream_t passed as void* (NULL = legacy default stream). */
+int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+                  int C_p, int r, double eps, int s, int sub_mode, void* workspace,
+                  size_t ws_bytes, void* cuda_stream);
+
+/* As fgf_filter on HOST buffers (pinned memory gives overlapped transfers; pageable works
+ * but serialises).  Streams each image through the device: host->device copy of I, p,
+ * the filter, device->host copy of q, overlapped across images on separate streams.
+ * Synchronous.  device: CUDA device ordinal to run on. */
+int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+                    int C_p, int r, double eps, int s, int sub_mode, int device);
+
+/* Stages 1-5 only: writes the low-res mean maps mean_ab (DEVICE)
+ * [batch][C_p][C_I+1][h][w] fp32 -- for p channel c, components j < C_I are mean_a_{c,j}
+ * and j = C_I is mean_b_c.  Same validation and workspace rules as fgf_filter_ws. */
+int fgf_coefficients(const float* I, const float* p, float* mean_ab, int batch, int H, int W,
+                     int C_I, int C_p, int r, double eps, int s, int sub_mode, void* workspace,
+                     size_t ws_bytes, void* cuda_stream);
+
+/* Stages 6-7 only: q = upsample(mean_a)^T I + upsample(mean_b) from given DEVICE
+ * low-res mean maps laid out as fgf_coefficients writes them (h = ceil(H/s), w = ceil(W/s)).
+ * Needs no workspace. */
+int fgf_upsample_output(const float* I, const float* mean_ab, float* q, int batch, int H,
+                        int W, int C_I, int C_p, int s, void* cuda_stream);
+
+/* Diagnostics (single-threaded use): per-kernel CUDA-event timing of the launches this
+ * process enqueues.  fgf_profile_enable(1) clears old records and starts recording an event
+ * pair around every kernel launch on its launching stream; fgf_profile_enable(0) stops.
+ * fgf_profile_read() waits for the recorded events and writes, for each kernel kind
+ * (0 = subsample K0, 1 = statistics + coefficients K1, 2 = box of a, b K3,
+ * 3 = upsample + output K4), the summed device milliseconds and the launch count, then
+ * clears the records.  Returns the number of kinds written (<= max_kinds) or -FGF_ERR_CUDA. */
+int fgf_profile_enable(int on);
+int fgf_profile_read(double* ms, int* launches, int max_kinds);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int fgf_last_launch_count(void);
+
+/* Static description of a status code. */
+const char* fgf_status_str(int status);
+
+/* Library version string. */
+const char* fgf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FGF_H */

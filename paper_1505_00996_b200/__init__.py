@@ -1,0 +1,243 @@
+"""Python binding of libfgf.so, the B200-native Fast Guided Filter (arXiv 1505.00996).
+
+Argument marshalling only: every step of Alg. 2 runs in the CUDA
+kernels of csrc/ behind the C ABI of include/fgf.h.  The binding has the C names
+(fgf_filter, fgf_filter_ws, fgf_filter_host, fgf_coefficients, fgf_upsample_output,
+fgf_workspace_bytes, fgf_status_str, fgf_last_launch_count) and accepts torch tensors
+(or raw integer addresses) for the buffers.  There is no CPU fallback: importing this
+package without the built library raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfgf.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
+                      "there is no fallback implementation")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+FGF_OK = 0
+FGF_ERR_PARAM = 1
+FGF_ERR_SHAPE = 2
+FGF_ERR_NULL = 3
+FGF_ERR_ALIAS = 4
+FGF_ERR_ALIGN = 5
+FGF_ERR_CUDA = 6
+FGF_ERR_NOMEM = 7
+FGF_ERR_NCCL = 8
+FGF_ERR_UNSUPPORTED = 9
+FGF_ERR_DEVICE = 10
+FGF_SUB_NEAREST = 0
+FGF_SUB_BILINEAR = 1
+
+# Every symbol include/fgf.h declares (tests check the library exports each one).
+EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_host",
+           "fgf_coefficients", "fgf_upsample_output", "fgf_last_launch_count", "fgf_status_str",
+           "fgf_version", "fgf_profile_enable", "fgf_profile_read")
+KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output")
+
+_P = ctypes.c_void_p
+_i, _d, _sz = ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+_GEOM = [_i, _i, _i, _i, _i, _i, _d, _i, _i]  # batch H W C_I C_p r eps s sub_mode
+_lib.fgf_filter.argtypes = [_P, _P, _P] + _GEOM
+_lib.fgf_filter.restype = _i
+_lib.fgf_filter_ws.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
+_lib.fgf_filter_ws.restype = _i
+_lib.fgf_filter_host.argtypes = [_P, _P, _P] + _GEOM + [_i]
+_lib.fgf_filter_host.restype = _i
+_lib.fgf_coefficients.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
+_lib.fgf_coefficients.restype = _i
+_lib.fgf_upsample_output.argtypes = [_P, _P, _P, _i, _i, _i, _i, _i, _i, _P]
+_lib.fgf_upsample_output.restype = _i
+_lib.fgf_workspace_bytes.argtypes = [_i, _i, _i, _i, _i, _i, _i]
+_lib.fgf_workspace_bytes.restype = _sz
+_lib.fgf_last_launch_count.argtypes = []
+_lib.fgf_last_launch_count.restype = _i
+_lib.fgf_status_str.argtypes = [_i]
+_lib.fgf_status_str.restype = ctypes.c_char_p
+_lib.fgf_profile_enable.argtypes = [_i]
+_lib.fgf_profile_enable.restype = _i
+_lib.fgf_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _i]
+_lib.fgf_profile_read.restype = _i
+_lib.fgf_version.argtypes = []
+_lib.fgf_version.restype = ctypes.c_char_p
+
+
+class FGFError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {fgf_status_str(status)} (status {status})")
+        self.status = status
+
+
+def _addr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    if hasattr(x, "ctypes"):  # numpy
+        return x.ctypes.data
+    raise TypeError(f"cannot take the address of {type(x)}")
+
+
+def _stream(st):
+    if st is None:
+        return None
+    if isinstance(st, int):
+        return st
+    return st.cuda_stream
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != FGF_OK:
+        raise FGFError(rc, where)
+
+
+def fgf_status_str(status: int) -> str:
+    return _lib.fgf_status_str(status).decode()
+
+
+def fgf_version() -> str:
+    return _lib.fgf_version().decode()
+
+
+def fgf_last_launch_count() -> int:
+    return _lib.fgf_last_launch_count()
+
+
+def fgf_profile_enable(on: bool) -> None:
+    _lib.fgf_profile_enable(1 if on else 0)
+
+
+def fgf_profile_read():
+    """{kind: (total_ms, launches)} for the launches recorded since fgf_profile_enable."""
+    ms = (ctypes.c_double * 4)()
+    n = (ctypes.c_int * 4)()
+    k = _lib.fgf_profile_read(ms, n, 4)
+    if k < 0:
+        raise FGFError(-k, "fgf_profile_read")
+    return {KERNEL_KINDS[i]: (ms[i], n[i]) for i in range(k)}
+
+
+def fgf_workspace_bytes(batch, H, W, C_I, C_p, r, s) -> int:
+    return _lib.fgf_workspace_bytes(batch, H, W, C_I, C_p, r, s)
+
+
+def fgf_filter(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode=FGF_SUB_NEAREST, check=True):
+    rc = _lib.fgf_filter(_addr(I), _addr(p), _addr(q), batch, H, W, C_I, C_p, r, float(eps), s,
+                         sub_mode)
+    if check:
+        _check(rc, "fgf_filter")
+    return rc
+
+
+def fgf_filter_ws(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, workspace, ws_bytes,
+                  stream=None, check=True):
+    rc = _lib.fgf_filter_ws(_addr(I), _addr(p), _addr(q), batch, H, W, C_I, C_p, r, float(eps),
+                            s, sub_mode, _addr(workspace), ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_ws")
+    return rc
+
+
+def fgf_filter_host(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode=FGF_SUB_NEAREST,
+                    device=0, check=True):
+    rc = _lib.fgf_filter_host(_addr(I), _addr(p), _addr(q), batch, H, W, C_I, C_p, r, float(eps),
+                              s, sub_mode, device)
+    if check:
+        _check(rc, "fgf_filter_host")
+    return rc
+
+
+def fgf_coefficients(I, p, mean_ab, batch, H, W, C_I, C_p, r, eps, s, sub_mode, workspace,
+                     ws_bytes, stream=None, check=True):
+    rc = _lib.fgf_coefficients(_addr(I), _addr(p), _addr(mean_ab), batch, H, W, C_I, C_p, r,
+                               float(eps), s, sub_mode, _addr(workspace), ws_bytes,
+                               _stream(stream))
+    if check:
+        _check(rc, "fgf_coefficients")
+    return rc
+
+
+def fgf_upsample_output(I, mean_ab, q, batch, H, W, C_I, C_p, s, stream=None, check=True):
+    rc = _lib.fgf_upsample_output(_addr(I), _addr(mean_ab), _addr(q), batch, H, W, C_I, C_p, s,
+                                  _stream(stream))
+    if check:
+        _check(rc, "fgf_upsample_output")
+    return rc
+
+
+# ----------------------------------------------------------------- torch convenience layer
+
+def _geom(I, p):
+    if I.dim() != 4 or p.dim() != 4:
+        raise ValueError("I and p must be [batch, C, H, W]")
+    B, C_I, H, W = I.shape
+    if p.shape[0] != B or tuple(p.shape[2:]) != (H, W):
+        raise ValueError("I and p shapes disagree")
+    return B, H, W, C_I, p.shape[1]
+
+
+class Workspace:
+    """Grow-only device workspace for fgf_filter_ws (one per device/stream user)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes, device):
+        import torch
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+def filter(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None, workspace=None):
+    """q = FastGuidedFilter(I, p) on CUDA tensors [B, C, H, W] fp32 contiguous.
+    Enqueued on `stream` (default: torch's current stream); returns q."""
+    import torch
+    B, H, W, C_I, C_p = _geom(I, p)
+    for t in (I, p):
+        if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError("I and p must be contiguous float32 CUDA tensors")
+    if out is None:
+        out = torch.empty((B, C_p, H, W), dtype=torch.float32, device=I.device)
+    ws = workspace or Workspace()
+    nbytes = fgf_workspace_bytes(B, H, W, C_I, C_p, r, s)
+    if nbytes == 0:
+        _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
+    buf = ws.get(nbytes, I.device)
+    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    fgf_filter_ws(I, p, out, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, buf.numel(), st)
+    return out
+
+
+def coefficients(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, stream=None):
+    """Low-res mean maps [B, C_p, C_I+1, h, w] (stages 1-5)."""
+    import torch
+    B, H, W, C_I, C_p = _geom(I, p)
+    h, w = -(-H // s), -(-W // s)
+    mean_ab = torch.empty((B, C_p, C_I + 1, h, w), dtype=torch.float32, device=I.device)
+    nbytes = fgf_workspace_bytes(B, H, W, C_I, C_p, r, s)
+    if nbytes == 0:
+        _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=I.device)
+    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    fgf_coefficients(I, p, mean_ab, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, nbytes, st)
+    return mean_ab
+
+
+def upsample_output(I, mean_ab, s, stream=None):
+    """q from given low-res mean maps (stages 6-7)."""
+    import torch
+    B, C_I, H, W = I.shape
+    C_p = mean_ab.shape[1]
+    q = torch.empty((B, C_p, H, W), dtype=torch.float32, device=I.device)
+    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    fgf_upsample_output(I, mean_ab.contiguous(), q, B, H, W, C_I, C_p, s, st)
+    return q

@@ -1,0 +1,624 @@
+// fgf_api.cu -- C ABI of libfgf.so (declared and documented in include/fgf.h).
+//
+// Host side of the hot path: argument validation (before any launch), the launch plan
+// (low-res dims, r', strip and tile geometry, chunking of the batch so that each chunk's
+// low-res workspace and the sample rows of I stay resident in the 126 MB L2), and the
+// kernel launches of Alg. 2 on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/fgf.h"
+#include "fgf_kernels.cuh"
+
+namespace fgf {
+namespace {
+
+thread_local int g_last_launches = 0;
+
+constexpr size_t kAlign = 256;
+constexpr size_t kChunkTargetBytes = 32u << 20;  // full-res guidance bytes per chunk
+constexpr int kOutSmemBudget = 64 * 1024;
+
+// ---- optional per-launch event timing (fgf_profile_*)
+enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, NKIND = 4 };
+struct ProfRec {
+    int kind;
+    cudaEvent_t a, b;
+};
+struct Profiler {
+    bool on = false;
+    std::vector<ProfRec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void clear() {
+        for (auto& r : recs) {
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        recs.clear();
+    }
+};
+Profiler g_prof;
+
+struct ProfScope {
+    cudaStream_t st;
+    int kind;
+    cudaEvent_t a = nullptr;
+    ProfScope(int k, cudaStream_t s) : st(s), kind(k) {
+        if (g_prof.on) {
+            a = g_prof.get();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = g_prof.get();
+            cudaEventRecord(b, st);
+            g_prof.recs.push_back({kind, a, b});
+        }
+    }
+};
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Plan {
+    int batch, H, W, CI, CP, r, s, sub;
+    double eps;
+    int h, w, R, NC;
+    size_t N, n;
+    int chunk;
+    // strip box engine
+    int nt, TW, strips;
+    // output kernel
+    int TR, TC, nrl;
+    size_t out_smem;
+    // workspace carve-up per chunk (bytes)
+    size_t ws_planes, ws_coef, ws_mean;
+};
+
+int lowres_dim(int D, int s) { return (D + s - 1) / s; }
+
+// R2: r' = max(1, floor(r/s + 1/2)).
+int radius_lowres(int r, int s) { return std::max(1, (2 * r + s) / (2 * s)); }
+
+int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double eps, int s,
+                       int sub) {
+    if (batch < 1 || H < 1 || W < 1) return FGF_ERR_SHAPE;
+    if (CI != 1 && CI != 3) return FGF_ERR_SHAPE;
+    if (CP < 1 || CP > 4) return FGF_ERR_SHAPE;
+    if (r < 1 || s < 1 || !std::isfinite(eps) || !(eps > 0.0)) return FGF_ERR_PARAM;
+    if (sub != FGF_SUB_NEAREST && sub != FGF_SUB_BILINEAR) return FGF_ERR_PARAM;
+    if (s > 1 && (s >= H || s >= W)) return FGF_ERR_PARAM;  // S:246, R7
+    if ((long long)H * W > (1LL << 40)) return FGF_ERR_SHAPE;
+    return FGF_OK;
+}
+
+// Output-kernel tile: as large as the shared-memory budget allows.
+int max_lowres_rows(int TR, int H, int h) {
+    // exact max over tiles of (y1(last row) - y0(first row) + 1)
+    auto y0 = [&](int Y) {
+        long long num = (long long)(2 * Y + 1) * h - H;
+        if (num <= 0) return 0;
+        long long q = num / (2LL * H);
+        return (int)std::min<long long>(q, h - 1);
+    };
+    int best = 1;
+    for (int Y0 = 0; Y0 < H; Y0 += TR) {
+        int Ylast = std::min(H, Y0 + TR) - 1;
+        int a = y0(Y0), b = std::min(y0(Ylast) + 1, h - 1);
+        best = std::max(best, b - a + 1);
+    }
+    return best;
+}
+
+size_t out_smem_bytes(int nrl, int NC, int TR, int TC) {
+    return (size_t)nrl * NC * TC * sizeof(float) + (size_t)TR * 3 * sizeof(int);
+}
+
+int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
+              int sub) {
+    int rc = check_shape_params(batch, H, W, CI, CP, r, eps, s, sub);
+    if (rc) return rc;
+    P.batch = batch; P.H = H; P.W = W; P.CI = CI; P.CP = CP; P.r = r; P.eps = eps; P.s = s;
+    P.sub = sub;
+    P.h = lowres_dim(H, s);
+    P.w = lowres_dim(W, s);
+    P.R = radius_lowres(r, s);
+    P.NC = (CI + 1) * CP;
+    P.N = (size_t)H * W;
+    P.n = (size_t)P.h * P.w;
+
+    // Strip geometry: one thread per halo column, ncol = TW + 2R <= NT.
+    if (P.w <= 256) { P.nt = 256; P.TW = P.w; }
+    else if (256 - 2 * P.R >= 64) { P.nt = 256; P.TW = 256 - 2 * P.R; }
+    else if (P.w <= 512) { P.nt = 512; P.TW = P.w; }
+    else if (512 - 2 * P.R >= 32) { P.nt = 512; P.TW = 512 - 2 * P.R; }
+    else return FGF_ERR_UNSUPPORTED;
+    P.strips = (P.w + P.TW - 1) / P.TW;
+
+    // Output tile.
+    P.TC = 256;
+    P.TR = 32;
+    for (;;) {
+        P.nrl = max_lowres_rows(P.TR, H, P.h);
+        P.out_smem = out_smem_bytes(P.nrl, P.NC, P.TR, P.TC);
+        if (P.out_smem <= (size_t)kOutSmemBudget) break;
+        if (P.TR > 8) P.TR /= 2;
+        else if (P.TC > 64) P.TC /= 2;
+        else if (P.TR > 1) P.TR /= 2;
+        else break;
+    }
+    if (P.out_smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+
+    // Chunk of images per launch group.
+    size_t per_img = (size_t)CI * P.N * sizeof(float);
+    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(batch, kChunkTargetBytes / std::max<size_t>(per_img, 1)));
+    P.ws_planes = s > 1 ? align_up((size_t)P.chunk * (CI + CP) * P.n * sizeof(float)) : 0;
+    P.ws_coef = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
+    P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
+    return FGF_OK;
+}
+
+size_t plan_ws(const Plan& P, bool need_mean) {
+    return P.ws_planes + P.ws_coef + (need_mean ? P.ws_mean : 0);
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+    auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return x < y + nb && y < x + na;
+}
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int check_pointers(const float* I, const float* p, const float* q, const Plan& P, bool device) {
+    if (!I || !p || !q) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(p) |
+         reinterpret_cast<uintptr_t>(q)) & 3u)
+        return FGF_ERR_ALIGN;
+    const size_t bI = (size_t)P.batch * P.CI * P.N * 4, bp = (size_t)P.batch * P.CP * P.N * 4;
+    if (overlaps(q, bp, I, bI) || overlaps(q, bp, p, bp)) return FGF_ERR_ALIAS;
+    if (device) {
+        if (!is_device_ptr(I) || !is_device_ptr(p) || !is_device_ptr(q)) return FGF_ERR_DEVICE;
+    } else {
+        if (is_device_ptr(I) || is_device_ptr(p) || is_device_ptr(q)) return FGF_ERR_DEVICE;
+    }
+    return FGF_OK;
+}
+
+// --------------------------------------------------------------------- launch helpers
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+int last_error() { return cudaGetLastError() == cudaSuccess ? FGF_OK : FGF_ERR_CUDA; }
+
+int launch_subsample(const float* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
+    SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s};
+    dim3 grid((P.w + 255) / 256, P.h, planes);
+    ProfScope ps(KIND_SUB, st);
+    const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (P.W % 4) == 0;
+    if (P.sub == FGF_SUB_NEAREST)
+        subsample_kernel<0><<<grid, 256, 0, st>>>(sp);
+    else if (P.s == 4 && al16)
+        subsample_block4_kernel<<<grid, 256, 0, st>>>(sp);
+    else
+        subsample_kernel<1><<<grid, 256, 0, st>>>(sp);
+    ++g_last_launches;
+    return last_error();
+}
+
+template <int MODE, int CI, int CP, int NT>
+int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
+    using C = StripConfig<MODE, CI, CP, NT>;
+    StripParams sp = sp0;
+    const int runs = 32 * C::WPR;
+    int K = (P.TW + runs - 1) / runs;
+    if ((K & 1) == 0) ++K;
+    sp.K = K;
+    // Segment height: enough CTAs for ~4 waves of 148 SMs, >= G rows, <= 64 rows.
+    long long want = 4LL * 148;
+    long long per_seg_rows = (long long)P.strips * images;
+    int TH = (int)std::min<long long>(64, std::max<long long>(C::GG, (P.h * per_seg_rows + want - 1) / want));
+    TH = (TH + C::GG - 1) / C::GG * C::GG;
+    sp.TH = TH;
+    sp.TW = P.TW;
+    dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
+    auto kern = box_strip_kernel<MODE, CI, CP, NT>;
+    set_smem(kern, C::SMEM);
+    ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
+    kern<<<grid, NT, C::SMEM, st>>>(sp);
+    ++g_last_launches;
+    return last_error();
+}
+
+template <int MODE, int CI, int CP>
+int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
+    if (P.nt == 256) return launch_strip_t<MODE, CI, CP, 256>(sp, images, P, st);
+    return launch_strip_t<MODE, CI, CP, 512>(sp, images, P, st);
+}
+
+template <int MODE>
+int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
+    switch (P.CI * 10 + P.CP) {
+        case 11: return launch_strip_nt<MODE, 1, 1>(sp, images, P, st);
+        case 12: return launch_strip_nt<MODE, 1, 2>(sp, images, P, st);
+        case 13: return launch_strip_nt<MODE, 1, 3>(sp, images, P, st);
+        case 14: return launch_strip_nt<MODE, 1, 4>(sp, images, P, st);
+        case 31: return launch_strip_nt<MODE, 3, 1>(sp, images, P, st);
+        case 32: return launch_strip_nt<MODE, 3, 2>(sp, images, P, st);
+        case 33: return launch_strip_nt<MODE, 3, 3>(sp, images, P, st);
+        case 34: return launch_strip_nt<MODE, 3, 4>(sp, images, P, st);
+    }
+    return FGF_ERR_SHAPE;
+}
+
+template <int CI, int CP>
+int launch_output_t(const OutParams& op, int images, const Plan& P, bool vec, cudaStream_t st) {
+    dim3 grid((P.W + P.TC - 1) / P.TC, (P.H + P.TR - 1) / P.TR, images);
+    ProfScope ps(KIND_OUT, st);
+    if (vec) {
+        auto kern = output_kernel<CI, CP, true>;
+        set_smem(kern, P.out_smem);
+        kern<<<grid, 256, P.out_smem, st>>>(op);
+    } else {
+        auto kern = output_kernel<CI, CP, false>;
+        set_smem(kern, P.out_smem);
+        kern<<<grid, 256, P.out_smem, st>>>(op);
+    }
+    ++g_last_launches;
+    return last_error();
+}
+
+int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
+                  cudaStream_t st) {
+    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR, P.TC, P.nrl};
+    const bool vec = (P.W % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
+    switch (P.CI * 10 + P.CP) {
+        case 11: return launch_output_t<1, 1>(op, images, P, vec, st);
+        case 12: return launch_output_t<1, 2>(op, images, P, vec, st);
+        case 13: return launch_output_t<1, 3>(op, images, P, vec, st);
+        case 14: return launch_output_t<1, 4>(op, images, P, vec, st);
+        case 31: return launch_output_t<3, 1>(op, images, P, vec, st);
+        case 32: return launch_output_t<3, 2>(op, images, P, vec, st);
+        case 33: return launch_output_t<3, 3>(op, images, P, vec, st);
+        case 34: return launch_output_t<3, 4>(op, images, P, vec, st);
+    }
+    return FGF_ERR_SHAPE;
+}
+
+// Steps 1-5 (and optionally 6-7) for images [b0, b0+nb) of the batch.
+int run_chunk(const float* I, const float* p, float* q, float* mean_out, int b0, int nb,
+              const Plan& P, char* ws, cudaStream_t st) {
+    const bool p_is_I = (I == p) && P.CI == 1 && P.CP == 1;
+    const float* Ib = I + (size_t)b0 * P.CI * P.N;
+    const float* pb = p + (size_t)b0 * P.CP * P.N;
+    float* planes = reinterpret_cast<float*>(ws);
+    float* coef = reinterpret_cast<float*>(ws + P.ws_planes);
+    float* mean = mean_out ? mean_out + (size_t)b0 * P.NC * P.n
+                           : reinterpret_cast<float*>(ws + P.ws_planes + P.ws_coef);
+    int rc;
+
+    // Step 1: subsample (R3/R4); at s = 1 the kernels read I and p directly.
+    StripParams sp{};
+    if (P.s > 1) {
+        float* Is = planes;
+        float* ps = planes + (size_t)nb * P.CI * P.n;
+        if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
+        if (p_is_I) {
+            ps = Is;
+        } else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) {
+            return rc;
+        }
+        sp.srcI = Is; sp.strideI = (long long)P.CI * P.n;
+        sp.srcP = ps; sp.strideP = p_is_I ? (long long)P.n : (long long)P.CP * P.n;
+    } else {
+        sp.srcI = Ib; sp.strideI = (long long)P.CI * P.n;
+        sp.srcP = pb; sp.strideP = (long long)P.CP * P.n;
+    }
+    sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
+
+    // Steps 2-4: statistics + coefficients a, b.
+    sp.dst = coef;
+    if ((rc = launch_strip<MODE_STATS>(sp, nb, P, st))) return rc;
+
+    // Step 5: mean_a, mean_b.
+    StripParams mp{};
+    mp.srcI = coef; mp.strideI = (long long)P.NC * P.n;
+    mp.srcP = nullptr; mp.strideP = 0;
+    mp.dst = mean;
+    mp.h = P.h; mp.w = P.w; mp.R = P.R; mp.eps = P.eps;
+    if ((rc = launch_strip<MODE_MEAN>(mp, nb, P, st))) return rc;
+
+    // Steps 6-7: upsample + output.
+    if (q) return launch_output(Ib, mean, q + (size_t)b0 * P.CP * P.N, nb, P, st);
+    return FGF_OK;
+}
+
+int run_all(const float* I, const float* p, float* q, float* mean_out, const Plan& P, void* ws,
+            size_t ws_bytes, cudaStream_t st) {
+    if (!ws) return FGF_ERR_NULL;
+    if (ws_bytes < plan_ws(P, mean_out == nullptr)) return FGF_ERR_NOMEM;
+    for (int b0 = 0; b0 < P.batch; b0 += P.chunk) {
+        const int nb = std::min(P.chunk, P.batch - b0);
+        int rc = run_chunk(I, p, q, mean_out, b0, nb, P, static_cast<char*>(ws), st);
+        if (rc) return rc;
+    }
+    return FGF_OK;
+}
+
+// Internal grow-only workspace for fgf_filter(), one per device.
+struct DevWs {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_ws_mu;
+std::vector<DevWs> g_ws;
+
+// Host-buffer pipeline state (fgf_filter_host), one per device.
+struct HostPipe {
+    float* dbuf[2] = {nullptr, nullptr};
+    size_t dbytes = 0;
+    void* ws = nullptr;
+    size_t wsbytes = 0;
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in[2], ev_done[2], ev_free[2];
+    bool init = false;
+};
+std::mutex g_host_mu;
+std::vector<HostPipe> g_host;
+
+}  // namespace
+}  // namespace fgf
+
+using namespace fgf;
+
+extern "C" {
+
+const char* fgf_version(void) { return "fgf-b200 0.1 (sm_100a)"; }
+
+int fgf_last_launch_count(void) { return g_last_launches; }
+
+int fgf_profile_enable(int on) {
+    g_prof.clear();
+    g_prof.on = on != 0;
+    return FGF_OK;
+}
+
+int fgf_profile_read(double* ms, int* launches, int max_kinds) {
+    const int nk = std::min<int>(max_kinds, NKIND);
+    for (int k = 0; k < nk; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (launches) launches[k] = 0;
+    }
+    for (auto& r : g_prof.recs) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return -FGF_ERR_CUDA;
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) return -FGF_ERR_CUDA;
+        if (r.kind < nk) {
+            if (ms) ms[r.kind] += t;
+            if (launches) launches[r.kind] += 1;
+        }
+    }
+    g_prof.clear();
+    return nk;
+}
+
+const char* fgf_status_str(int status) {
+    switch (status) {
+        case FGF_OK: return "ok";
+        case FGF_ERR_PARAM: return "invalid parameter (r, eps, s, sub_mode)";
+        case FGF_ERR_SHAPE: return "invalid shape (batch, H, W, C_I, C_p)";
+        case FGF_ERR_NULL: return "null pointer";
+        case FGF_ERR_ALIAS: return "output overlaps an input";
+        case FGF_ERR_ALIGN: return "pointer not 4-byte aligned";
+        case FGF_ERR_CUDA: return "CUDA error";
+        case FGF_ERR_NOMEM: return "workspace too small or allocation failed";
+        case FGF_ERR_NCCL: return "NCCL error";
+        case FGF_ERR_UNSUPPORTED: return "unsupported geometry (r' > 240 with w > 512)";
+        case FGF_ERR_DEVICE: return "pointer is in the wrong memory space";
+    }
+    return "unknown status";
+}
+
+size_t fgf_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s) {
+    Plan P;
+    if (make_plan(P, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
+    return plan_ws(P, true);
+}
+
+int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+                  int C_p, int r, double eps, int s, int sub_mode, void* workspace,
+                  size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if ((rc = check_pointers(I, p, q, P, true))) return rc;
+    return run_all(I, p, q, nullptr, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+               int C_p, int r, double eps, int s, int sub_mode) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if ((rc = check_pointers(I, p, q, P, true))) return rc;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return FGF_ERR_CUDA;
+    const size_t need = plan_ws(P, true);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    if ((int)g_ws.size() <= dev) g_ws.resize(dev + 1);
+    DevWs& d = g_ws[dev];
+    if (d.bytes < need) {
+        if (d.ptr) {
+            cudaDeviceSynchronize();
+            cudaFree(d.ptr);
+            d.ptr = nullptr;
+            d.bytes = 0;
+        }
+        if (cudaMalloc(&d.ptr, need) != cudaSuccess) {
+            cudaGetLastError();
+            return FGF_ERR_NOMEM;
+        }
+        d.bytes = need;
+    }
+    return run_all(I, p, q, nullptr, P, d.ptr, d.bytes, nullptr);
+}
+
+int fgf_coefficients(const float* I, const float* p, float* mean_ab, int batch, int H, int W,
+                     int C_I, int C_p, int r, double eps, int s, int sub_mode, void* workspace,
+                     size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if (!I || !p || !mean_ab) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(p) |
+         reinterpret_cast<uintptr_t>(mean_ab)) & 3u)
+        return FGF_ERR_ALIGN;
+    if (!is_device_ptr(I) || !is_device_ptr(p) || !is_device_ptr(mean_ab)) return FGF_ERR_DEVICE;
+    return run_all(I, p, nullptr, mean_ab, P, workspace, ws_bytes,
+                   static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_upsample_output(const float* I, const float* mean_ab, float* q, int batch, int H, int W,
+                        int C_I, int C_p, int s, void* cuda_stream) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, 1, 1.0, s, FGF_SUB_NEAREST);
+    if (rc) return rc;
+    if (!I || !mean_ab || !q) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(mean_ab) |
+         reinterpret_cast<uintptr_t>(q)) & 3u)
+        return FGF_ERR_ALIGN;
+    const size_t bq = (size_t)batch * C_p * P.N * 4;
+    if (overlaps(q, bq, I, (size_t)batch * C_I * P.N * 4) ||
+        overlaps(q, bq, mean_ab, (size_t)batch * P.NC * P.n * 4))
+        return FGF_ERR_ALIAS;
+    if (!is_device_ptr(I) || !is_device_ptr(mean_ab) || !is_device_ptr(q)) return FGF_ERR_DEVICE;
+    return launch_output(I, mean_ab, q, batch, P, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+                    int C_p, int r, double eps, int s, int sub_mode, int device) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if ((rc = check_pointers(I, p, q, P, false))) return rc;
+    if (cudaSetDevice(device) != cudaSuccess) return FGF_ERR_CUDA;
+    const bool self = (I == p) && C_I == 1 && C_p == 1;
+
+    // Sub-batch per pipeline slot: ~256 MB of I+p+q, at least one image.
+    const size_t img_floats = (size_t)(C_I + (self ? 0 : C_p) + C_p) * P.N;
+    const int sb = (int)std::max<size_t>(1, std::min<size_t>(batch, (256u << 20) / (img_floats * 4)));
+    Plan Psub;
+    make_plan(Psub, sb, H, W, C_I, C_p, r, eps, s, sub_mode);
+    const size_t slot_bytes = align_up(img_floats * sb * 4);
+    const size_t need_ws = plan_ws(Psub, true);
+
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    if ((int)g_host.size() <= device) g_host.resize(device + 1);
+    HostPipe& hp = g_host[device];
+    if (!hp.init) {
+        if (cudaStreamCreateWithFlags(&hp.s_h2d, cudaStreamNonBlocking) ||
+            cudaStreamCreateWithFlags(&hp.s_comp, cudaStreamNonBlocking) ||
+            cudaStreamCreateWithFlags(&hp.s_d2h, cudaStreamNonBlocking))
+            return FGF_ERR_CUDA;
+        for (int k = 0; k < 2; ++k) {
+            if (cudaEventCreateWithFlags(&hp.ev_in[k], cudaEventDisableTiming) ||
+                cudaEventCreateWithFlags(&hp.ev_done[k], cudaEventDisableTiming) ||
+                cudaEventCreateWithFlags(&hp.ev_free[k], cudaEventDisableTiming))
+                return FGF_ERR_CUDA;
+        }
+        hp.init = true;
+    }
+    if (hp.dbytes < slot_bytes) {
+        cudaDeviceSynchronize();
+        for (int k = 0; k < 2; ++k) {
+            if (hp.dbuf[k]) cudaFree(hp.dbuf[k]);
+            hp.dbuf[k] = nullptr;
+        }
+        hp.dbytes = 0;
+        for (int k = 0; k < 2; ++k)
+            if (cudaMalloc(&hp.dbuf[k], slot_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                return FGF_ERR_NOMEM;
+            }
+        hp.dbytes = slot_bytes;
+    }
+    if (hp.wsbytes < need_ws) {
+        cudaDeviceSynchronize();
+        if (hp.ws) cudaFree(hp.ws);
+        hp.ws = nullptr;
+        hp.wsbytes = 0;
+        if (cudaMalloc(&hp.ws, need_ws) != cudaSuccess) {
+            cudaGetLastError();
+            return FGF_ERR_NOMEM;
+        }
+        hp.wsbytes = need_ws;
+    }
+
+    int launches = 0;
+    int k = 0;
+    for (int b0 = 0; b0 < batch; b0 += sb, ++k) {
+        const int nb = std::min(sb, batch - b0);
+        const int slot = k & 1;
+        float* dI = hp.dbuf[slot];
+        float* dp = self ? dI : dI + (size_t)nb * C_I * P.N;
+        float* dq = dI + (size_t)nb * (C_I + (self ? 0 : C_p)) * P.N;
+        // The slot is free once the D2H of chunk k-2 has finished.
+        if (k >= 2 && cudaStreamWaitEvent(hp.s_h2d, hp.ev_free[slot], 0)) return FGF_ERR_CUDA;
+        if (cudaMemcpyAsync(dI, I + (size_t)b0 * C_I * P.N, (size_t)nb * C_I * P.N * 4,
+                            cudaMemcpyHostToDevice, hp.s_h2d))
+            return FGF_ERR_CUDA;
+        if (!self && cudaMemcpyAsync(dp, p + (size_t)b0 * C_p * P.N, (size_t)nb * C_p * P.N * 4,
+                                     cudaMemcpyHostToDevice, hp.s_h2d))
+            return FGF_ERR_CUDA;
+        cudaEventRecord(hp.ev_in[slot], hp.s_h2d);
+        cudaStreamWaitEvent(hp.s_comp, hp.ev_in[slot], 0);
+        Plan Pc;
+        make_plan(Pc, nb, H, W, C_I, C_p, r, eps, s, sub_mode);
+        if ((rc = run_all(dI, dp, dq, nullptr, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return rc;
+        launches += g_last_launches;
+        g_last_launches = 0;
+        cudaEventRecord(hp.ev_done[slot], hp.s_comp);
+        cudaStreamWaitEvent(hp.s_d2h, hp.ev_done[slot], 0);
+        if (cudaMemcpyAsync(q + (size_t)b0 * C_p * P.N, dq, (size_t)nb * C_p * P.N * 4,
+                            cudaMemcpyDeviceToHost, hp.s_d2h))
+            return FGF_ERR_CUDA;
+        cudaEventRecord(hp.ev_free[slot], hp.s_d2h);
+    }
+    if (cudaStreamSynchronize(hp.s_d2h) != cudaSuccess) return FGF_ERR_CUDA;
+    g_last_launches = launches;
+    return FGF_OK;
+}
+
+}  // extern "C"

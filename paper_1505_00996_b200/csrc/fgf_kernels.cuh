@@ -1,0 +1,569 @@
+// fgf_kernels.cuh -- sm_100a kernels of the Fast Guided Filter hot path.
+//
+// Algorithm 2 of He & Sun, "Fast Guided Filter", split into four kernels:
+//
+//   K0 subsample_kernel   step 1: I' = f_subsample(I, s), p' = f_subsample(p, s)
+//                         into compact low-res planes (HBM-streaming; skipped at s = 1).
+//   K1 box_strip_kernel<STATS>  steps 2-4 (Eq.2-3): the four (gray) / 13 / 21
+//                         (color) box means of I', p', I'I'^T, I'p'^T, then the coefficient
+//                         epilogue a, b (gray closed form, color 3x3 symmetric adjugate).
+//   K3 box_strip_kernel<MEAN>   step 5: mean_a, mean_b = f_mean(a, b).
+//   K4 output_kernel      steps 6-7: bilinear upsample of mean_a, mean_b and
+//                         q = mean_a^T I + mean_b with the FULL-resolution I.
+//
+// The box engine (K1/K3) is a vertical-running-sum / horizontal-sliding-sum separable
+// filter over a strip of low-res columns: one thread per column keeps fp64 running sums of
+// every statistic map in registers while it walks down a segment of rows (O(1) per row,
+// P:16 "independent of the filter size"); every G rows it snapshots the column sums into
+// shared memory and each warp slides a horizontal window along one row.  Clip-and-
+// renormalize borders (R1): counts are the in-bounds counts.
+//
+// Nothing here is shared with oracle/ (the independent CPU reference).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fgf {
+
+enum { MODE_STATS = 0, MODE_MEAN = 1 };
+
+// ------------------------------------------------------------------ K0: subsample (step 1)
+
+struct SubParams {
+    const float* src;       // [img][C][H][W] (plane index = img*C + c)
+    float* dst;             // [img][C][h][w]
+    int H, W, h, w, s;
+};
+
+// One thread per low-res pixel.  SUB = 0: nearest, top-left sample (R3).
+// SUB = 1: mean of the clipped s x s block (R4), summed in fp64.
+// grid (ceil(w/256), h, planes).
+template <int SUB>
+__global__ void __launch_bounds__(256) subsample_kernel(SubParams P) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= P.w) return;
+    const size_t plane = blockIdx.z;
+    const float* src = P.src + plane * (size_t)P.H * P.W;
+    float out;
+    if (SUB == 0) {
+        out = __ldg(src + (size_t)y * P.s * P.W + (size_t)x * P.s);
+    } else {
+        const int ya = y * P.s, yb = min(P.H, ya + P.s);
+        const int xa = x * P.s, xb = min(P.W, xa + P.s);
+        double acc = 0.0;
+        for (int yy = ya; yy < yb; ++yy) {
+            const float* row = src + (size_t)yy * P.W;
+            for (int xx = xa; xx < xb; ++xx) acc += (double)__ldg(row + xx);
+        }
+        out = (float)(acc / (double)((yb - ya) * (xb - xa)));
+    }
+    P.dst[plane * (size_t)P.h * P.w + (size_t)y * P.w + x] = out;
+}
+
+// Block mean specialised for s = 4 with 16-byte aligned rows: one float4 per block row.
+__global__ void __launch_bounds__(256) subsample_block4_kernel(SubParams P) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= P.w) return;
+    const size_t plane = blockIdx.z;
+    const float* src = P.src + plane * (size_t)P.H * P.W;
+    const int ya = y * 4, yb = min(P.H, ya + 4);
+    double acc = 0.0;
+    for (int yy = ya; yy < yb; ++yy) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)yy * P.W) + x);
+        acc += (double)v.x;
+        acc += (double)v.y;
+        acc += (double)v.z;
+        acc += (double)v.w;
+    }
+    P.dst[plane * (size_t)P.h * P.w + (size_t)y * P.w + x] =
+        (float)(acc / (double)((yb - ya) * 4));
+}
+
+// ------------------------------------------------------------------ K1 / K3: strip box filter
+
+template <int MODE, int CI, int CP>
+struct StripTraits;
+
+// Statistics of Alg.2 step 2 for gray guidance, per low-res pixel:
+//   [0] I', [1] I'I', [2+c] p'_c, [2+CP+c] I'p'_c.
+template <int CP>
+struct StripTraits<MODE_STATS, 1, CP> {
+    static constexpr int NIN = 1 + CP;
+    static constexpr int NMAP = 2 + 2 * CP;
+    __device__ static void products(const float* v, double* pr) {
+        const double I = (double)v[0];
+        pr[0] = I;
+        pr[1] = I * I;  // exact: a float product fits in a double
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double p = (double)v[1 + c];
+            pr[2 + c] = p;
+            pr[2 + CP + c] = I * p;
+        }
+    }
+};
+
+// Color guidance: [0..2] I'_j, [3..8] I'_j I'_k (j<=k: 00 01 02 11 12 22),
+//   [9+4c] p'_c, [10+4c+j] I'_j p'_c.
+template <int CP>
+struct StripTraits<MODE_STATS, 3, CP> {
+    static constexpr int NIN = 3 + CP;
+    static constexpr int NMAP = 9 + 4 * CP;
+    __device__ static void products(const float* v, double* pr) {
+        const double I0 = v[0], I1 = v[1], I2 = v[2];
+        pr[0] = I0; pr[1] = I1; pr[2] = I2;
+        pr[3] = I0 * I0; pr[4] = I0 * I1; pr[5] = I0 * I2;
+        pr[6] = I1 * I1; pr[7] = I1 * I2; pr[8] = I2 * I2;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double p = (double)v[3 + c];
+            pr[9 + 4 * c] = p;
+            pr[10 + 4 * c] = I0 * p;
+            pr[11 + 4 * c] = I1 * p;
+            pr[12 + 4 * c] = I2 * p;
+        }
+    }
+};
+
+// Step 5: the box of the (CI+1)*CP coefficient maps themselves.
+template <int CI, int CP>
+struct StripTraits<MODE_MEAN, CI, CP> {
+    static constexpr int NIN = (CI + 1) * CP;
+    static constexpr int NMAP = NIN;
+    __device__ static void products(const float* v, double* pr) {
+#pragma unroll
+        for (int m = 0; m < NMAP; ++m) pr[m] = (double)v[m];
+    }
+};
+
+struct StripParams {
+    const float* srcI;      // STATS: I' planes [img][CI][h][w]; MEAN: coef maps [img][NC][h][w]
+    const float* srcP;      // STATS: p' planes [img][CP][h][w]; MEAN: unused
+    float* dst;             // STATS: a, b maps; MEAN: mean maps; both [img][(CI+1)CP][h][w]
+    long long strideI;      // elements between images in srcI
+    long long strideP;      // elements between images in srcP
+    int h, w, R;            // low-res dims and radius r'
+    int TW, TH;             // output columns per strip, output rows per segment
+    int K;                  // odd horizontal run length (bank-conflict-free sliding)
+    double eps;
+};
+
+// Rows-per-batch G and shared-memory need.
+template <int MODE, int CI, int CP, int NT>
+struct StripConfig {
+    static constexpr int NMAP = StripTraits<MODE, CI, CP>::NMAP;
+    static constexpr int NW = NT / 32;
+    static constexpr int BYTES_PER_ROW = NMAP * NT * 8;
+    static constexpr int G0 = (100 * 1024) / BYTES_PER_ROW;
+    static constexpr int G = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
+    static constexpr int GG = G > NW ? NW : G;
+    static constexpr int WPR = NW / GG;                    // warps per row
+    static constexpr size_t SMEM = (size_t)GG * BYTES_PER_ROW;
+};
+
+// Epilogue of step 3-4 for gray guidance: a = cov/(max(var,0)+eps), b = mean_p - a mean_I.
+template <int MODE, int CI, int CP>
+struct StripEpilogue;
+
+template <int CP>
+struct StripEpilogue<MODE_STATS, 1, CP> {
+    __device__ static void emit(const double* S, double inv, double eps, float* dst, size_t n) {
+        const double mI = S[0] * inv;
+        double var = S[1] * inv - mI * mI;           // var_I
+        var = var < 0.0 ? 0.0 : var;                 // R8
+        const double den = var + eps;
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double mp = S[2 + c] * inv;
+            const double cov = S[2 + CP + c] * inv - mI * mp;  // cov_Ip
+            const double a = cov / den;                         // Eq.2 / P:80
+            const double b = mp - a * mI;                       // Eq.3 / P:81
+            dst[(size_t)(2 * c) * n] = (float)a;
+            dst[(size_t)(2 * c + 1) * n] = (float)b;
+        }
+    }
+};
+
+// Color guidance (R9): a_c = (Sigma + eps U)^-1 v_c with the closed-form symmetric
+// adjugate, v_c = corr_Ip_c - mu p_bar_c, b_c = p_bar_c - a_c^T mu; all fp64.
+template <int CP>
+struct StripEpilogue<MODE_STATS, 3, CP> {
+    __device__ static void emit(const double* S, double inv, double eps, float* dst, size_t n) {
+        const double m0 = S[0] * inv, m1 = S[1] * inv, m2 = S[2] * inv;
+        const double s00 = S[3] * inv - m0 * m0 + eps;
+        const double s01 = S[4] * inv - m0 * m1;
+        const double s02 = S[5] * inv - m0 * m2;
+        const double s11 = S[6] * inv - m1 * m1 + eps;
+        const double s12 = S[7] * inv - m1 * m2;
+        const double s22 = S[8] * inv - m2 * m2 + eps;
+        const double c00 = s11 * s22 - s12 * s12;
+        const double c01 = s02 * s12 - s01 * s22;
+        const double c02 = s01 * s12 - s02 * s11;
+        const double c11 = s00 * s22 - s02 * s02;
+        const double c12 = s01 * s02 - s00 * s12;
+        const double c22 = s00 * s11 - s01 * s01;
+        const double idet = 1.0 / (s00 * c00 + s01 * c01 + s02 * c02);
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double mp = S[9 + 4 * c] * inv;
+            const double v0 = S[10 + 4 * c] * inv - m0 * mp;
+            const double v1 = S[11 + 4 * c] * inv - m1 * mp;
+            const double v2 = S[12 + 4 * c] * inv - m2 * mp;
+            const double a0 = (c00 * v0 + c01 * v1 + c02 * v2) * idet;
+            const double a1 = (c01 * v0 + c11 * v1 + c12 * v2) * idet;
+            const double a2 = (c02 * v0 + c12 * v1 + c22 * v2) * idet;
+            const double b = mp - (a0 * m0 + a1 * m1 + a2 * m2);
+            float* d = dst + (size_t)(4 * c) * n;
+            d[0] = (float)a0;
+            d[n] = (float)a1;
+            d[2 * n] = (float)a2;
+            d[3 * n] = (float)b;
+        }
+    }
+};
+
+template <int CI, int CP>
+struct StripEpilogue<MODE_MEAN, CI, CP> {
+    __device__ static void emit(const double* S, double inv, double, float* dst, size_t n) {
+#pragma unroll
+        for (int m = 0; m < (CI + 1) * CP; ++m) dst[(size_t)m * n] = (float)(S[m] * inv);
+    }
+};
+
+template <int MODE, int CI, int CP>
+__device__ __forceinline__ void load_inputs(const StripParams& P, const float* bI, const float* bP,
+                                            size_t n, int y, float* v) {
+    using T = StripTraits<MODE, CI, CP>;
+    const size_t off = (size_t)y * P.w;
+    if (MODE == MODE_STATS) {
+#pragma unroll
+        for (int j = 0; j < CI; ++j) v[j] = __ldg(bI + j * n + off);
+#pragma unroll
+        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(bP + c * n + off);
+    } else {
+#pragma unroll
+        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(bI + m * n + off);
+    }
+}
+
+// grid (strips, segments, images); block NT.  Strip b covers output columns
+// [b*TW, b*TW+TW) and reads the halo columns [x0-R, x0+TW+R) clipped to the image.
+template <int MODE, int CI, int CP, int NT>
+__global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
+    using T = StripTraits<MODE, CI, CP>;
+    using C = StripConfig<MODE, CI, CP, NT>;
+    constexpr int NMAP = T::NMAP;
+    constexpr int NIN = T::NIN;
+    constexpr int G = C::GG;
+    extern __shared__ double Vs[];  // [G][NMAP][NT] column sums of the batch's rows
+
+    const int tid = threadIdx.x;
+    const int img = blockIdx.z;
+    const int h = P.h, w = P.w, R = P.R;
+    const size_t n = (size_t)h * w;
+    const int x0 = blockIdx.x * P.TW;
+    const int xe = min(w, x0 + P.TW);
+    const int y0 = blockIdx.y * P.TH;
+    const int ye = min(h, y0 + P.TH);
+    const int xs0 = max(0, x0 - R);
+    const int ncol = min(w, xe + R) - xs0;
+    const bool colthr = tid < ncol;
+    const int gx = xs0 + (colthr ? tid : 0);
+
+    const float* bI = P.srcI + (size_t)img * P.strideI + gx;
+    const float* bP = (MODE == MODE_STATS) ? P.srcP + (size_t)img * P.strideP + gx : nullptr;
+    float* dst = P.dst + (size_t)img * (size_t)(CI + 1) * CP * n;
+
+    // Running vertical window sums of this thread's column, fp64 (N1).
+    double acc[NMAP];
+#pragma unroll
+    for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
+
+    // Warm-up: the window of "row y0-1", rows [y0-R-1, y0+R-1] clipped; loads batched for MLP.
+    if (colthr) {
+        constexpr int WB = NIN <= 4 ? 8 : (NIN <= 8 ? 4 : 2);
+        const int wa = max(0, y0 - R - 1), wb = min(h - 1, y0 + R - 1);
+        for (int y = wa; y <= wb; y += WB) {
+            float v[WB][NIN];
+#pragma unroll
+            for (int k = 0; k < WB; ++k)
+                if (y + k <= wb) load_inputs<MODE, CI, CP>(P, bI, bP, n, y + k, v[k]);
+#pragma unroll
+            for (int k = 0; k < WB; ++k) {
+                if (y + k <= wb) {
+                    double pr[NMAP];
+                    T::products(v[k], pr);
+#pragma unroll
+                    for (int m = 0; m < NMAP; ++m) acc[m] += pr[m];
+                }
+            }
+        }
+    }
+
+    // Horizontal-phase mapping: each warp owns one of the G rows of a batch; the WPR warps
+    // of a row split it into 32*WPR runs of K (odd) consecutive output columns, so the 16
+    // lanes of a half-warp hit 16 distinct fp64 banks.
+    const int warp = tid >> 5, lane = tid & 31;
+    const int hg = warp % G;
+    const int run = (warp / G) * 32 + lane;
+    const int oc0 = run * P.K;               // first output column (local) of the run
+    const int ocn = xe - x0;                 // output columns in this strip
+    const int cbase = x0 - xs0;              // local column of output column 0
+
+    for (int yb = y0; yb < ye; yb += G) {
+        // ---- column phase: slide the vertical windows of G rows, snapshot to smem.
+        if (colthr) {
+            float va[G][NIN], vs[G][NIN];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int yo = yb + g;
+                if (yo < ye) {
+                    if (yo + R < h) load_inputs<MODE, CI, CP>(P, bI, bP, n, yo + R, va[g]);
+                    if (yo - R - 1 >= 0) load_inputs<MODE, CI, CP>(P, bI, bP, n, yo - R - 1, vs[g]);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int yo = yb + g;
+                if (yo < ye) {
+                    double pr[NMAP];
+                    if (yo + R < h) {
+                        T::products(va[g], pr);
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) acc[m] += pr[m];
+                    }
+                    if (yo - R - 1 >= 0) {
+                        T::products(vs[g], pr);
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) acc[m] -= pr[m];
+                    }
+                    double* row = Vs + (size_t)g * NMAP * NT;
+#pragma unroll
+                    for (int m = 0; m < NMAP; ++m) row[m * NT + tid] = acc[m];
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- horizontal phase: sliding window along each snapshotted row.
+        const int yo = yb + hg;
+        if (yo < ye && oc0 < ocn) {
+            const double* row = Vs + (size_t)hg * NMAP * NT;
+            const int cy = min(h - 1, yo + R) - max(0, yo - R) + 1;
+            int c = cbase + oc0;
+            const int lo = max(0, c - R), hi = min(ncol - 1, c + R);
+            double S[NMAP];
+#pragma unroll
+            for (int m = 0; m < NMAP; ++m) S[m] = 0.0;
+            for (int k = lo; k <= hi; ++k) {
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m) S[m] += row[m * NT + k];
+            }
+            float* drow = dst + (size_t)yo * w + x0;
+            const int oce = min(ocn, oc0 + P.K);
+            for (int oc = oc0; oc < oce; ++oc, ++c) {
+                const int cx = min(ncol - 1, c + R) - max(0, c - R) + 1;
+                const double inv = 1.0 / ((double)cx * (double)cy);
+                StripEpilogue<MODE, CI, CP>::emit(S, inv, P.eps, drow + oc, n);
+                if (oc + 1 < oce) {
+                    const int ca = c + R + 1, cs = c - R;
+                    if (ca < ncol) {
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) S[m] += row[m * NT + ca];
+                    }
+                    if (cs >= 0) {
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) S[m] -= row[m * NT + cs];
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ K4: upsample + output
+
+struct OutParams {
+    const float* I;        // [img][CI][H][W]
+    const float* M;        // [img][(CI+1)CP][h][w] mean maps
+    float* q;              // [img][CP][H][W]
+    int H, W, h, w;
+    int TR, TC;            // full-res tile rows / cols
+    int nrl;               // max low-res rows any tile touches (smem sizing)
+};
+
+// R5: source coordinate of destination index d, resize n_src -> n_dst, exactly in
+// integers: c = ((2d+1) n_src - n_dst) / (2 n_dst), clamped to [0, n_src-1].
+__device__ __forceinline__ void src_coord(int d, int n_src, int n_dst, int& i0, int& i1,
+                                          float& f) {
+    const long long num = (long long)(2 * d + 1) * n_src - n_dst;
+    const long long den = 2LL * n_dst;
+    if (num <= 0) {
+        i0 = 0;
+        f = 0.0f;
+    } else {
+        const long long q = num / den;
+        if (q >= n_src - 1) {
+            i0 = n_src - 1;
+            f = 0.0f;
+        } else {
+            i0 = (int)q;
+            f = (float)(num - q * den) / (float)den;
+        }
+    }
+    i1 = min(i0 + 1, n_src - 1);
+}
+
+template <int CI, int CP>
+struct OutConfig {
+    static constexpr int NC = (CI + 1) * CP;                 // coefficient maps
+    static constexpr int U = (CI == 1) ? 8 : 4;              // rows in flight per thread
+};
+
+// grid (ceil(W/TC), ceil(H/TR), images), block 256.
+// smem: Hx[nrl][NC][TC] (horizontally interpolated low-res rows) + row table [TR].
+template <int CI, int CP, bool VEC>
+__global__ void __launch_bounds__(256) output_kernel(OutParams P) {
+    constexpr int NT = 256;
+    constexpr int NC = OutConfig<CI, CP>::NC;
+    constexpr int U = OutConfig<CI, CP>::U;
+    extern __shared__ float smem[];
+    const int TC = P.TC, TR = P.TR;
+    float* Hx = smem;                                          // [nrl][NC][TC]
+    int* rt0 = reinterpret_cast<int*>(Hx + (size_t)P.nrl * NC * TC);
+    int* rt1 = rt0 + TR;
+    float* rfy = reinterpret_cast<float*>(rt1 + TR);
+
+    const int tid = threadIdx.x;
+    const int img = blockIdx.z;
+    const int X0 = blockIdx.x * TC, Y0 = blockIdx.y * TR;
+    const int H = P.H, W = P.W, h = P.h, w = P.w;
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+    const int nrows = min(TR, H - Y0), ncols = min(TC, W - X0);
+
+    int ylo, ydummy;
+    float fdummy;
+    src_coord(Y0, h, H, ylo, ydummy, fdummy);
+
+    // Row table: low-res rows (relative to ylo) and vertical weight of each tile row.
+    for (int t = tid; t < nrows; t += NT) {
+        int a, b;
+        float f;
+        src_coord(Y0 + t, h, H, a, b, f);
+        rt0[t] = a - ylo;
+        rt1[t] = b - ylo;
+        rfy[t] = f;
+    }
+    int yhi_a, yhi;
+    src_coord(Y0 + nrows - 1, h, H, yhi_a, yhi, fdummy);
+    const int nrl = yhi - ylo + 1;
+
+    // Hx: horizontal bilinear pass of the nrl low-res rows over the tile's columns.
+    const float* Mimg = P.M + (size_t)img * NC * n;
+    for (int xi = tid; xi < ncols; xi += NT) {
+        int xa, xb;
+        float fx;
+        src_coord(X0 + xi, w, W, xa, xb, fx);
+        for (int rr = 0; rr < nrl; ++rr) {
+            const float* mrow = Mimg + (size_t)(ylo + rr) * w;
+#pragma unroll
+            for (int m = 0; m < NC; ++m) {
+                const float va = __ldg(mrow + m * n + xa);
+                const float vb = __ldg(mrow + m * n + xb);
+                Hx[((size_t)rr * NC + m) * TC + xi] = fmaf(fx, vb - va, va);
+            }
+        }
+    }
+    __syncthreads();
+
+    const float* Iimg = P.I + (size_t)img * CI * N;
+    float* qimg = P.q + (size_t)img * CP * N;
+
+    if (VEC) {
+        // Each thread streams float4 columns; U independent rows of loads in flight.
+        const int tpr = TC >> 2;               // threads per row
+        const int rpp = NT / tpr;              // rows per pass
+        const int c4 = tid % tpr, ro = tid / tpr;
+        const int xi = c4 * 4;
+        if (xi < ncols) {
+            const size_t colo = (size_t)(X0 + xi);
+            for (int rb = ro; rb < nrows; rb += rpp * U) {
+                float4 iv[U][CI];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = rb + u * rpp;
+                    if (t < nrows) {
+                        const size_t off = (size_t)(Y0 + t) * W + colo;
+#pragma unroll
+                        for (int j = 0; j < CI; ++j)
+                            iv[u][j] = __ldcs(reinterpret_cast<const float4*>(Iimg + j * N + off));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = rb + u * rpp;
+                    if (t < nrows) {
+                        const float fy = rfy[t];
+                        const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
+                        const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
+                        float4 A[NC];
+#pragma unroll
+                        for (int m = 0; m < NC; ++m) {
+                            const float4 a0 = *reinterpret_cast<const float4*>(h0 + m * TC);
+                            const float4 a1 = *reinterpret_cast<const float4*>(h1 + m * TC);
+                            A[m].x = fmaf(fy, a1.x - a0.x, a0.x);
+                            A[m].y = fmaf(fy, a1.y - a0.y, a0.y);
+                            A[m].z = fmaf(fy, a1.z - a0.z, a0.z);
+                            A[m].w = fmaf(fy, a1.w - a0.w, a0.w);
+                        }
+                        const size_t off = (size_t)(Y0 + t) * W + colo;
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            float4 o = A[c * (CI + 1) + CI];
+#pragma unroll
+                            for (int j = 0; j < CI; ++j) {
+                                const float4 a = A[c * (CI + 1) + j];
+                                o.x = fmaf(a.x, iv[u][j].x, o.x);
+                                o.y = fmaf(a.y, iv[u][j].y, o.y);
+                                o.z = fmaf(a.z, iv[u][j].z, o.z);
+                                o.w = fmaf(a.w, iv[u][j].w, o.w);
+                            }
+                            __stcs(reinterpret_cast<float4*>(qimg + c * N + off), o);
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        // Scalar path (W % 4 != 0 or unaligned buffers): one pixel per thread-iteration.
+        for (int idx = tid; idx < nrows * TC; idx += NT) {
+            const int t = idx / TC, xi = idx % TC;
+            if (xi >= ncols) continue;
+            const float fy = rfy[t];
+            const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
+            const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
+            const size_t off = (size_t)(Y0 + t) * W + X0 + xi;
+            float iv[CI];
+#pragma unroll
+            for (int j = 0; j < CI; ++j) iv[j] = __ldcs(Iimg + j * N + off);
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+                const int mb = c * (CI + 1) + CI;
+                float o = fmaf(fy, h1[mb * TC] - h0[mb * TC], h0[mb * TC]);
+#pragma unroll
+                for (int j = 0; j < CI; ++j) {
+                    const int m = c * (CI + 1) + j;
+                    const float a = fmaf(fy, h1[m * TC] - h0[m * TC], h0[m * TC]);
+                    o = fmaf(a, iv[j], o);
+                }
+                __stcs(qimg + c * N + off, o);
+            }
+        }
+    }
+}
+
+}  // namespace fgf

@@ -1,0 +1,242 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 CPU oracle.
+
+Bar (BASELINE.json north_star): max|q_gpu - q_oracle| <= 1e-4 when eps >= 1e-3 and
+<= 1e-3 when eps < 1e-3 (R15), images in [0,1].  Inputs are the seeded synthetic
+stand-ins of synth.py; the oracle receives host copies of exactly the GPU's fp32 inputs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+import paper_1505_00996_b200 as fgf  # no fallback: a missing libfgf.so fails here
+
+
+def tol(eps):
+    return 1e-4 if eps >= 1e-3 else 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.set_device(0)
+    yield
+
+
+def gpu_filter(I, p, r, eps, s, sub):
+    q = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    assert fgf.fgf_last_launch_count() >= 3   # K0/K1/K3/K4 went through libfgf.so
+    return q
+
+
+def compare(I, p, q, r, eps, s, sub, images=None):
+    """Oracle on the listed images (all by default); returns the max abs error."""
+    B = I.shape[0]
+    images = range(B) if images is None else images
+    worst = 0.0
+    for b in images:
+        Ih = I[b:b + 1].cpu().numpy()
+        ph = p[b:b + 1].cpu().numpy()
+        ref = oracle.fast_guided_filter(Ih, ph, r, eps, s, sub)
+        got = q[b:b + 1].double().cpu().numpy()
+        assert np.isfinite(got).all()
+        worst = max(worst, float(np.abs(got - ref).max()))
+    return worst
+
+
+# ---------------------------------------------------------------- BASELINE.json configs
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_config_single_image(cfg):
+    prm = synth.params(cfg)
+    I, p = synth.make_batch(cfg, "cuda")
+    q = gpu_filter(I, p, **prm)
+    err = compare(I, p, q, **prm)
+    assert err <= tol(prm["eps"]), err
+
+
+def test_config1_s1_exact_guided_filter():
+    prm = synth.params(1, s=1)
+    I, p = synth.make_batch(1, "cuda")
+    q = gpu_filter(I, p, **prm)
+    err = compare(I, p, q, **prm)
+    assert err <= tol(prm["eps"]), err
+
+
+def test_config3_full_batch_sampled():
+    """Config 3 in the bench launch configuration (64 images, one call); oracle on a
+    deterministic sample of images."""
+    prm = synth.params(3)
+    I, p = synth.make_batch(3, "cuda")
+    q = gpu_filter(I, p, **prm)
+    err = compare(I, p, q, **prm, images=[0, 1, 31, 63])
+    assert err <= tol(prm["eps"]), err
+
+
+@pytest.mark.parametrize("s", [4])
+def test_config4_full_batch_sampled(s):
+    """Config 4 (256 x 4096^2) exactly as bench.py runs it; oracle on images 0, 1, 127, 255."""
+    prm = synth.params(4, s=s)
+    I, p = synth.make_batch(4, "cuda")
+    q = gpu_filter(I, p, **prm)
+    err = compare(I, p, q, **prm, images=[0, 1, 127, 255])
+    assert err <= tol(prm["eps"]), err
+
+
+@pytest.mark.parametrize("s", [1, 2, 8])
+def test_config4_s_sweep(s):
+    prm = synth.params(4, s=s)
+    I, p = synth.make_batch(4, "cuda", batch=2)
+    q = gpu_filter(I, p, **prm)
+    err = compare(I, p, q, **prm)
+    assert err <= tol(prm["eps"]), err
+
+
+# ---------------------------------------------------------------- ragged / edge geometry
+
+CASES = [
+    # (B, H, W, C_I, C_p, r, eps, s, sub)
+    (2, 37, 53, 1, 1, 3, 0.01, 4, 0),      # ragged low-res, W % 4 != 0 (scalar output path)
+    (1, 301, 517, 1, 2, 7, 0.02, 3, 1),    # s = 3, block mean with partial blocks, C_p = 2
+    (3, 64, 100, 3, 1, 5, 1e-4, 2, 0),     # color, small eps
+    (1, 97, 1031, 3, 4, 9, 0.01, 4, 1),    # color, C_p = 4, w > 256 (several strips)
+    (1, 200, 2052, 1, 3, 16, 0.01, 2, 0),  # w = 1026: several strips with halos
+    (1, 1, 130, 1, 1, 2, 0.01, 1, 0),      # one-row image, s = 1 (R7)
+    (1, 130, 1, 1, 1, 2, 0.01, 1, 0),      # one-column image
+    (2, 16, 16, 1, 1, 60, 0.01, 4, 0),     # r' larger than the low-res image
+    (1, 40, 44, 1, 1, 1, 0.01, 4, 0),      # s > r: r' clipped to 1
+    (1, 120, 2048, 1, 1, 150, 0.01, 1, 0), # r' = 150: 512-thread strips
+    (1, 300, 700, 3, 1, 100, 1e-6, 1, 0),  # color, large r', NT = 512 single strip
+    (1, 33, 4097, 1, 1, 4, 0.05, 8, 1),    # s = 8 block mean, ragged
+    (4, 128, 128, 1, 4, 8, 0.01, 4, 0),    # gray, 4 p channels, batch
+    (1, 5, 7, 3, 3, 2, 0.01, 2, 1),        # tiny
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_ragged_and_edge_cases(case):
+    B, H, W, CI, CP, r, eps, s, sub = case
+    g = torch.Generator(device="cuda").manual_seed(hash(case) % (2 ** 31))
+    I = torch.rand((B, CI, H, W), device="cuda", generator=g)
+    p = torch.rand((B, CP, H, W), device="cuda", generator=g)
+    q = gpu_filter(I, p, r, eps, s, sub)
+    err = compare(I, p, q, r, eps, s, sub)
+    assert err <= tol(eps), (case, err)
+
+
+def test_self_guided_aliasing():
+    """I == p (config 0 style) must equal the result with a separate copy of p."""
+    I, _ = synth.make_batch(0, "cuda")
+    q1 = gpu_filter(I, I, 8, 0.01, 4, 0)
+    q2 = gpu_filter(I, I.clone(), 8, 0.01, 4, 0)
+    assert torch.equal(q1, q2)
+
+
+# ---------------------------------------------------------------- stages in isolation
+
+@pytest.mark.parametrize("CI,CP,s,sub", [(1, 1, 4, 0), (3, 3, 4, 1), (3, 1, 2, 0), (1, 2, 1, 0)])
+def test_stage_coefficients(CI, CP, s, sub):
+    """Stages 1-5 (fgf_coefficients) against the oracle's mean maps."""
+    g = torch.Generator(device="cuda").manual_seed(5 + CI + CP + s)
+    I = torch.rand((2, CI, 203, 301), device="cuda", generator=g)
+    p = torch.rand((2, CP, 203, 301), device="cuda", generator=g)
+    m = fgf.coefficients(I, p, 9, 0.01, s, sub)
+    torch.cuda.synchronize()
+    ref = oracle.coefficients(I.cpu().numpy(), p.cpu().numpy(), 9, 0.01, s, sub)
+    assert m.shape == ref.shape
+    assert float(np.abs(m.double().cpu().numpy() - ref).max()) < 2e-5
+
+
+@pytest.mark.parametrize("CI,CP,s,H,W", [(1, 1, 4, 256, 256), (3, 3, 4, 270, 480),
+                                         (1, 2, 3, 101, 203), (3, 1, 1, 64, 64),
+                                         (1, 1, 8, 1000, 1024)])
+def test_stage_upsample_output(CI, CP, s, H, W):
+    """Stages 6-7 alone (K4), fed with oracle-produced mean maps rounded to fp32; the oracle
+    gets the same fp32 maps, so this isolates the upsample + output kernel."""
+    rng = np.random.default_rng(CI * 100 + CP * 10 + s)
+    I = rng.random((2, CI, H, W)).astype(np.float32)
+    p = rng.random((2, CP, H, W)).astype(np.float32)
+    m = oracle.coefficients(I, p, 8, 0.01, s, 0).astype(np.float32)
+    q = fgf.upsample_output(torch.from_numpy(I).cuda(), torch.from_numpy(m).cuda(), s)
+    torch.cuda.synchronize()
+    ref = oracle.upsample_output(I, m.astype(np.float64), s)
+    assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 2e-6
+
+
+# ---------------------------------------------------------------- identities, robustness
+
+@pytest.mark.parametrize("CI,s,sub", [(1, 4, 0), (3, 4, 1), (3, 1, 0)])
+def test_constant_p(CI, s, sub):
+    g = torch.Generator(device="cuda").manual_seed(11)
+    I = torch.rand((1, CI, 300, 400), device="cuda", generator=g)
+    p = torch.full((1, 2, 300, 400), 0.3, device="cuda")
+    p[:, 1] = 0.8
+    q = gpu_filter(I, p, 16, 1e-6, s, sub)
+    assert float((q[:, 0] - 0.3).abs().max()) < 1e-5
+    assert float((q[:, 1] - 0.8).abs().max()) < 1e-5
+
+
+def test_noise_free_color_feathering_robustness():
+    """noise-free piecewise-constant colour guidance makes Sigma singular
+    (rank 0 in flat windows); fp64 statistics + solve must stay within 1e-3 at eps=1e-6."""
+    I, rng, _ = synth.color_scene(synth.seed_of(2, 99), 750, 1000, "cuda", noise=0.0)
+    p = synth.blob_mask(rng, 750, 1000, "cuda").view(1, 1, 750, 1000)
+    I = I.view(1, 3, 750, 1000).contiguous()
+    q = gpu_filter(I, p, 60, 1e-6, 4, 0)
+    err = compare(I, p, q, 60, 1e-6, 4, 0)
+    assert err <= 1e-3, err
+
+
+def test_deterministic_and_batch_split_invariant():
+    """P16: bitwise identical results across runs and however the batch is split."""
+    I, p = synth.make_batch(3, "cuda", batch=4, H=270, W=480)
+    prm = synth.params(3)
+    q1 = gpu_filter(I, p, **prm)
+    q2 = gpu_filter(I, p, **prm)
+    assert torch.equal(q1, q2)
+    for b in range(4):
+        qb = gpu_filter(I[b:b + 1].contiguous(), p[b:b + 1].contiguous(), **prm)
+        assert torch.equal(qb, q1[b:b + 1])
+
+
+def test_host_entry_point_matches_device():
+    I, p = synth.make_batch(1, "cuda", batch=3, H=540, W=960)
+    prm = synth.params(1)
+    qd = gpu_filter(I, p, **prm)
+    Ih, ph = I.cpu().pin_memory(), p.cpu().pin_memory()
+    qh = torch.empty(qd.shape, dtype=torch.float32).pin_memory()
+    fgf.fgf_filter_host(Ih, ph, qh, 3, 540, 960, 1, 1, prm["r"], prm["eps"], prm["s"],
+                        prm["sub_mode"], 0)
+    assert torch.equal(qh, qd.cpu())
+    # pageable host memory works too
+    qh2 = torch.empty(qd.shape, dtype=torch.float32)
+    fgf.fgf_filter_host(I.cpu(), p.cpu(), qh2, 3, 540, 960, 1, 1, prm["r"], prm["eps"],
+                        prm["s"], prm["sub_mode"], 0)
+    assert torch.equal(qh2, qd.cpu())
+
+
+def test_default_stream_entry_point():
+    I, p = synth.make_batch(0, "cuda")
+    q = torch.empty_like(I)
+    fgf.fgf_filter(I, p, q, 1, 256, 256, 1, 1, 8, 0.01, 4, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(q, gpu_filter(I, p, 8, 0.01, 4, 0))
+
+
+def test_device_errors():
+    I = torch.rand((1, 1, 64, 64), device="cuda")
+    q = torch.empty_like(I)
+    assert fgf.fgf_filter(I, I, I, 1, 64, 64, 1, 1, 8, 0.01, 4, 0, check=False) == fgf.FGF_ERR_ALIAS
+    ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    assert fgf.fgf_filter_ws(I, I, q, 1, 64, 64, 1, 1, 8, 0.01, 4, 0, ws, 16, None,
+                             check=False) == fgf.FGF_ERR_NOMEM
+    Ih = torch.rand((1, 1, 64, 64))
+    assert fgf.fgf_filter_host(I, I, Ih, 1, 64, 64, 1, 1, 8, 0.01, 4, 0, 0,
+                               check=False) == fgf.FGF_ERR_DEVICE
