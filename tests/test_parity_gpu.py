@@ -29,14 +29,14 @@ def _cuda():
     yield
 
 
-def gpu_filter(I, p, r, eps, s, sub):
-    q = fgf.filter(I, p, r, eps, s, sub)
+def gpu_filter(I, p, r, eps, s, sub_mode):
+    q = fgf.filter(I, p, r, eps, s, sub_mode)
     torch.cuda.synchronize()
     assert fgf.fgf_last_launch_count() >= 3   # K0/K1/K3/K4 went through libfgf.so
     return q
 
 
-def compare(I, p, q, r, eps, s, sub, images=None):
+def compare(I, p, q, r, eps, s, sub_mode, images=None):
     """Oracle on the listed images (all by default); returns the max abs error."""
     B = I.shape[0]
     images = range(B) if images is None else images
@@ -44,7 +44,7 @@ def compare(I, p, q, r, eps, s, sub, images=None):
     for b in images:
         Ih = I[b:b + 1].cpu().numpy()
         ph = p[b:b + 1].cpu().numpy()
-        ref = oracle.fast_guided_filter(Ih, ph, r, eps, s, sub)
+        ref = oracle.fast_guided_filter(Ih, ph, r, eps, s, sub_mode)
         got = q[b:b + 1].double().cpu().numpy()
         assert np.isfinite(got).all()
         worst = max(worst, float(np.abs(got - ref).max()))
