@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -22,8 +23,8 @@ namespace {
 thread_local int g_last_launches = 0;
 
 constexpr size_t kAlign = 256;
-constexpr size_t kChunkTargetBytes = 32u << 20;  // full-res guidance bytes per chunk
-constexpr int kOutSmemBudget = 64 * 1024;
+constexpr size_t kChunkTargetBytes = 16u << 20;  // low-res workspace bytes per pipeline slot
+constexpr int kOutSmemBudget = 50 * 1024;
 
 // ---- optional per-launch event timing (fgf_profile_*)
 enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, NKIND = 4 };
@@ -85,10 +86,11 @@ struct Plan {
     // strip box engine
     int nt, TW, strips;
     // output kernel
-    int TR, TC, nrl;
+    int TR, TC, nrl, ncl;
     size_t out_smem;
-    // workspace carve-up per chunk (bytes)
-    size_t ws_planes, ws_coef, ws_mean;
+    // workspace carve-up per pipeline slot (bytes)
+    size_t ws_planes, ws_coef, ws_mean, ws_slot;
+    int nslots;
 };
 
 int lowres_dim(int D, int s) { return (D + s - 1) / s; }
@@ -108,26 +110,26 @@ int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double ep
     return FGF_OK;
 }
 
-// Output-kernel tile: as large as the shared-memory budget allows.
-int max_lowres_rows(int TR, int H, int h) {
-    // exact max over tiles of (y1(last row) - y0(first row) + 1)
-    auto y0 = [&](int Y) {
-        long long num = (long long)(2 * Y + 1) * h - H;
+// Exact max over tiles of (last low-res index touched - first + 1) for a resize
+// n_src -> n_dst tiled by T destination samples (R5 coordinates).
+int max_lowres_span(int T, int n_dst, int n_src) {
+    auto lo = [&](int d) {
+        long long num = (long long)(2 * d + 1) * n_src - n_dst;
         if (num <= 0) return 0;
-        long long q = num / (2LL * H);
-        return (int)std::min<long long>(q, h - 1);
+        long long q = num / (2LL * n_dst);
+        return (int)std::min<long long>(q, n_src - 1);
     };
     int best = 1;
-    for (int Y0 = 0; Y0 < H; Y0 += TR) {
-        int Ylast = std::min(H, Y0 + TR) - 1;
-        int a = y0(Y0), b = std::min(y0(Ylast) + 1, h - 1);
+    for (int d0 = 0; d0 < n_dst; d0 += T) {
+        int dl = std::min(n_dst, d0 + T) - 1;
+        int a = lo(d0), b = std::min(lo(dl) + 1, n_src - 1);
         best = std::max(best, b - a + 1);
     }
     return best;
 }
 
-size_t out_smem_bytes(int nrl, int NC, int TR, int TC) {
-    return (size_t)nrl * NC * TC * sizeof(float) + (size_t)TR * 3 * sizeof(int);
+size_t out_smem_bytes(int nrl, int ncl, int NC, int TR, int TC) {
+    return (size_t)nrl * NC * (TC + ncl) * sizeof(float) + (size_t)TR * 3 * sizeof(int);
 }
 
 int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
@@ -151,31 +153,42 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     else return FGF_ERR_UNSUPPORTED;
     P.strips = (P.w + P.TW - 1) / P.TW;
 
-    // Output tile.
-    P.TC = 256;
-    P.TR = 32;
-    for (;;) {
-        P.nrl = max_lowres_rows(P.TR, H, P.h);
-        P.out_smem = out_smem_bytes(P.nrl, P.NC, P.TR, P.TC);
-        if (P.out_smem <= (size_t)kOutSmemBudget) break;
-        if (P.TR > 8) P.TR /= 2;
-        else if (P.TC > 64) P.TC /= 2;
-        else if (P.TR > 1) P.TR /= 2;
-        else break;
+    // Output tile: the first candidate whose staged maps fit the shared-memory budget.
+    static const int cand[][2] = {{64, 256}, {32, 256}, {16, 256}, {32, 128}, {16, 128},
+                                  {8, 256},  {8, 128},  {16, 64},  {8, 64},   {4, 64},
+                                  {2, 64},   {1, 64},   {1, 32}};
+    bool ok = false;
+    for (auto& c : cand) {
+        P.TR = c[0];
+        P.TC = c[1];
+        P.nrl = max_lowres_span(P.TR, H, P.h);
+        P.ncl = max_lowres_span(P.TC, W, P.w);
+        P.out_smem = out_smem_bytes(P.nrl, P.ncl, P.NC, P.TR, P.TC);
+        if (P.out_smem <= (size_t)kOutSmemBudget) {
+            ok = true;
+            break;
+        }
     }
-    if (P.out_smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+    if (!ok && P.out_smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
 
-    // Chunk of images per launch group.
-    size_t per_img = (size_t)CI * P.N * sizeof(float);
-    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(batch, kChunkTargetBytes / std::max<size_t>(per_img, 1)));
-    P.ws_planes = s > 1 ? align_up((size_t)P.chunk * (CI + CP) * P.n * sizeof(float)) : 0;
+    // Chunk of images per pipeline stage: the low-res workspace of one slot ~ kChunkTargetBytes.
+    const bool planes = s > 1 && sub == FGF_SUB_BILINEAR;
+    const size_t per_img = (size_t)((planes ? CI + CP : 0) + 2 * P.NC) * P.n * sizeof(float);
+    size_t target = kChunkTargetBytes;
+    if (const char* e = getenv("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
+    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(batch, target / std::max<size_t>(per_img, 1)));
+    P.ws_planes = planes ? align_up((size_t)P.chunk * (CI + CP) * P.n * sizeof(float)) : 0;
     P.ws_coef = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
     P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
+    P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
+    P.nslots = batch > P.chunk ? 2 : 1;
     return FGF_OK;
 }
 
+// need_mean: false when the caller provides the mean maps buffer (fgf_coefficients).
 size_t plan_ws(const Plan& P, bool need_mean) {
-    return P.ws_planes + P.ws_coef + (need_mean ? P.ws_mean : 0);
+    if (!need_mean) return P.ws_planes + P.ws_coef;
+    return P.ws_slot * P.nslots;
 }
 
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
@@ -217,17 +230,16 @@ void set_smem(K kernel, size_t bytes) {
 
 int last_error() { return cudaGetLastError() == cudaSuccess ? FGF_OK : FGF_ERR_CUDA; }
 
+// K0 (block-mean subsampling only).
 int launch_subsample(const float* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
-    SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s};
-    dim3 grid((P.w + 255) / 256, P.h, planes);
+    SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s, 8};
+    dim3 grid((P.w + 255) / 256, (P.h + sp.rows_per_cta - 1) / sp.rows_per_cta, planes);
     ProfScope ps(KIND_SUB, st);
-    const bool al16 = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (P.W % 4) == 0;
-    if (P.sub == FGF_SUB_NEAREST)
-        subsample_kernel<0><<<grid, 256, 0, st>>>(sp);
-    else if (P.s == 4 && al16)
-        subsample_block4_kernel<<<grid, 256, 0, st>>>(sp);
+    const bool vec4 = P.s == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (P.W % 4) == 0;
+    if (vec4)
+        subsample_block_kernel<true><<<grid, 256, 0, st>>>(sp);
     else
-        subsample_kernel<1><<<grid, 256, 0, st>>>(sp);
+        subsample_block_kernel<false><<<grid, 256, 0, st>>>(sp);
     ++g_last_launches;
     return last_error();
 }
@@ -240,11 +252,13 @@ int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream
     int K = (P.TW + runs - 1) / runs;
     if ((K & 1) == 0) ++K;
     sp.K = K;
-    // Segment height: enough CTAs for ~4 waves of 148 SMs, >= G rows, <= 64 rows.
-    long long want = 4LL * 148;
-    long long per_seg_rows = (long long)P.strips * images;
-    int TH = (int)std::min<long long>(64, std::max<long long>(C::GG, (P.h * per_seg_rows + want - 1) / want));
-    TH = (TH + C::GG - 1) / C::GG * C::GG;
+    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 2G and 64 rows.
+    const long long want = 4LL * 148;
+    const long long strips_imgs = (long long)P.strips * images;
+    long long th = (P.h * strips_imgs + want - 1) / want;
+    th = std::max<long long>(th, std::max(2 * C::G, 2 * P.R / 3));
+    int TH = (int)std::min<long long>(64, th);
+    TH = (TH + C::G - 1) / C::G * C::G;
     sp.TH = TH;
     sp.TW = P.TW;
     dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
@@ -296,7 +310,7 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, bool vec, cu
 
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
                   cudaStream_t st) {
-    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR, P.TC, P.nrl};
+    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR, P.TC, P.nrl, P.ncl};
     const bool vec = (P.W % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
     switch (P.CI * 10 + P.CP) {
@@ -312,34 +326,32 @@ int launch_output(const float* I, const float* M, float* q, int images, const Pl
     return FGF_ERR_SHAPE;
 }
 
-// Steps 1-5 (and optionally 6-7) for images [b0, b0+nb) of the batch.
-int run_chunk(const float* I, const float* p, float* q, float* mean_out, int b0, int nb,
-              const Plan& P, char* ws, cudaStream_t st) {
+// Steps 1-5 for images [b0, b0+nb): writes the mean maps into `mean`.
+int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, const Plan& P,
+               char* slot, cudaStream_t st) {
     const bool p_is_I = (I == p) && P.CI == 1 && P.CP == 1;
     const float* Ib = I + (size_t)b0 * P.CI * P.N;
     const float* pb = p + (size_t)b0 * P.CP * P.N;
-    float* planes = reinterpret_cast<float*>(ws);
-    float* coef = reinterpret_cast<float*>(ws + P.ws_planes);
-    float* mean = mean_out ? mean_out + (size_t)b0 * P.NC * P.n
-                           : reinterpret_cast<float*>(ws + P.ws_planes + P.ws_coef);
+    float* planes = reinterpret_cast<float*>(slot);
+    float* coef = reinterpret_cast<float*>(slot + P.ws_planes);
     int rc;
 
-    // Step 1: subsample (R3/R4); at s = 1 the kernels read I and p directly.
     StripParams sp{};
-    if (P.s > 1) {
+    if (P.s > 1 && P.sub == FGF_SUB_BILINEAR) {
+        // Step 1 as its own pass (R4 block mean) into compact low-res planes.
         float* Is = planes;
         float* ps = planes + (size_t)nb * P.CI * P.n;
         if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
-        if (p_is_I) {
-            ps = Is;
-        } else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) {
-            return rc;
-        }
-        sp.srcI = Is; sp.strideI = (long long)P.CI * P.n;
-        sp.srcP = ps; sp.strideP = p_is_I ? (long long)P.n : (long long)P.CP * P.n;
+        if (p_is_I) ps = Is;
+        else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) return rc;
+        sp.srcI = Is; sp.imgI = (long long)P.CI * P.n; sp.planeI = (long long)P.n;
+        sp.srcP = ps; sp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; sp.planeP = (long long)P.n;
+        sp.row = P.w; sp.col = 1;
     } else {
-        sp.srcI = Ib; sp.strideI = (long long)P.CI * P.n;
-        sp.srcP = pb; sp.strideP = (long long)P.CP * P.n;
+        // Step 1 fused (R3 nearest, or s = 1): K1 reads I[y*s][x*s] from the full image.
+        sp.srcI = Ib; sp.imgI = (long long)P.CI * P.N; sp.planeI = (long long)P.N;
+        sp.srcP = pb; sp.imgP = (long long)P.CP * P.N; sp.planeP = (long long)P.N;
+        sp.row = (long long)P.s * P.W; sp.col = P.s;
     }
     sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
 
@@ -349,24 +361,96 @@ int run_chunk(const float* I, const float* p, float* q, float* mean_out, int b0,
 
     // Step 5: mean_a, mean_b.
     StripParams mp{};
-    mp.srcI = coef; mp.strideI = (long long)P.NC * P.n;
-    mp.srcP = nullptr; mp.strideP = 0;
+    mp.srcI = coef; mp.imgI = (long long)P.NC * P.n; mp.planeI = (long long)P.n;
+    mp.srcP = nullptr;
+    mp.row = P.w; mp.col = 1;
     mp.dst = mean;
     mp.h = P.h; mp.w = P.w; mp.R = P.R; mp.eps = P.eps;
-    if ((rc = launch_strip<MODE_MEAN>(mp, nb, P, st))) return rc;
+    return launch_strip<MODE_MEAN>(mp, nb, P, st);
+}
 
-    // Steps 6-7: upsample + output.
-    if (q) return launch_output(Ib, mean, q + (size_t)b0 * P.CP * P.N, nb, P, st);
+// Per-device pipeline objects: a high-priority stream for the low-res chain and the
+// fork / hand-off events.  Guarded by g_pipe_mu for the duration of an enqueue.
+struct Pipe {
+    bool init = false;
+    cudaStream_t low = nullptr;
+    cudaEvent_t fork = nullptr, done_low[2] = {nullptr, nullptr}, done_out[2] = {nullptr, nullptr};
+};
+std::mutex g_pipe_mu;
+std::vector<Pipe> g_pipe;
+
+int get_pipe(Pipe*& out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return FGF_ERR_CUDA;
+    if ((int)g_pipe.size() <= dev) g_pipe.resize(dev + 1);
+    Pipe& pp = g_pipe[dev];
+    if (!pp.init) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&pp.low, cudaStreamNonBlocking, hi) != cudaSuccess)
+            return FGF_ERR_CUDA;
+        if (cudaEventCreateWithFlags(&pp.fork, cudaEventDisableTiming)) return FGF_ERR_CUDA;
+        for (int k = 0; k < 2; ++k) {
+            if (cudaEventCreateWithFlags(&pp.done_low[k], cudaEventDisableTiming) ||
+                cudaEventCreateWithFlags(&pp.done_out[k], cudaEventDisableTiming))
+                return FGF_ERR_CUDA;
+        }
+        pp.init = true;
+    }
+    out = &pp;
     return FGF_OK;
 }
 
-int run_all(const float* I, const float* p, float* q, float* mean_out, const Plan& P, void* ws,
-            size_t ws_bytes, cudaStream_t st) {
+// The whole filter.  Chunk j's low-res chain (K0-K3) runs on the pipeline's high-priority
+// stream while the output pass K4 of chunk j-1 streams the full-resolution images on the
+// caller's stream; the two workspace slots alternate.  The caller's stream is joined
+// before return (it waits on the last low-res event, and all K4s are on it).
+int run_all(const float* I, const float* p, float* q, const Plan& P, void* ws, size_t ws_bytes,
+            cudaStream_t st) {
     if (!ws) return FGF_ERR_NULL;
-    if (ws_bytes < plan_ws(P, mean_out == nullptr)) return FGF_ERR_NOMEM;
+    if (ws_bytes < plan_ws(P, true)) return FGF_ERR_NOMEM;
+    char* base = static_cast<char*>(ws);
+    const int nchunks = (P.batch + P.chunk - 1) / P.chunk;
+    if (nchunks == 1) {
+        int rc = run_lowres(I, p, reinterpret_cast<float*>(base + P.ws_planes + P.ws_coef), 0,
+                            P.batch, P, base, st);
+        if (rc) return rc;
+        return launch_output(I, reinterpret_cast<float*>(base + P.ws_planes + P.ws_coef), q,
+                             P.batch, P, st);
+    }
+    std::lock_guard<std::mutex> lk(g_pipe_mu);
+    Pipe* pp = nullptr;
+    int rc = get_pipe(pp);
+    if (rc) return rc;
+    if (cudaEventRecord(pp->fork, st) || cudaStreamWaitEvent(pp->low, pp->fork, 0))
+        return FGF_ERR_CUDA;
+    for (int j = 0; j < nchunks; ++j) {
+        const int b0 = j * P.chunk, nb = std::min(P.chunk, P.batch - b0);
+        const int k = j & 1;
+        char* slot = base + (size_t)k * P.ws_slot;
+        float* mean = reinterpret_cast<float*>(slot + P.ws_planes + P.ws_coef);
+        // The slot is free once the output pass of chunk j-2 has read its mean maps.
+        if (j >= 2 && cudaStreamWaitEvent(pp->low, pp->done_out[k], 0)) return FGF_ERR_CUDA;
+        if ((rc = run_lowres(I, p, mean, b0, nb, P, slot, pp->low))) return rc;
+        if (cudaEventRecord(pp->done_low[k], pp->low) || cudaStreamWaitEvent(st, pp->done_low[k], 0))
+            return FGF_ERR_CUDA;
+        if ((rc = launch_output(I + (size_t)b0 * P.CI * P.N, mean, q + (size_t)b0 * P.CP * P.N,
+                                nb, P, st)))
+            return rc;
+        if (cudaEventRecord(pp->done_out[k], st)) return FGF_ERR_CUDA;
+    }
+    return FGF_OK;
+}
+
+// Steps 1-5 into a caller buffer (fgf_coefficients), on the caller's stream.
+int run_coefficients(const float* I, const float* p, float* mean_out, const Plan& P, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
+    if (!ws) return FGF_ERR_NULL;
+    if (ws_bytes < plan_ws(P, false)) return FGF_ERR_NOMEM;
     for (int b0 = 0; b0 < P.batch; b0 += P.chunk) {
         const int nb = std::min(P.chunk, P.batch - b0);
-        int rc = run_chunk(I, p, q, mean_out, b0, nb, P, static_cast<char*>(ws), st);
+        int rc = run_lowres(I, p, mean_out + (size_t)b0 * P.NC * P.n, b0, nb, P,
+                            static_cast<char*>(ws), st);
         if (rc) return rc;
     }
     return FGF_OK;
@@ -447,9 +531,11 @@ const char* fgf_status_str(int status) {
 }
 
 size_t fgf_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s) {
-    Plan P;
-    if (make_plan(P, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
-    return plan_ws(P, true);
+    // The larger of the two subsampling modes (block mean needs the I', p' planes).
+    Plan P0, P1;
+    if (make_plan(P0, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
+    if (make_plan(P1, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_BILINEAR)) return 0;
+    return std::max(plan_ws(P0, true), plan_ws(P1, true));
 }
 
 int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
@@ -460,7 +546,7 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
     int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
     if (rc) return rc;
     if ((rc = check_pointers(I, p, q, P, true))) return rc;
-    return run_all(I, p, q, nullptr, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
@@ -489,7 +575,7 @@ int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W
         }
         d.bytes = need;
     }
-    return run_all(I, p, q, nullptr, P, d.ptr, d.bytes, nullptr);
+    return run_all(I, p, q, P, d.ptr, d.bytes, nullptr);
 }
 
 int fgf_coefficients(const float* I, const float* p, float* mean_ab, int batch, int H, int W,
@@ -504,8 +590,8 @@ int fgf_coefficients(const float* I, const float* p, float* mean_ab, int batch, 
          reinterpret_cast<uintptr_t>(mean_ab)) & 3u)
         return FGF_ERR_ALIGN;
     if (!is_device_ptr(I) || !is_device_ptr(p) || !is_device_ptr(mean_ab)) return FGF_ERR_DEVICE;
-    return run_all(I, p, nullptr, mean_ab, P, workspace, ws_bytes,
-                   static_cast<cudaStream_t>(cuda_stream));
+    return run_coefficients(I, p, mean_ab, P, workspace, ws_bytes,
+                            static_cast<cudaStream_t>(cuda_stream));
 }
 
 int fgf_upsample_output(const float* I, const float* mean_ab, float* q, int batch, int H, int W,
@@ -606,7 +692,7 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
         cudaStreamWaitEvent(hp.s_comp, hp.ev_in[slot], 0);
         Plan Pc;
         make_plan(Pc, nb, H, W, C_I, C_p, r, eps, s, sub_mode);
-        if ((rc = run_all(dI, dp, dq, nullptr, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return rc;
+        if ((rc = run_all(dI, dp, dq, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return rc;
         launches += g_last_launches;
         g_last_launches = 0;
         cudaEventRecord(hp.ev_done[slot], hp.s_comp);

@@ -1,22 +1,28 @@
 // fgf_kernels.cuh -- sm_100a kernels of the Fast Guided Filter hot path.
 //
-// Algorithm 2 of He & Sun, "Fast Guided Filter", split into four kernels:
+// Algorithm 2 of He & Sun, "Fast Guided Filter", as four kernels:
 //
-//   K0 subsample_kernel   step 1: I' = f_subsample(I, s), p' = f_subsample(p, s)
-//                         into compact low-res planes (HBM-streaming; skipped at s = 1).
-//   K1 box_strip_kernel<STATS>  steps 2-4 (Eq.2-3): the four (gray) / 13 / 21
-//                         (color) box means of I', p', I'I'^T, I'p'^T, then the coefficient
-//                         epilogue a, b (gray closed form, color 3x3 symmetric adjugate).
-//   K3 box_strip_kernel<MEAN>   step 5: mean_a, mean_b = f_mean(a, b).
+//   K0 subsample_block_kernel  step 1 for "bilinear" (= clipped s x s block mean,
+//                         DESIGN.md R4) subsampling only: I', p' into compact low-res planes.
+//                         Nearest subsampling (R3) needs no pass: K1 reads the sample sites
+//                         I[y*s][x*s] straight from the full-resolution image.
+//   K1 box_strip_kernel<STATS>  steps 1-4 (Eq.2-3): the 4 (gray) / 9+4C_p (color)
+//                         box means of I', p', I'I'^T, I'p'^T, then the coefficient epilogue
+//                         a, b (gray closed form, color 3x3 symmetric adjugate), all fp64.
+//   K3 box_strip_kernel<MEAN>   step 5: mean_a, mean_b = f_mean(a, b), fp64 sums.
 //   K4 output_kernel      steps 6-7: bilinear upsample of mean_a, mean_b and
 //                         q = mean_a^T I + mean_b with the FULL-resolution I.
 //
-// The box engine (K1/K3) is a vertical-running-sum / horizontal-sliding-sum separable
-// filter over a strip of low-res columns: one thread per column keeps fp64 running sums of
-// every statistic map in registers while it walks down a segment of rows (O(1) per row,
-// P:16 "independent of the filter size"); every G rows it snapshots the column sums into
-// shared memory and each warp slides a horizontal window along one row.  Clip-and-
-// renormalize borders (R1): counts are the in-bounds counts.
+// Box engine (K1/K3).  A CTA owns a strip of TW low-res output columns and a segment of TH
+// output rows; it reads the halo columns [x0-R, x0+TW+R) clipped to the image.  One thread
+// per halo column keeps fp64 running sums of every statistic map in registers while it walks
+// down the rows (add row y+R, subtract row y-R-1: O(1) per row, "independent of the
+// filter size").  Every G rows the column sums are snapshot to shared memory and each warp
+// slides a horizontal window along one row in runs of K (odd) columns, so the 16 lanes of a
+// half-warp hit 16 distinct fp64 banks.  The next G rows' loads are issued before the
+// horizontal phase (software pipelining) and results are staged in shared memory so the
+// global stores are coalesced.  Borders: clip-and-renormalize, counts are in-bounds counts
+// (R1).
 //
 // Nothing here is shared with oracle/ (the independent CPU reference).
 #pragma once
@@ -28,58 +34,47 @@ namespace fgf {
 
 enum { MODE_STATS = 0, MODE_MEAN = 1 };
 
-// ------------------------------------------------------------------ K0: subsample (step 1)
+// ------------------------------------------------------------------ K0: block-mean subsample
 
 struct SubParams {
-    const float* src;       // [img][C][H][W] (plane index = img*C + c)
-    float* dst;             // [img][C][h][w]
+    const float* src;       // [plane][H][W]
+    float* dst;             // [plane][h][w]
     int H, W, h, w, s;
+    int rows_per_cta;       // low-res rows per CTA (grid-y covers h / rows_per_cta)
 };
 
-// One thread per low-res pixel.  SUB = 0: nearest, top-left sample (R3).
-// SUB = 1: mean of the clipped s x s block (R4), summed in fp64.
-// grid (ceil(w/256), h, planes).
-template <int SUB>
-__global__ void __launch_bounds__(256) subsample_kernel(SubParams P) {
+// R4: mean of the clipped s x s block, summed in fp64.  One thread per
+// low-res column, several low-res rows per CTA for memory-level parallelism.
+// grid (ceil(w/256), ceil(h/rows_per_cta), planes).
+template <bool VEC4>
+__global__ void __launch_bounds__(256) subsample_block_kernel(SubParams P) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
     if (x >= P.w) return;
     const size_t plane = blockIdx.z;
     const float* src = P.src + plane * (size_t)P.H * P.W;
-    float out;
-    if (SUB == 0) {
-        out = __ldg(src + (size_t)y * P.s * P.W + (size_t)x * P.s);
-    } else {
+    float* dst = P.dst + plane * (size_t)P.h * P.w;
+    const int y0 = blockIdx.y * P.rows_per_cta;
+    const int y1 = min(P.h, y0 + P.rows_per_cta);
+    const int xa = x * P.s, xb = min(P.W, xa + P.s);
+    for (int y = y0; y < y1; ++y) {
         const int ya = y * P.s, yb = min(P.H, ya + P.s);
-        const int xa = x * P.s, xb = min(P.W, xa + P.s);
         double acc = 0.0;
-        for (int yy = ya; yy < yb; ++yy) {
-            const float* row = src + (size_t)yy * P.W;
-            for (int xx = xa; xx < xb; ++xx) acc += (double)__ldg(row + xx);
+        if (VEC4) {  // s == 4, W % 4 == 0, 16-byte aligned rows
+            for (int yy = ya; yy < yb; ++yy) {
+                const float4 v = __ldcs(reinterpret_cast<const float4*>(src + (size_t)yy * P.W) + x);
+                acc += (double)v.x;
+                acc += (double)v.y;
+                acc += (double)v.z;
+                acc += (double)v.w;
+            }
+        } else {
+            for (int yy = ya; yy < yb; ++yy) {
+                const float* row = src + (size_t)yy * P.W;
+                for (int xx = xa; xx < xb; ++xx) acc += (double)__ldcs(row + xx);
+            }
         }
-        out = (float)(acc / (double)((yb - ya) * (xb - xa)));
+        dst[(size_t)y * P.w + x] = (float)(acc / (double)((yb - ya) * (xb - xa)));
     }
-    P.dst[plane * (size_t)P.h * P.w + (size_t)y * P.w + x] = out;
-}
-
-// Block mean specialised for s = 4 with 16-byte aligned rows: one float4 per block row.
-__global__ void __launch_bounds__(256) subsample_block4_kernel(SubParams P) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int y = blockIdx.y;
-    if (x >= P.w) return;
-    const size_t plane = blockIdx.z;
-    const float* src = P.src + plane * (size_t)P.H * P.W;
-    const int ya = y * 4, yb = min(P.H, ya + 4);
-    double acc = 0.0;
-    for (int yy = ya; yy < yb; ++yy) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(src + (size_t)yy * P.W) + x);
-        acc += (double)v.x;
-        acc += (double)v.y;
-        acc += (double)v.z;
-        acc += (double)v.w;
-    }
-    P.dst[plane * (size_t)P.h * P.w + (size_t)y * P.w + x] =
-        (float)(acc / (double)((yb - ya) * 4));
 }
 
 // ------------------------------------------------------------------ K1 / K3: strip box filter
@@ -93,6 +88,7 @@ template <int CP>
 struct StripTraits<MODE_STATS, 1, CP> {
     static constexpr int NIN = 1 + CP;
     static constexpr int NMAP = 2 + 2 * CP;
+    static constexpr int NOUT = 2 * CP;
     __device__ static void products(const float* v, double* pr) {
         const double I = (double)v[0];
         pr[0] = I;
@@ -112,6 +108,7 @@ template <int CP>
 struct StripTraits<MODE_STATS, 3, CP> {
     static constexpr int NIN = 3 + CP;
     static constexpr int NMAP = 9 + 4 * CP;
+    static constexpr int NOUT = 4 * CP;
     __device__ static void products(const float* v, double* pr) {
         const double I0 = v[0], I1 = v[1], I2 = v[2];
         pr[0] = I0; pr[1] = I1; pr[2] = I2;
@@ -133,6 +130,7 @@ template <int CI, int CP>
 struct StripTraits<MODE_MEAN, CI, CP> {
     static constexpr int NIN = (CI + 1) * CP;
     static constexpr int NMAP = NIN;
+    static constexpr int NOUT = NIN;
     __device__ static void products(const float* v, double* pr) {
 #pragma unroll
         for (int m = 0; m < NMAP; ++m) pr[m] = (double)v[m];
@@ -140,37 +138,44 @@ struct StripTraits<MODE_MEAN, CI, CP> {
 };
 
 struct StripParams {
-    const float* srcI;      // STATS: I' planes [img][CI][h][w]; MEAN: coef maps [img][NC][h][w]
-    const float* srcP;      // STATS: p' planes [img][CP][h][w]; MEAN: unused
-    float* dst;             // STATS: a, b maps; MEAN: mean maps; both [img][(CI+1)CP][h][w]
-    long long strideI;      // elements between images in srcI
-    long long strideP;      // elements between images in srcP
+    // Input sample (y, x) of plane j of image b is at src[b*img + j*plane + y*row + x*col].
+    // STATS: srcI = I (or I' planes), srcP = p (or p' planes); MEAN: srcI = coefficient maps.
+    const float* srcI;
+    const float* srcP;
+    long long imgI, planeI, imgP, planeP;
+    long long row, col;     // row pitch and column stride of a sample (s*W and s for nearest)
+    float* dst;             // [img][(CI+1)CP][h][w]
     int h, w, R;            // low-res dims and radius r'
     int TW, TH;             // output columns per strip, output rows per segment
-    int K;                  // odd horizontal run length (bank-conflict-free sliding)
+    int K;                  // odd horizontal run length
     double eps;
 };
 
-// Rows-per-batch G and shared-memory need.
+// Rows-per-batch G and shared-memory layout.
 template <int MODE, int CI, int CP, int NT>
 struct StripConfig {
-    static constexpr int NMAP = StripTraits<MODE, CI, CP>::NMAP;
+    using T = StripTraits<MODE, CI, CP>;
+    static constexpr int NMAP = T::NMAP;
+    static constexpr int NOUT = T::NOUT;
     static constexpr int NW = NT / 32;
-    static constexpr int BYTES_PER_ROW = NMAP * NT * 8;
-    static constexpr int G0 = (100 * 1024) / BYTES_PER_ROW;
-    static constexpr int G = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
-    static constexpr int GG = G > NW ? NW : G;
-    static constexpr int WPR = NW / GG;                    // warps per row
-    static constexpr size_t SMEM = (size_t)GG * BYTES_PER_ROW;
+    static constexpr int V_ROW = NMAP * NT * 8;                 // fp64 column sums, one row
+    static constexpr int O_ROW = NOUT * NT * 4;                 // fp32 staged outputs, one row
+    static constexpr int G0 = (64 * 1024) / (V_ROW + O_ROW);
+    static constexpr int G1 = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
+    static constexpr int G = G1 > NW ? NW : G1;
+    static constexpr int WPR = NW / G;                           // warps per row
+    static constexpr size_t SMEM = (size_t)G * (V_ROW + O_ROW) + (size_t)NT * 8;
+    static constexpr int WB = T::NIN <= 2 ? 16 : (T::NIN <= 4 ? 8 : (T::NIN <= 8 ? 4 : 2));
 };
 
-// Epilogue of step 3-4 for gray guidance: a = cov/(max(var,0)+eps), b = mean_p - a mean_I.
+// Epilogue of steps 3-4; writes NOUT values at dst[m * ostride].
 template <int MODE, int CI, int CP>
 struct StripEpilogue;
 
+// Gray: a = cov/(max(var,0)+eps), b = mean_p - a mean_I (Eq.2-3, R8).
 template <int CP>
 struct StripEpilogue<MODE_STATS, 1, CP> {
-    __device__ static void emit(const double* S, double inv, double eps, float* dst, size_t n) {
+    __device__ static void emit(const double* S, double inv, double eps, float* dst, int ostride) {
         const double mI = S[0] * inv;
         double var = S[1] * inv - mI * mI;           // var_I
         var = var < 0.0 ? 0.0 : var;                 // R8
@@ -181,17 +186,17 @@ struct StripEpilogue<MODE_STATS, 1, CP> {
             const double cov = S[2 + CP + c] * inv - mI * mp;  // cov_Ip
             const double a = cov / den;                         // Eq.2 / P:80
             const double b = mp - a * mI;                       // Eq.3 / P:81
-            dst[(size_t)(2 * c) * n] = (float)a;
-            dst[(size_t)(2 * c + 1) * n] = (float)b;
+            dst[(2 * c) * ostride] = (float)a;
+            dst[(2 * c + 1) * ostride] = (float)b;
         }
     }
 };
 
-// Color guidance (R9): a_c = (Sigma + eps U)^-1 v_c with the closed-form symmetric
-// adjugate, v_c = corr_Ip_c - mu p_bar_c, b_c = p_bar_c - a_c^T mu; all fp64.
+// Color (R9): a_c = (Sigma + eps U)^-1 v_c by the closed-form symmetric adjugate,
+// v_c = corr_Ip_c - mu p_bar_c, b_c = p_bar_c - a_c^T mu; all fp64.
 template <int CP>
 struct StripEpilogue<MODE_STATS, 3, CP> {
-    __device__ static void emit(const double* S, double inv, double eps, float* dst, size_t n) {
+    __device__ static void emit(const double* S, double inv, double eps, float* dst, int ostride) {
         const double m0 = S[0] * inv, m1 = S[1] * inv, m2 = S[2] * inv;
         const double s00 = S[3] * inv - m0 * m0 + eps;
         const double s01 = S[4] * inv - m0 * m1;
@@ -216,49 +221,52 @@ struct StripEpilogue<MODE_STATS, 3, CP> {
             const double a1 = (c01 * v0 + c11 * v1 + c12 * v2) * idet;
             const double a2 = (c02 * v0 + c12 * v1 + c22 * v2) * idet;
             const double b = mp - (a0 * m0 + a1 * m1 + a2 * m2);
-            float* d = dst + (size_t)(4 * c) * n;
+            float* d = dst + (4 * c) * ostride;
             d[0] = (float)a0;
-            d[n] = (float)a1;
-            d[2 * n] = (float)a2;
-            d[3 * n] = (float)b;
+            d[ostride] = (float)a1;
+            d[2 * ostride] = (float)a2;
+            d[3 * ostride] = (float)b;
         }
     }
 };
 
 template <int CI, int CP>
 struct StripEpilogue<MODE_MEAN, CI, CP> {
-    __device__ static void emit(const double* S, double inv, double, float* dst, size_t n) {
+    __device__ static void emit(const double* S, double inv, double, float* dst, int ostride) {
 #pragma unroll
-        for (int m = 0; m < (CI + 1) * CP; ++m) dst[(size_t)m * n] = (float)(S[m] * inv);
+        for (int m = 0; m < (CI + 1) * CP; ++m) dst[m * ostride] = (float)(S[m] * inv);
     }
 };
 
 template <int MODE, int CI, int CP>
-__device__ __forceinline__ void load_inputs(const StripParams& P, const float* bI, const float* bP,
-                                            size_t n, int y, float* v) {
+__device__ __forceinline__ void load_row(const StripParams& P, const float* bI, const float* bP,
+                                         int y, float* v) {
     using T = StripTraits<MODE, CI, CP>;
-    const size_t off = (size_t)y * P.w;
+    const long long off = (long long)y * P.row;
     if (MODE == MODE_STATS) {
 #pragma unroll
-        for (int j = 0; j < CI; ++j) v[j] = __ldg(bI + j * n + off);
+        for (int j = 0; j < CI; ++j) v[j] = __ldg(bI + j * P.planeI + off);
 #pragma unroll
-        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(bP + c * n + off);
+        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(bP + c * P.planeP + off);
     } else {
 #pragma unroll
-        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(bI + m * n + off);
+        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(bI + m * P.planeI + off);
     }
 }
 
-// grid (strips, segments, images); block NT.  Strip b covers output columns
-// [b*TW, b*TW+TW) and reads the halo columns [x0-R, x0+TW+R) clipped to the image.
+// grid (strips, segments, images); block NT.
 template <int MODE, int CI, int CP, int NT>
 __global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
     using T = StripTraits<MODE, CI, CP>;
     using C = StripConfig<MODE, CI, CP, NT>;
     constexpr int NMAP = T::NMAP;
     constexpr int NIN = T::NIN;
-    constexpr int G = C::GG;
-    extern __shared__ double Vs[];  // [G][NMAP][NT] column sums of the batch's rows
+    constexpr int NOUT = T::NOUT;
+    constexpr int G = C::G;
+    extern __shared__ double smem_d[];
+    double* Vs = smem_d;                                               // [G][NMAP][NT]
+    float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * NT);   // [G][NOUT][NT]
+    double* invx = reinterpret_cast<double*>(Os + (size_t)G * NOUT * NT);  // [NT]
 
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
@@ -270,27 +278,35 @@ __global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
     const int ye = min(h, y0 + P.TH);
     const int xs0 = max(0, x0 - R);
     const int ncol = min(w, xe + R) - xs0;
+    const int ocn = xe - x0;                 // output columns of this strip
+    const int cbase = x0 - xs0;              // local column of output column 0
     const bool colthr = tid < ncol;
     const int gx = xs0 + (colthr ? tid : 0);
 
-    const float* bI = P.srcI + (size_t)img * P.strideI + gx;
-    const float* bP = (MODE == MODE_STATS) ? P.srcP + (size_t)img * P.strideP + gx : nullptr;
-    float* dst = P.dst + (size_t)img * (size_t)(CI + 1) * CP * n;
+    const float* bI = P.srcI + img * P.imgI + gx * P.col;
+    const float* bP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP + gx * P.col : nullptr;
+    float* dst = P.dst + (size_t)img * NOUT * n;
 
-    // Running vertical window sums of this thread's column, fp64 (N1).
+    // 1 / (horizontal in-bounds count) per output column (R1).
+    if (tid < ocn) {
+        const int c = cbase + tid;
+        invx[tid] = 1.0 / (double)(min(ncol - 1, c + R) - max(0, c - R) + 1);
+    }
+
+    // Running vertical window sums of this thread's column (fp64).
     double acc[NMAP];
 #pragma unroll
     for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
 
-    // Warm-up: the window of "row y0-1", rows [y0-R-1, y0+R-1] clipped; loads batched for MLP.
+    // Warm-up: the window of "row y0-1", rows [y0-R-1, y0+R-1] clipped; WB rows per round.
     if (colthr) {
-        constexpr int WB = NIN <= 4 ? 8 : (NIN <= 8 ? 4 : 2);
+        constexpr int WB = C::WB;
         const int wa = max(0, y0 - R - 1), wb = min(h - 1, y0 + R - 1);
         for (int y = wa; y <= wb; y += WB) {
             float v[WB][NIN];
 #pragma unroll
             for (int k = 0; k < WB; ++k)
-                if (y + k <= wb) load_inputs<MODE, CI, CP>(P, bI, bP, n, y + k, v[k]);
+                if (y + k <= wb) load_row<MODE, CI, CP>(P, bI, bP, y + k, v[k]);
 #pragma unroll
             for (int k = 0; k < WB; ++k) {
                 if (y + k <= wb) {
@@ -303,28 +319,32 @@ __global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
         }
     }
 
-    // Horizontal-phase mapping: each warp owns one of the G rows of a batch; the WPR warps
-    // of a row split it into 32*WPR runs of K (odd) consecutive output columns, so the 16
-    // lanes of a half-warp hit 16 distinct fp64 banks.
+    // Horizontal-phase mapping: warp -> row hg of the batch; the WPR warps of a row split it
+    // into 32*WPR runs of K consecutive output columns.
     const int warp = tid >> 5, lane = tid & 31;
     const int hg = warp % G;
     const int run = (warp / G) * 32 + lane;
-    const int oc0 = run * P.K;               // first output column (local) of the run
-    const int ocn = xe - x0;                 // output columns in this strip
-    const int cbase = x0 - xs0;              // local column of output column 0
+    const int oc0 = run * P.K;
 
-    for (int yb = y0; yb < ye; yb += G) {
-        // ---- column phase: slide the vertical windows of G rows, snapshot to smem.
-        if (colthr) {
-            float va[G][NIN], vs[G][NIN];
+    // Software pipeline: va/vs hold the add/subtract rows of the current batch.
+    float va[G][NIN], vs[G][NIN];
+    auto load_batch = [&](int yb) {
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const int yo = yb + g;
-                if (yo < ye) {
-                    if (yo + R < h) load_inputs<MODE, CI, CP>(P, bI, bP, n, yo + R, va[g]);
-                    if (yo - R - 1 >= 0) load_inputs<MODE, CI, CP>(P, bI, bP, n, yo - R - 1, vs[g]);
-                }
+        for (int g = 0; g < G; ++g) {
+            const int yo = yb + g;
+            if (yo < ye) {
+                if (yo + R < h) load_row<MODE, CI, CP>(P, bI, bP, yo + R, va[g]);
+                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(P, bI, bP, yo - R - 1, vs[g]);
             }
+        }
+    };
+    if (colthr) load_batch(y0);
+
+    int prev_rows = 0;       // rows staged in Os by the previous batch, not yet stored
+    int prev_yb = 0;
+    for (int yb = y0; yb < ye; yb += G) {
+        // ---- column phase: slide the vertical windows of the batch's rows, snapshot.
+        if (colthr) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const int yo = yb + g;
@@ -340,19 +360,30 @@ __global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
 #pragma unroll
                         for (int m = 0; m < NMAP; ++m) acc[m] -= pr[m];
                     }
-                    double* row = Vs + (size_t)g * NMAP * NT;
+                    double* vrow = Vs + (size_t)g * NMAP * NT;
 #pragma unroll
-                    for (int m = 0; m < NMAP; ++m) row[m * NT + tid] = acc[m];
+                    for (int m = 0; m < NMAP; ++m) vrow[m * NT + tid] = acc[m];
                 }
             }
         }
+        // ---- coalesced store of the previous batch's staged outputs.
+        for (int idx = tid; idx < prev_rows * NOUT * ocn; idx += NT) {
+            const int oc = idx % ocn;
+            const int gm = idx / ocn;
+            const int m = gm % NOUT, g = gm / NOUT;
+            dst[(size_t)m * n + (size_t)(prev_yb + g) * w + x0 + oc] =
+                Os[((size_t)g * NOUT + m) * NT + oc];
+        }
         __syncthreads();
+
+        // ---- prefetch the next batch (in flight during the horizontal phase).
+        if (colthr && yb + G < ye) load_batch(yb + G);
 
         // ---- horizontal phase: sliding window along each snapshotted row.
         const int yo = yb + hg;
         if (yo < ye && oc0 < ocn) {
-            const double* row = Vs + (size_t)hg * NMAP * NT;
-            const int cy = min(h - 1, yo + R) - max(0, yo - R) + 1;
+            const double* vrow = Vs + (size_t)hg * NMAP * NT;
+            const double invy = 1.0 / (double)(min(h - 1, yo + R) - max(0, yo - R) + 1);
             int c = cbase + oc0;
             const int lo = max(0, c - R), hi = min(ncol - 1, c + R);
             double S[NMAP];
@@ -360,28 +391,34 @@ __global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
             for (int m = 0; m < NMAP; ++m) S[m] = 0.0;
             for (int k = lo; k <= hi; ++k) {
 #pragma unroll
-                for (int m = 0; m < NMAP; ++m) S[m] += row[m * NT + k];
+                for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + k];
             }
-            float* drow = dst + (size_t)yo * w + x0;
+            float* orow = Os + (size_t)hg * NOUT * NT;
             const int oce = min(ocn, oc0 + P.K);
             for (int oc = oc0; oc < oce; ++oc, ++c) {
-                const int cx = min(ncol - 1, c + R) - max(0, c - R) + 1;
-                const double inv = 1.0 / ((double)cx * (double)cy);
-                StripEpilogue<MODE, CI, CP>::emit(S, inv, P.eps, drow + oc, n);
+                StripEpilogue<MODE, CI, CP>::emit(S, invx[oc] * invy, P.eps, orow + oc, NT);
                 if (oc + 1 < oce) {
                     const int ca = c + R + 1, cs = c - R;
                     if (ca < ncol) {
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) S[m] += row[m * NT + ca];
+                        for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + ca];
                     }
                     if (cs >= 0) {
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) S[m] -= row[m * NT + cs];
+                        for (int m = 0; m < NMAP; ++m) S[m] -= vrow[m * NT + cs];
                     }
                 }
             }
         }
+        prev_rows = min(G, ye - yb);
+        prev_yb = yb;
         __syncthreads();
+    }
+    for (int idx = tid; idx < prev_rows * NOUT * ocn; idx += NT) {
+        const int oc = idx % ocn;
+        const int gm = idx / ocn;
+        const int m = gm % NOUT, g = gm / NOUT;
+        dst[(size_t)m * n + (size_t)(prev_yb + g) * w + x0 + oc] = Os[((size_t)g * NOUT + m) * NT + oc];
     }
 }
 
@@ -393,7 +430,7 @@ struct OutParams {
     float* q;              // [img][CP][H][W]
     int H, W, h, w;
     int TR, TC;            // full-res tile rows / cols
-    int nrl;               // max low-res rows any tile touches (smem sizing)
+    int nrl, ncl;          // max low-res rows / cols any tile touches (smem sizing)
 };
 
 // R5: source coordinate of destination index d, resize n_src -> n_dst, exactly in
@@ -421,20 +458,22 @@ __device__ __forceinline__ void src_coord(int d, int n_src, int n_dst, int& i0, 
 template <int CI, int CP>
 struct OutConfig {
     static constexpr int NC = (CI + 1) * CP;                 // coefficient maps
-    static constexpr int U = (CI == 1) ? 8 : 4;              // rows in flight per thread
+    static constexpr int U = (CI == 1) ? 4 : 2;              // rows per thread per batch
 };
 
 // grid (ceil(W/TC), ceil(H/TR), images), block 256.
-// smem: Hx[nrl][NC][TC] (horizontally interpolated low-res rows) + row table [TR].
+// smem: Hx[nrl][NC][TC] (horizontally interpolated low-res rows), Mraw[nrl][NC][ncl],
+//       row table [TR].
 template <int CI, int CP, bool VEC>
-__global__ void __launch_bounds__(256) output_kernel(OutParams P) {
+__global__ void __launch_bounds__(256, (CI == 1 ? 4 : 2)) output_kernel(OutParams P) {
     constexpr int NT = 256;
     constexpr int NC = OutConfig<CI, CP>::NC;
     constexpr int U = OutConfig<CI, CP>::U;
     extern __shared__ float smem[];
     const int TC = P.TC, TR = P.TR;
-    float* Hx = smem;                                          // [nrl][NC][TC]
-    int* rt0 = reinterpret_cast<int*>(Hx + (size_t)P.nrl * NC * TC);
+    float* Hx = smem;                                           // [nrl][NC][TC]
+    float* Mr = Hx + (size_t)P.nrl * NC * TC;                    // [nrl][NC][ncl]
+    int* rt0 = reinterpret_cast<int*>(Mr + (size_t)P.nrl * NC * P.ncl);
     int* rt1 = rt0 + TR;
     float* rfy = reinterpret_cast<float*>(rt1 + TR);
 
@@ -444,12 +483,41 @@ __global__ void __launch_bounds__(256) output_kernel(OutParams P) {
     const int H = P.H, W = P.W, h = P.h, w = P.w;
     const size_t N = (size_t)H * W, n = (size_t)h * w;
     const int nrows = min(TR, H - Y0), ncols = min(TC, W - X0);
+    const float* Iimg = P.I + (size_t)img * CI * N;
+    float* qimg = P.q + (size_t)img * CP * N;
 
-    int ylo, ydummy;
-    float fdummy;
-    src_coord(Y0, h, H, ylo, ydummy, fdummy);
+    // VEC: thread streams float4 column c4 of rows ro, ro + rpp, ... ; U rows per batch.
+    const int tpr = TC >> 2;
+    const int rpp = NT / tpr;
+    const int c4 = tid % tpr, ro = tid / tpr;
+    const int xi = c4 * 4;
+    const bool vact = VEC && xi < ncols;
+    const size_t colo = (size_t)(X0 + xi);
+    const int rstep = rpp * U;
+    float4 cur[U][CI];
+    auto load_batch = [&](int rb, float4 (&buf)[U][CI]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = rb + u * rpp;
+            if (t < nrows) {
+                const size_t off = (size_t)(Y0 + t) * W + colo;
+#pragma unroll
+                for (int j = 0; j < CI; ++j)
+                    buf[u][j] = __ldcs(reinterpret_cast<const float4*>(Iimg + j * N + off));
+            }
+        }
+    };
+    // Issue the first batch of full-resolution loads before the prologue.
+    if (vact) load_batch(ro, cur);
 
-    // Row table: low-res rows (relative to ylo) and vertical weight of each tile row.
+    // Prologue 1: row table and raw low-res rows/cols the tile touches.
+    int ylo, yd, xlo, xd, yhi, xhi;
+    float fd;
+    src_coord(Y0, h, H, ylo, yd, fd);
+    src_coord(Y0 + nrows - 1, h, H, yd, yhi, fd);
+    src_coord(X0, w, W, xlo, xd, fd);
+    src_coord(X0 + ncols - 1, w, W, xd, xhi, fd);
+    const int nrl = yhi - ylo + 1, ncl = xhi - xlo + 1;
     for (int t = tid; t < nrows; t += NT) {
         int a, b;
         float f;
@@ -458,95 +526,84 @@ __global__ void __launch_bounds__(256) output_kernel(OutParams P) {
         rt1[t] = b - ylo;
         rfy[t] = f;
     }
-    int yhi_a, yhi;
-    src_coord(Y0 + nrows - 1, h, H, yhi_a, yhi, fdummy);
-    const int nrl = yhi - ylo + 1;
-
-    // Hx: horizontal bilinear pass of the nrl low-res rows over the tile's columns.
     const float* Mimg = P.M + (size_t)img * NC * n;
-    for (int xi = tid; xi < ncols; xi += NT) {
+    for (int idx = tid; idx < nrl * NC * ncl; idx += NT) {
+        const int xx = idx % ncl, rm = idx / ncl;
+        const int m = rm % NC, rr = rm / NC;
+        Mr[idx] = __ldg(Mimg + (size_t)m * n + (size_t)(ylo + rr) * w + xlo + xx);
+    }
+    __syncthreads();
+
+    // Prologue 2: Hx = horizontal bilinear pass of the nrl low-res rows over the tile.
+    for (int x = tid; x < ncols; x += NT) {
         int xa, xb;
         float fx;
-        src_coord(X0 + xi, w, W, xa, xb, fx);
+        src_coord(X0 + x, w, W, xa, xb, fx);
+        xa -= xlo;
+        xb -= xlo;
         for (int rr = 0; rr < nrl; ++rr) {
-            const float* mrow = Mimg + (size_t)(ylo + rr) * w;
 #pragma unroll
             for (int m = 0; m < NC; ++m) {
-                const float va = __ldg(mrow + m * n + xa);
-                const float vb = __ldg(mrow + m * n + xb);
-                Hx[((size_t)rr * NC + m) * TC + xi] = fmaf(fx, vb - va, va);
+                const float* mr = Mr + ((size_t)rr * NC + m) * ncl;
+                const float va = mr[xa], vb = mr[xb];
+                Hx[((size_t)rr * NC + m) * TC + x] = fmaf(fx, vb - va, va);
             }
         }
     }
     __syncthreads();
 
-    const float* Iimg = P.I + (size_t)img * CI * N;
-    float* qimg = P.q + (size_t)img * CP * N;
-
     if (VEC) {
-        // Each thread streams float4 columns; U independent rows of loads in flight.
-        const int tpr = TC >> 2;               // threads per row
-        const int rpp = NT / tpr;              // rows per pass
-        const int c4 = tid % tpr, ro = tid / tpr;
-        const int xi = c4 * 4;
-        if (xi < ncols) {
-            const size_t colo = (size_t)(X0 + xi);
-            for (int rb = ro; rb < nrows; rb += rpp * U) {
-                float4 iv[U][CI];
+        if (!vact) return;
+        for (int rb = ro; rb < nrows; rb += rstep) {
+            float4 nxt[U][CI];
+            if (rb + rstep < nrows) load_batch(rb + rstep, nxt);
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = rb + u * rpp;
-                    if (t < nrows) {
-                        const size_t off = (size_t)(Y0 + t) * W + colo;
+            for (int u = 0; u < U; ++u) {
+                const int t = rb + u * rpp;
+                if (t < nrows) {
+                    const float fy = rfy[t];
+                    const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
+                    const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
+                    float4 A[NC];
 #pragma unroll
-                        for (int j = 0; j < CI; ++j)
-                            iv[u][j] = __ldcs(reinterpret_cast<const float4*>(Iimg + j * N + off));
+                    for (int m = 0; m < NC; ++m) {
+                        const float4 a0 = *reinterpret_cast<const float4*>(h0 + m * TC);
+                        const float4 a1 = *reinterpret_cast<const float4*>(h1 + m * TC);
+                        A[m].x = fmaf(fy, a1.x - a0.x, a0.x);
+                        A[m].y = fmaf(fy, a1.y - a0.y, a0.y);
+                        A[m].z = fmaf(fy, a1.z - a0.z, a0.z);
+                        A[m].w = fmaf(fy, a1.w - a0.w, a0.w);
                     }
-                }
+                    const size_t off = (size_t)(Y0 + t) * W + colo;
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = rb + u * rpp;
-                    if (t < nrows) {
-                        const float fy = rfy[t];
-                        const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
-                        const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
-                        float4 A[NC];
+                    for (int c = 0; c < CP; ++c) {
+                        float4 o = A[c * (CI + 1) + CI];
 #pragma unroll
-                        for (int m = 0; m < NC; ++m) {
-                            const float4 a0 = *reinterpret_cast<const float4*>(h0 + m * TC);
-                            const float4 a1 = *reinterpret_cast<const float4*>(h1 + m * TC);
-                            A[m].x = fmaf(fy, a1.x - a0.x, a0.x);
-                            A[m].y = fmaf(fy, a1.y - a0.y, a0.y);
-                            A[m].z = fmaf(fy, a1.z - a0.z, a0.z);
-                            A[m].w = fmaf(fy, a1.w - a0.w, a0.w);
+                        for (int j = 0; j < CI; ++j) {
+                            const float4 a = A[c * (CI + 1) + j];
+                            o.x = fmaf(a.x, cur[u][j].x, o.x);
+                            o.y = fmaf(a.y, cur[u][j].y, o.y);
+                            o.z = fmaf(a.z, cur[u][j].z, o.z);
+                            o.w = fmaf(a.w, cur[u][j].w, o.w);
                         }
-                        const size_t off = (size_t)(Y0 + t) * W + colo;
-#pragma unroll
-                        for (int c = 0; c < CP; ++c) {
-                            float4 o = A[c * (CI + 1) + CI];
-#pragma unroll
-                            for (int j = 0; j < CI; ++j) {
-                                const float4 a = A[c * (CI + 1) + j];
-                                o.x = fmaf(a.x, iv[u][j].x, o.x);
-                                o.y = fmaf(a.y, iv[u][j].y, o.y);
-                                o.z = fmaf(a.z, iv[u][j].z, o.z);
-                                o.w = fmaf(a.w, iv[u][j].w, o.w);
-                            }
-                            __stcs(reinterpret_cast<float4*>(qimg + c * N + off), o);
-                        }
+                        __stcs(reinterpret_cast<float4*>(qimg + c * N + off), o);
                     }
                 }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int j = 0; j < CI; ++j) cur[u][j] = nxt[u][j];
         }
     } else {
         // Scalar path (W % 4 != 0 or unaligned buffers): one pixel per thread-iteration.
         for (int idx = tid; idx < nrows * TC; idx += NT) {
-            const int t = idx / TC, xi = idx % TC;
-            if (xi >= ncols) continue;
+            const int t = idx / TC, x = idx % TC;
+            if (x >= ncols) continue;
             const float fy = rfy[t];
-            const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
-            const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
-            const size_t off = (size_t)(Y0 + t) * W + X0 + xi;
+            const float* h0 = Hx + (size_t)rt0[t] * NC * TC + x;
+            const float* h1 = Hx + (size_t)rt1[t] * NC * TC + x;
+            const size_t off = (size_t)(Y0 + t) * W + X0 + x;
             float iv[CI];
 #pragma unroll
             for (int j = 0; j < CI; ++j) iv[j] = __ldcs(Iimg + j * N + off);
