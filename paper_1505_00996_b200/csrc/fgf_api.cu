@@ -172,7 +172,7 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     if (!ok && P.out_smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
 
     // Chunk of images per pipeline stage: the low-res workspace of one slot ~ kChunkTargetBytes.
-    const bool planes = s > 1 && sub == FGF_SUB_BILINEAR;
+    const bool planes = s > 1;
     const size_t per_img = (size_t)((planes ? CI + CP : 0) + 2 * P.NC) * P.n * sizeof(float);
     size_t target = kChunkTargetBytes;
     if (const char* e = getenv("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
@@ -230,13 +230,15 @@ void set_smem(K kernel, size_t bytes) {
 
 int last_error() { return cudaGetLastError() == cudaSuccess ? FGF_OK : FGF_ERR_CUDA; }
 
-// K0 (block-mean subsampling only).
+// K0: step 1 into compact low-res planes.
 int launch_subsample(const float* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
     SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s, 8};
     dim3 grid((P.w + 255) / 256, (P.h + sp.rows_per_cta - 1) / sp.rows_per_cta, planes);
     ProfScope ps(KIND_SUB, st);
     const bool vec4 = P.s == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (P.W % 4) == 0;
-    if (vec4)
+    if (P.sub == FGF_SUB_NEAREST)
+        subsample_nearest_kernel<8><<<grid, 256, 0, st>>>(sp);
+    else if (vec4)
         subsample_block_kernel<true><<<grid, 256, 0, st>>>(sp);
     else
         subsample_block_kernel<false><<<grid, 256, 0, st>>>(sp);
@@ -256,7 +258,7 @@ int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream
     const long long want = 4LL * 148;
     const long long strips_imgs = (long long)P.strips * images;
     long long th = (P.h * strips_imgs + want - 1) / want;
-    th = std::max<long long>(th, std::max(2 * C::G, 2 * P.R / 3));
+    th = std::max<long long>(th, std::max(4 * C::G, 2 * P.R));
     int TH = (int)std::min<long long>(64, th);
     TH = (TH + C::G - 1) / C::G * C::G;
     sp.TH = TH;
@@ -337,8 +339,8 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
     int rc;
 
     StripParams sp{};
-    if (P.s > 1 && P.sub == FGF_SUB_BILINEAR) {
-        // Step 1 as its own pass (R4 block mean) into compact low-res planes.
+    if (P.s > 1) {
+        // Step 1 as its own pass (R3 nearest / R4 block mean) into compact low-res planes.
         float* Is = planes;
         float* ps = planes + (size_t)nb * P.CI * P.n;
         if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
@@ -348,10 +350,10 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
         sp.srcP = ps; sp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; sp.planeP = (long long)P.n;
         sp.row = P.w; sp.col = 1;
     } else {
-        // Step 1 fused (R3 nearest, or s = 1): K1 reads I[y*s][x*s] from the full image.
+        // s = 1: I' = I, p' = p; K1 reads the images directly.
         sp.srcI = Ib; sp.imgI = (long long)P.CI * P.N; sp.planeI = (long long)P.N;
         sp.srcP = pb; sp.imgP = (long long)P.CP * P.N; sp.planeP = (long long)P.N;
-        sp.row = (long long)P.s * P.W; sp.col = P.s;
+        sp.row = P.W; sp.col = 1;
     }
     sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
 

@@ -77,6 +77,27 @@ __global__ void __launch_bounds__(256) subsample_block_kernel(SubParams P) {
     }
 }
 
+// R3: nearest = top-left sample I[y*s][x*s], compacted into low-res planes so
+// that the box engine's repeated row reads (warm-up, subtracted rows) touch 4 bytes per
+// sample instead of a 32-byte sector.  RPC rows per thread, loads issued before stores.
+// grid (ceil(w/256), ceil(h/RPC), planes).
+template <int RPC>
+__global__ void __launch_bounds__(256) subsample_nearest_kernel(SubParams P) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= P.w) return;
+    const size_t plane = blockIdx.z;
+    const float* src = P.src + plane * (size_t)P.H * P.W + (size_t)x * P.s;
+    float* dst = P.dst + plane * (size_t)P.h * P.w + x;
+    const int y0 = blockIdx.y * RPC;
+    float v[RPC];
+#pragma unroll
+    for (int k = 0; k < RPC; ++k)
+        if (y0 + k < P.h) v[k] = __ldg(src + (size_t)(y0 + k) * P.s * P.W);
+#pragma unroll
+    for (int k = 0; k < RPC; ++k)
+        if (y0 + k < P.h) dst[(size_t)(y0 + k) * P.w] = v[k];
+}
+
 // ------------------------------------------------------------------ K1 / K3: strip box filter
 
 template <int MODE, int CI, int CP>
@@ -165,7 +186,8 @@ struct StripConfig {
     static constexpr int G = G1 > NW ? NW : G1;
     static constexpr int WPR = NW / G;                           // warps per row
     static constexpr size_t SMEM = (size_t)G * (V_ROW + O_ROW) + (size_t)NT * 8;
-    static constexpr int WB = T::NIN <= 2 ? 16 : (T::NIN <= 4 ? 8 : (T::NIN <= 8 ? 4 : 2));
+    static constexpr int WB = T::NIN <= 4 ? 8 : (T::NIN <= 8 ? 4 : 2);
+    static constexpr int MINB = NT == 256 ? (NMAP <= 2 ? 4 : (NMAP <= 6 ? 3 : (NMAP <= 13 ? 2 : 1))) : 1;
 };
 
 // Epilogue of steps 3-4; writes NOUT values at dst[m * ostride].
@@ -184,9 +206,10 @@ struct StripEpilogue<MODE_STATS, 1, CP> {
         for (int c = 0; c < CP; ++c) {
             const double mp = S[2 + c] * inv;
             const double cov = S[2 + CP + c] * inv - mI * mp;  // cov_Ip
-            const double a = cov / den;                         // Eq.2 / P:80
-            const double b = mp - a * mI;                       // Eq.3 / P:81
-            dst[(2 * c) * ostride] = (float)a;
+            // Eq.2 / P:80: the cancellations above are fp64; the quotient only needs fp32.
+            const float a = __fdiv_rn((float)cov, (float)den);
+            const double b = mp - (double)a * mI;               // Eq.3 / P:81
+            dst[(2 * c) * ostride] = a;
             dst[(2 * c + 1) * ostride] = (float)b;
         }
     }
@@ -256,7 +279,7 @@ __device__ __forceinline__ void load_row(const StripParams& P, const float* bI, 
 
 // grid (strips, segments, images); block NT.
 template <int MODE, int CI, int CP, int NT>
-__global__ void __launch_bounds__(NT) box_strip_kernel(StripParams P) {
+__global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box_strip_kernel(StripParams P) {
     using T = StripTraits<MODE, CI, CP>;
     using C = StripConfig<MODE, CI, CP, NT>;
     constexpr int NMAP = T::NMAP;
