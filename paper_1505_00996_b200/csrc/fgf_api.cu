@@ -24,7 +24,6 @@ thread_local int g_last_launches = 0;
 
 constexpr size_t kAlign = 256;
 constexpr size_t kChunkTargetBytes = 16u << 20;  // low-res workspace bytes per pipeline slot
-constexpr int kOutSmemBudget = 50 * 1024;
 
 // ---- optional per-launch event timing (fgf_profile_*)
 enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, NKIND = 4 };
@@ -86,8 +85,7 @@ struct Plan {
     // strip box engine
     int nt, TW, strips;
     // output kernel
-    int TR, TC, nrl, ncl;
-    size_t out_smem;
+    int TR;
     // workspace carve-up per pipeline slot (bytes)
     size_t ws_planes, ws_coef, ws_mean, ws_slot;
     int nslots;
@@ -108,28 +106,6 @@ int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double ep
     if (s > 1 && (s >= H || s >= W)) return FGF_ERR_PARAM;  // S:246, R7
     if ((long long)H * W > (1LL << 40)) return FGF_ERR_SHAPE;
     return FGF_OK;
-}
-
-// Exact max over tiles of (last low-res index touched - first + 1) for a resize
-// n_src -> n_dst tiled by T destination samples (R5 coordinates).
-int max_lowres_span(int T, int n_dst, int n_src) {
-    auto lo = [&](int d) {
-        long long num = (long long)(2 * d + 1) * n_src - n_dst;
-        if (num <= 0) return 0;
-        long long q = num / (2LL * n_dst);
-        return (int)std::min<long long>(q, n_src - 1);
-    };
-    int best = 1;
-    for (int d0 = 0; d0 < n_dst; d0 += T) {
-        int dl = std::min(n_dst, d0 + T) - 1;
-        int a = lo(d0), b = std::min(lo(dl) + 1, n_src - 1);
-        best = std::max(best, b - a + 1);
-    }
-    return best;
-}
-
-size_t out_smem_bytes(int nrl, int ncl, int NC, int TR, int TC) {
-    return (size_t)nrl * NC * (TC + ncl) * sizeof(float) + (size_t)TR * 3 * sizeof(int);
 }
 
 int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
@@ -153,23 +129,8 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     else return FGF_ERR_UNSUPPORTED;
     P.strips = (P.w + P.TW - 1) / P.TW;
 
-    // Output tile: the first candidate whose staged maps fit the shared-memory budget.
-    static const int cand[][2] = {{64, 256}, {32, 256}, {16, 256}, {32, 128}, {16, 128},
-                                  {8, 256},  {8, 128},  {16, 64},  {8, 64},   {4, 64},
-                                  {2, 64},   {1, 64},   {1, 32}};
-    bool ok = false;
-    for (auto& c : cand) {
-        P.TR = c[0];
-        P.TC = c[1];
-        P.nrl = max_lowres_span(P.TR, H, P.h);
-        P.ncl = max_lowres_span(P.TC, W, P.w);
-        P.out_smem = out_smem_bytes(P.nrl, P.ncl, P.NC, P.TR, P.TC);
-        if (P.out_smem <= (size_t)kOutSmemBudget) {
-            ok = true;
-            break;
-        }
-    }
-    if (!ok && P.out_smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+    // Output pass: each thread walks TR full-resolution rows.
+    P.TR = 64;
 
     // Chunk of images per pipeline stage: the low-res workspace of one slot ~ kChunkTargetBytes.
     const bool planes = s > 1;
@@ -293,37 +254,39 @@ int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t 
     return FGF_ERR_SHAPE;
 }
 
-template <int CI, int CP>
-int launch_output_t(const OutParams& op, int images, const Plan& P, bool vec, cudaStream_t st) {
-    dim3 grid((P.W + P.TC - 1) / P.TC, (P.H + P.TR - 1) / P.TR, images);
+template <int CI, int CP, int PX>
+int launch_output_px(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
+    dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + P.TR - 1) / P.TR, images);
     ProfScope ps(KIND_OUT, st);
-    if (vec) {
-        auto kern = output_kernel<CI, CP, true>;
-        set_smem(kern, P.out_smem);
-        kern<<<grid, 256, P.out_smem, st>>>(op);
-    } else {
-        auto kern = output_kernel<CI, CP, false>;
-        set_smem(kern, P.out_smem);
-        kern<<<grid, 256, P.out_smem, st>>>(op);
-    }
+    output_kernel<CI, CP, PX><<<grid, 256, 0, st>>>(op);
     ++g_last_launches;
     return last_error();
 }
 
+// Pixels per thread: as wide as alignment allows while 3 NC PX coefficient registers <= 48.
+template <int CI, int CP>
+int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
+    constexpr int NC = (CI + 1) * CP;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
+    if (NC <= 4 && P.W % 4 == 0 && (al & 15u) == 0)
+        return launch_output_px<CI, CP, (NC <= 4 ? 4 : 1)>(op, images, P, st);
+    if (NC <= 8 && P.W % 2 == 0 && (al & 7u) == 0)
+        return launch_output_px<CI, CP, (NC <= 8 ? 2 : 1)>(op, images, P, st);
+    return launch_output_px<CI, CP, 1>(op, images, P, st);
+}
+
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
                   cudaStream_t st) {
-    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR, P.TC, P.nrl, P.ncl};
-    const bool vec = (P.W % 4 == 0) &&
-                     ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
+    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR};
     switch (P.CI * 10 + P.CP) {
-        case 11: return launch_output_t<1, 1>(op, images, P, vec, st);
-        case 12: return launch_output_t<1, 2>(op, images, P, vec, st);
-        case 13: return launch_output_t<1, 3>(op, images, P, vec, st);
-        case 14: return launch_output_t<1, 4>(op, images, P, vec, st);
-        case 31: return launch_output_t<3, 1>(op, images, P, vec, st);
-        case 32: return launch_output_t<3, 2>(op, images, P, vec, st);
-        case 33: return launch_output_t<3, 3>(op, images, P, vec, st);
-        case 34: return launch_output_t<3, 4>(op, images, P, vec, st);
+        case 11: return launch_output_t<1, 1>(op, images, P, st);
+        case 12: return launch_output_t<1, 2>(op, images, P, st);
+        case 13: return launch_output_t<1, 3>(op, images, P, st);
+        case 14: return launch_output_t<1, 4>(op, images, P, st);
+        case 31: return launch_output_t<3, 1>(op, images, P, st);
+        case 32: return launch_output_t<3, 2>(op, images, P, st);
+        case 33: return launch_output_t<3, 3>(op, images, P, st);
+        case 34: return launch_output_t<3, 4>(op, images, P, st);
     }
     return FGF_ERR_SHAPE;
 }

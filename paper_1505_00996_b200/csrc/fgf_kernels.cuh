@@ -181,7 +181,7 @@ struct StripConfig {
     static constexpr int NW = NT / 32;
     static constexpr int V_ROW = NMAP * NT * 8;                 // fp64 column sums, one row
     static constexpr int O_ROW = NOUT * NT * 4;                 // fp32 staged outputs, one row
-    static constexpr int G0 = (64 * 1024) / (V_ROW + O_ROW);
+    static constexpr int G0 = (82 * 1024) / (V_ROW + O_ROW);
     static constexpr int G1 = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
     static constexpr int G = G1 > NW ? NW : G1;
     static constexpr int WPR = NW / G;                           // warps per row
@@ -261,19 +261,19 @@ struct StripEpilogue<MODE_MEAN, CI, CP> {
     }
 };
 
+// Loads the NIN inputs of one row for this thread's column; `at` points at plane 0.
 template <int MODE, int CI, int CP>
-__device__ __forceinline__ void load_row(const StripParams& P, const float* bI, const float* bP,
-                                         int y, float* v) {
+__device__ __forceinline__ void load_row(const float* atI, const float* atP, long long planeI,
+                                         long long planeP, float* v) {
     using T = StripTraits<MODE, CI, CP>;
-    const long long off = (long long)y * P.row;
     if (MODE == MODE_STATS) {
 #pragma unroll
-        for (int j = 0; j < CI; ++j) v[j] = __ldg(bI + j * P.planeI + off);
+        for (int j = 0; j < CI; ++j) v[j] = __ldg(atI + j * planeI);
 #pragma unroll
-        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(bP + c * P.planeP + off);
+        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(atP + c * planeP);
     } else {
 #pragma unroll
-        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(bI + m * P.planeI + off);
+        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(atI + m * planeI);
     }
 }
 
@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     constexpr int NOUT = T::NOUT;
     constexpr int G = C::G;
     extern __shared__ double smem_d[];
-    double* Vs = smem_d;                                               // [G][NMAP][NT]
-    float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * NT);   // [G][NOUT][NT]
+    double* Vs = smem_d;                                                  // [G][NMAP][NT]
+    float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * NT);      // [G][NOUT][NT]
     double* invx = reinterpret_cast<double*>(Os + (size_t)G * NOUT * NT);  // [NT]
 
     const int tid = threadIdx.x;
@@ -305,10 +305,11 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     const int cbase = x0 - xs0;              // local column of output column 0
     const bool colthr = tid < ncol;
     const int gx = xs0 + (colthr ? tid : 0);
+    const long long row = P.row, planeI = P.planeI, planeP = P.planeP;
 
-    const float* bI = P.srcI + img * P.imgI + gx * P.col;
-    const float* bP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP + gx * P.col : nullptr;
-    float* dst = P.dst + (size_t)img * NOUT * n;
+    const float* cI = P.srcI + img * P.imgI + gx * P.col;   // this column, row 0, plane 0
+    const float* cP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP + gx * P.col : cI;
+    float* dst = P.dst + (size_t)img * NOUT * n + x0;
 
     // 1 / (horizontal in-bounds count) per output column (R1).
     if (tid < ocn) {
@@ -316,7 +317,8 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
         invx[tid] = 1.0 / (double)(min(ncol - 1, c + R) - max(0, c - R) + 1);
     }
 
-    // Running vertical window sums of this thread's column (fp64).
+    // Running vertical window sums of this thread's column (fp64; products of two floats are
+    // exact in fp64, and fma(x, y, acc) rounds once).
     double acc[NMAP];
 #pragma unroll
     for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
@@ -327,9 +329,10 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
         const int wa = max(0, y0 - R - 1), wb = min(h - 1, y0 + R - 1);
         for (int y = wa; y <= wb; y += WB) {
             float v[WB][NIN];
+            const long long off = (long long)y * row;
 #pragma unroll
             for (int k = 0; k < WB; ++k)
-                if (y + k <= wb) load_row<MODE, CI, CP>(P, bI, bP, y + k, v[k]);
+                if (y + k <= wb) load_row<MODE, CI, CP>(cI + off + k * row, cP + off + k * row, planeI, planeP, v[k]);
 #pragma unroll
             for (int k = 0; k < WB; ++k) {
                 if (y + k <= wb) {
@@ -352,12 +355,13 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     // Software pipeline: va/vs hold the add/subtract rows of the current batch.
     float va[G][NIN], vs[G][NIN];
     auto load_batch = [&](int yb) {
+        const long long oa = (long long)(yb + R) * row, os = (long long)(yb - R - 1) * row;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const int yo = yb + g;
             if (yo < ye) {
-                if (yo + R < h) load_row<MODE, CI, CP>(P, bI, bP, yo + R, va[g]);
-                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(P, bI, bP, yo - R - 1, vs[g]);
+                if (yo + R < h) load_row<MODE, CI, CP>(cI + oa + g * row, cP + oa + g * row, planeI, planeP, va[g]);
+                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(cI + os + g * row, cP + os + g * row, planeI, planeP, vs[g]);
             }
         }
     };
@@ -383,19 +387,20 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
 #pragma unroll
                         for (int m = 0; m < NMAP; ++m) acc[m] -= pr[m];
                     }
-                    double* vrow = Vs + (size_t)g * NMAP * NT;
+                    double* vrow = Vs + (size_t)g * NMAP * NT + tid;
 #pragma unroll
-                    for (int m = 0; m < NMAP; ++m) vrow[m * NT + tid] = acc[m];
+                    for (int m = 0; m < NMAP; ++m) vrow[m * NT] = acc[m];
                 }
             }
         }
-        // ---- coalesced store of the previous batch's staged outputs.
-        for (int idx = tid; idx < prev_rows * NOUT * ocn; idx += NT) {
-            const int oc = idx % ocn;
-            const int gm = idx / ocn;
-            const int m = gm % NOUT, g = gm / NOUT;
-            dst[(size_t)m * n + (size_t)(prev_yb + g) * w + x0 + oc] =
-                Os[((size_t)g * NOUT + m) * NT + oc];
+        // ---- coalesced store of the previous batch's staged outputs (one column per thread).
+        if (tid < ocn) {
+            for (int g = 0; g < prev_rows; ++g) {
+                float* drow = dst + (size_t)(prev_yb + g) * w + tid;
+                const float* orow = Os + (size_t)g * NOUT * NT + tid;
+#pragma unroll
+                for (int m = 0; m < NOUT; ++m) drow[(size_t)m * n] = orow[m * NT];
+            }
         }
         __syncthreads();
 
@@ -420,16 +425,14 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
             const int oce = min(ocn, oc0 + P.K);
             for (int oc = oc0; oc < oce; ++oc, ++c) {
                 StripEpilogue<MODE, CI, CP>::emit(S, invx[oc] * invy, P.eps, orow + oc, NT);
-                if (oc + 1 < oce) {
-                    const int ca = c + R + 1, cs = c - R;
-                    if (ca < ncol) {
+                const int ca = c + R + 1, cs = c - R;
+                if (ca < ncol) {
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + ca];
-                    }
-                    if (cs >= 0) {
+                    for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + ca];
+                }
+                if (cs >= 0) {
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) S[m] -= vrow[m * NT + cs];
-                    }
+                    for (int m = 0; m < NMAP; ++m) S[m] -= vrow[m * NT + cs];
                 }
             }
         }
@@ -437,11 +440,13 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
         prev_yb = yb;
         __syncthreads();
     }
-    for (int idx = tid; idx < prev_rows * NOUT * ocn; idx += NT) {
-        const int oc = idx % ocn;
-        const int gm = idx / ocn;
-        const int m = gm % NOUT, g = gm / NOUT;
-        dst[(size_t)m * n + (size_t)(prev_yb + g) * w + x0 + oc] = Os[((size_t)g * NOUT + m) * NT + oc];
+    if (tid < ocn) {
+        for (int g = 0; g < prev_rows; ++g) {
+            float* drow = dst + (size_t)(prev_yb + g) * w + tid;
+            const float* orow = Os + (size_t)g * NOUT * NT + tid;
+#pragma unroll
+            for (int m = 0; m < NOUT; ++m) drow[(size_t)m * n] = orow[m * NT];
+        }
     }
 }
 
@@ -452,8 +457,7 @@ struct OutParams {
     const float* M;        // [img][(CI+1)CP][h][w] mean maps
     float* q;              // [img][CP][H][W]
     int H, W, h, w;
-    int TR, TC;            // full-res tile rows / cols
-    int nrl, ncl;          // max low-res rows / cols any tile touches (smem sizing)
+    int TR;                // full-resolution rows walked by each thread
 };
 
 // R5: source coordinate of destination index d, resize n_src -> n_dst, exactly in
@@ -478,169 +482,164 @@ __device__ __forceinline__ void src_coord(int d, int n_src, int n_dst, int& i0, 
     i1 = min(i0 + 1, n_src - 1);
 }
 
-template <int CI, int CP>
-struct OutConfig {
-    static constexpr int NC = (CI + 1) * CP;                 // coefficient maps
-    static constexpr int U = (CI == 1) ? 4 : 2;              // rows per thread per batch
+template <int PX>
+struct VecT;
+template <>
+struct VecT<1> {
+    using T = float;
+    __device__ static T ld(const float* p) { return __ldcs(p); }
+    __device__ static void st(float* p, const float* v) { __stcs(p, v[0]); }
+    __device__ static float get(const T& v, int) { return v; }
+};
+template <>
+struct VecT<2> {
+    using T = float2;
+    __device__ static T ld(const float* p) { return __ldcs(reinterpret_cast<const float2*>(p)); }
+    __device__ static void st(float* p, const float* v) {
+        __stcs(reinterpret_cast<float2*>(p), make_float2(v[0], v[1]));
+    }
+    __device__ static float get(const T& v, int i) { return i == 0 ? v.x : v.y; }
+};
+template <>
+struct VecT<4> {
+    using T = float4;
+    __device__ static T ld(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+    __device__ static void st(float* p, const float* v) {
+        __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+    }
+    __device__ static float get(const T& v, int i) {
+        return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+    }
 };
 
-// grid (ceil(W/TC), ceil(H/TR), images), block 256.
-// smem: Hx[nrl][NC][TC] (horizontally interpolated low-res rows), Mraw[nrl][NC][ncl],
-//       row table [TR].
-template <int CI, int CP, bool VEC>
-__global__ void __launch_bounds__(256, (CI == 1 ? 4 : 2)) output_kernel(OutParams P) {
-    constexpr int NT = 256;
-    constexpr int NC = OutConfig<CI, CP>::NC;
-    constexpr int U = OutConfig<CI, CP>::U;
-    extern __shared__ float smem[];
-    const int TC = P.TC, TR = P.TR;
-    float* Hx = smem;                                           // [nrl][NC][TC]
-    float* Mr = Hx + (size_t)P.nrl * NC * TC;                    // [nrl][NC][ncl]
-    int* rt0 = reinterpret_cast<int*>(Mr + (size_t)P.nrl * NC * P.ncl);
-    int* rt1 = rt0 + TR;
-    float* rfy = reinterpret_cast<float*>(rt1 + TR);
-
-    const int tid = threadIdx.x;
-    const int img = blockIdx.z;
-    const int X0 = blockIdx.x * TC, Y0 = blockIdx.y * TR;
+// Column walker.  Each thread owns PX consecutive pixels of a row and walks TR rows down
+// the image.  Their horizontal source coordinates are fixed, so the horizontally
+// interpolated coefficient rows H0 = Hx(y0), H1 = Hx(y1) live in registers and are
+// refreshed only when the low-res row pair changes (every ~s rows); per pixel and map the
+// upsample is then one FMA, A = H0 + fy (H1 - H0), and q_c = sum_j A_{c,j} I_j + A_{c,CI}
+// (P:84-86).  The vertical source coordinate is advanced incrementally in exact integers.
+// Full-resolution rows of I are prefetched U rows ahead (double-buffered registers) with
+// streaming (evict-first) loads; q is written with streaming stores.
+// grid (ceil(W / (256 PX)), ceil(H / TR), images), block 256.
+template <int CI, int CP, int PX>
+__global__ void __launch_bounds__(256, ((CI + 1) * CP * PX <= 8 ? 3 : 2)) output_kernel(OutParams P) {
+    constexpr int NC = (CI + 1) * CP;
+    constexpr int U = 4;
+    using V = VecT<PX>;
+    using VT = typename V::T;
     const int H = P.H, W = P.W, h = P.h, w = P.w;
+    const int X = (blockIdx.x * 256 + threadIdx.x) * PX;
+    if (X >= W) return;
+    const int img = blockIdx.z;
     const size_t N = (size_t)H * W, n = (size_t)h * w;
-    const int nrows = min(TR, H - Y0), ncols = min(TC, W - X0);
-    const float* Iimg = P.I + (size_t)img * CI * N;
-    float* qimg = P.q + (size_t)img * CP * N;
+    const int Y0 = blockIdx.y * P.TR;
+    const int nrows = min(P.TR, H - Y0);
+    const float* Ib = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
+    float* qb = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
+    const float* Mb = P.M + (size_t)img * NC * n;
 
-    // VEC: thread streams float4 column c4 of rows ro, ro + rpp, ... ; U rows per batch.
-    const int tpr = TC >> 2;
-    const int rpp = NT / tpr;
-    const int c4 = tid % tpr, ro = tid / tpr;
-    const int xi = c4 * 4;
-    const bool vact = VEC && xi < ncols;
-    const size_t colo = (size_t)(X0 + xi);
-    const int rstep = rpp * U;
-    float4 cur[U][CI];
-    auto load_batch = [&](int rb, float4 (&buf)[U][CI]) {
+    int xa[PX], xb[PX];
+    float fx[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) src_coord(min(X + i, W - 1), w, W, xa[i], xb[i], fx[i]);
+
+    auto hrow = [&](int y, float (&out)[NC][PX]) {
+        const float* mr = Mb + (size_t)y * w;
+#pragma unroll
+        for (int m = 0; m < NC; ++m)
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                const float va = __ldg(mr + m * n + xa[i]);
+                const float vb = __ldg(mr + m * n + xb[i]);
+                out[m][i] = fmaf(fx[i], vb - va, va);
+            }
+    };
+
+    // Prefetch the first U rows.
+    VT cur[U][CI];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (u < nrows)
+#pragma unroll
+            for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ib + j * N + (size_t)u * W);
+
+    // Vertical coordinate state: num = (2Y+1) h - H; when num > 0, num = qy * den + rem.
+    const long long den = 2LL * H, step = 2LL * h;
+    long long num = (long long)(2 * Y0 + 1) * h - H;
+    long long qy = 0, rem = 0;
+    bool have = false;
+    const float inv_den = 1.0f / (float)den;
+    int cy = -1;                     // low-res row of H0 currently held
+    float H0[NC][PX], H1[NC][PX], D[NC][PX];
+
+    for (int rb = 0; rb < nrows; rb += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int t = rb + u * rpp;
+            const int t = rb + u;
             if (t < nrows) {
-                const size_t off = (size_t)(Y0 + t) * W + colo;
-#pragma unroll
-                for (int j = 0; j < CI; ++j)
-                    buf[u][j] = __ldcs(reinterpret_cast<const float4*>(Iimg + j * N + off));
-            }
-        }
-    };
-    // Issue the first batch of full-resolution loads before the prologue.
-    if (vact) load_batch(ro, cur);
-
-    // Prologue 1: row table and raw low-res rows/cols the tile touches.
-    int ylo, yd, xlo, xd, yhi, xhi;
-    float fd;
-    src_coord(Y0, h, H, ylo, yd, fd);
-    src_coord(Y0 + nrows - 1, h, H, yd, yhi, fd);
-    src_coord(X0, w, W, xlo, xd, fd);
-    src_coord(X0 + ncols - 1, w, W, xd, xhi, fd);
-    const int nrl = yhi - ylo + 1, ncl = xhi - xlo + 1;
-    for (int t = tid; t < nrows; t += NT) {
-        int a, b;
-        float f;
-        src_coord(Y0 + t, h, H, a, b, f);
-        rt0[t] = a - ylo;
-        rt1[t] = b - ylo;
-        rfy[t] = f;
-    }
-    const float* Mimg = P.M + (size_t)img * NC * n;
-    for (int idx = tid; idx < nrl * NC * ncl; idx += NT) {
-        const int xx = idx % ncl, rm = idx / ncl;
-        const int m = rm % NC, rr = rm / NC;
-        Mr[idx] = __ldg(Mimg + (size_t)m * n + (size_t)(ylo + rr) * w + xlo + xx);
-    }
-    __syncthreads();
-
-    // Prologue 2: Hx = horizontal bilinear pass of the nrl low-res rows over the tile.
-    for (int x = tid; x < ncols; x += NT) {
-        int xa, xb;
-        float fx;
-        src_coord(X0 + x, w, W, xa, xb, fx);
-        xa -= xlo;
-        xb -= xlo;
-        for (int rr = 0; rr < nrl; ++rr) {
-#pragma unroll
-            for (int m = 0; m < NC; ++m) {
-                const float* mr = Mr + ((size_t)rr * NC + m) * ncl;
-                const float va = mr[xa], vb = mr[xb];
-                Hx[((size_t)rr * NC + m) * TC + x] = fmaf(fx, vb - va, va);
-            }
-        }
-    }
-    __syncthreads();
-
-    if (VEC) {
-        if (!vact) return;
-        for (int rb = ro; rb < nrows; rb += rstep) {
-            float4 nxt[U][CI];
-            if (rb + rstep < nrows) load_batch(rb + rstep, nxt);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int t = rb + u * rpp;
-                if (t < nrows) {
-                    const float fy = rfy[t];
-                    const float* h0 = Hx + (size_t)rt0[t] * NC * TC + xi;
-                    const float* h1 = Hx + (size_t)rt1[t] * NC * TC + xi;
-                    float4 A[NC];
-#pragma unroll
-                    for (int m = 0; m < NC; ++m) {
-                        const float4 a0 = *reinterpret_cast<const float4*>(h0 + m * TC);
-                        const float4 a1 = *reinterpret_cast<const float4*>(h1 + m * TC);
-                        A[m].x = fmaf(fy, a1.x - a0.x, a0.x);
-                        A[m].y = fmaf(fy, a1.y - a0.y, a0.y);
-                        A[m].z = fmaf(fy, a1.z - a0.z, a0.z);
-                        A[m].w = fmaf(fy, a1.w - a0.w, a0.w);
+                int ya;
+                float fy;
+                if (num <= 0) {
+                    ya = 0;
+                    fy = 0.0f;
+                } else {
+                    if (!have) {
+                        qy = num / den;
+                        rem = num - qy * den;
+                        have = true;
                     }
-                    const size_t off = (size_t)(Y0 + t) * W + colo;
-#pragma unroll
-                    for (int c = 0; c < CP; ++c) {
-                        float4 o = A[c * (CI + 1) + CI];
-#pragma unroll
-                        for (int j = 0; j < CI; ++j) {
-                            const float4 a = A[c * (CI + 1) + j];
-                            o.x = fmaf(a.x, cur[u][j].x, o.x);
-                            o.y = fmaf(a.y, cur[u][j].y, o.y);
-                            o.z = fmaf(a.z, cur[u][j].z, o.z);
-                            o.w = fmaf(a.w, cur[u][j].w, o.w);
-                        }
-                        __stcs(reinterpret_cast<float4*>(qimg + c * N + off), o);
+                    if (qy >= h - 1) {
+                        ya = h - 1;
+                        fy = 0.0f;
+                    } else {
+                        ya = (int)qy;
+                        fy = (float)rem * inv_den;
                     }
                 }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int j = 0; j < CI; ++j) cur[u][j] = nxt[u][j];
-        }
-    } else {
-        // Scalar path (W % 4 != 0 or unaligned buffers): one pixel per thread-iteration.
-        for (int idx = tid; idx < nrows * TC; idx += NT) {
-            const int t = idx / TC, x = idx % TC;
-            if (x >= ncols) continue;
-            const float fy = rfy[t];
-            const float* h0 = Hx + (size_t)rt0[t] * NC * TC + x;
-            const float* h1 = Hx + (size_t)rt1[t] * NC * TC + x;
-            const size_t off = (size_t)(Y0 + t) * W + X0 + x;
-            float iv[CI];
-#pragma unroll
-            for (int j = 0; j < CI; ++j) iv[j] = __ldcs(Iimg + j * N + off);
-#pragma unroll
-            for (int c = 0; c < CP; ++c) {
-                const int mb = c * (CI + 1) + CI;
-                float o = fmaf(fy, h1[mb * TC] - h0[mb * TC], h0[mb * TC]);
-#pragma unroll
-                for (int j = 0; j < CI; ++j) {
-                    const int m = c * (CI + 1) + j;
-                    const float a = fmaf(fy, h1[m * TC] - h0[m * TC], h0[m * TC]);
-                    o = fmaf(a, iv[j], o);
+                num += step;
+                if (have) {
+                    rem += step;
+                    if (rem >= den) {
+                        rem -= den;
+                        ++qy;
+                    }
                 }
-                __stcs(qimg + c * N + off, o);
+                if (ya != cy) {
+                    const int y1 = min(ya + 1, h - 1);
+                    if (ya == cy + 1 && cy >= 0) {
+#pragma unroll
+                        for (int m = 0; m < NC; ++m)
+#pragma unroll
+                            for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+                    } else {
+                        hrow(ya, H0);
+                    }
+                    hrow(y1, H1);
+#pragma unroll
+                    for (int m = 0; m < NC; ++m)
+#pragma unroll
+                        for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+                    cy = ya;
+                }
+                float* qrow = qb + (size_t)t * W;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) {
+                    float o[PX];
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) {
+                        const int mb = c * (CI + 1);
+                        float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+#pragma unroll
+                        for (int j = 0; j < CI; ++j)
+                            acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
+                        o[i] = acc;
+                    }
+                    V::st(qrow + c * N, o);
+                }
+                // Rolling prefetch: this register slot now takes row t + U.
+                if (t + U < nrows)
+#pragma unroll
+                    for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ib + j * N + (size_t)(t + U) * W);
             }
         }
     }
