@@ -104,7 +104,9 @@ int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double ep
     if (r < 1 || s < 1 || !std::isfinite(eps) || !(eps > 0.0)) return FGF_ERR_PARAM;
     if (sub != FGF_SUB_NEAREST && sub != FGF_SUB_BILINEAR) return FGF_ERR_PARAM;
     if (s > 1 && (s >= H || s >= W)) return FGF_ERR_PARAM;  // S:246, R7
-    if ((long long)H * W > (1LL << 40)) return FGF_ERR_SHAPE;
+    // In-image element offsets are 32-bit in the kernels (batch offsets are 64-bit).
+    if ((long long)H * W * std::max(std::max(CI, CP), (CI + 1) * CP) >= (1LL << 31))
+        return FGF_ERR_UNSUPPORTED;
     return FGF_OK;
 }
 
@@ -130,7 +132,7 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     P.strips = (P.w + P.TW - 1) / P.TW;
 
     // Output pass: each thread walks TR full-resolution rows.
-    P.TR = 64;
+    P.TR = 32;
 
     // Chunk of images per pipeline stage: the low-res workspace of one slot ~ kChunkTargetBytes.
     const bool planes = s > 1;
@@ -211,11 +213,10 @@ template <int MODE, int CI, int CP, int NT>
 int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
     using C = StripConfig<MODE, CI, CP, NT>;
     StripParams sp = sp0;
-    const int runs = 32 * C::WPR;
-    int K = (P.TW + runs - 1) / runs;
-    if ((K & 1) == 0) ++K;
-    sp.K = K;
-    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 2G and 64 rows.
+    sp.VP = NT + 2 * P.R + C::K + 1;
+    const size_t smem = C::smem(sp.VP);
+    if (smem > 227 * 1024) return FGF_ERR_UNSUPPORTED;
+    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 4G (and 2R) and 64.
     const long long want = 4LL * 148;
     const long long strips_imgs = (long long)P.strips * images;
     long long th = (P.h * strips_imgs + want - 1) / want;
@@ -226,9 +227,9 @@ int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream
     sp.TW = P.TW;
     dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
     auto kern = box_strip_kernel<MODE, CI, CP, NT>;
-    set_smem(kern, C::SMEM);
+    set_smem(kern, smem);
     ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
-    kern<<<grid, NT, C::SMEM, st>>>(sp);
+    kern<<<grid, NT, smem, st>>>(sp);
     ++g_last_launches;
     return last_error();
 }
@@ -309,13 +310,13 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
         if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
         if (p_is_I) ps = Is;
         else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) return rc;
-        sp.srcI = Is; sp.imgI = (long long)P.CI * P.n; sp.planeI = (long long)P.n;
-        sp.srcP = ps; sp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; sp.planeP = (long long)P.n;
+        sp.srcI = Is; sp.imgI = (long long)P.CI * P.n; sp.planeI = (int)P.n;
+        sp.srcP = ps; sp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; sp.planeP = (int)P.n;
         sp.row = P.w; sp.col = 1;
     } else {
         // s = 1: I' = I, p' = p; K1 reads the images directly.
-        sp.srcI = Ib; sp.imgI = (long long)P.CI * P.N; sp.planeI = (long long)P.N;
-        sp.srcP = pb; sp.imgP = (long long)P.CP * P.N; sp.planeP = (long long)P.N;
+        sp.srcI = Ib; sp.imgI = (long long)P.CI * P.N; sp.planeI = (int)P.N;
+        sp.srcP = pb; sp.imgP = (long long)P.CP * P.N; sp.planeP = (int)P.N;
         sp.row = P.W; sp.col = 1;
     }
     sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
@@ -326,7 +327,7 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
 
     // Step 5: mean_a, mean_b.
     StripParams mp{};
-    mp.srcI = coef; mp.imgI = (long long)P.NC * P.n; mp.planeI = (long long)P.n;
+    mp.srcI = coef; mp.imgI = (long long)P.NC * P.n; mp.planeI = (int)P.n;
     mp.srcP = nullptr;
     mp.row = P.w; mp.col = 1;
     mp.dst = mean;

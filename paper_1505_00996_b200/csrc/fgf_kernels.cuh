@@ -159,35 +159,41 @@ struct StripTraits<MODE_MEAN, CI, CP> {
 };
 
 struct StripParams {
-    // Input sample (y, x) of plane j of image b is at src[b*img + j*plane + y*row + x*col].
+    // Input sample (y, x) of plane j of image b is at src[b*img + j*plane + y*row + x*col];
+    // all in-image offsets fit in 32 bits (validated on the host).
     // STATS: srcI = I (or I' planes), srcP = p (or p' planes); MEAN: srcI = coefficient maps.
     const float* srcI;
     const float* srcP;
-    long long imgI, planeI, imgP, planeP;
-    long long row, col;     // row pitch and column stride of a sample (s*W and s for nearest)
+    long long imgI, imgP;
+    int planeI, planeP;
+    int row, col;           // row pitch and column stride of a sample
     float* dst;             // [img][(CI+1)CP][h][w]
     int h, w, R;            // low-res dims and radius r'
     int TW, TH;             // output columns per strip, output rows per segment
-    int K;                  // odd horizontal run length
+    int VP;                 // padded fp64 row length in shared memory: NT + 2R + K + 1
     double eps;
 };
 
-// Rows-per-batch G and shared-memory layout.
+// Rows per batch G (each warp slides along one row of a batch), odd run length K, smem.
 template <int MODE, int CI, int CP, int NT>
 struct StripConfig {
     using T = StripTraits<MODE, CI, CP>;
     static constexpr int NMAP = T::NMAP;
     static constexpr int NOUT = T::NOUT;
     static constexpr int NW = NT / 32;
-    static constexpr int V_ROW = NMAP * NT * 8;                 // fp64 column sums, one row
-    static constexpr int O_ROW = NOUT * NT * 4;                 // fp32 staged outputs, one row
-    static constexpr int G0 = (82 * 1024) / (V_ROW + O_ROW);
+    static constexpr int VPMAX = NT == 256 ? 448 : 992;         // worst-case padded row
+    static constexpr int ROWB = NMAP * VPMAX * 8 + NOUT * NT * 4;
+    static constexpr int G0 = (160 * 1024) / ROWB;
     static constexpr int G1 = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
     static constexpr int G = G1 > NW ? NW : G1;
     static constexpr int WPR = NW / G;                           // warps per row
-    static constexpr size_t SMEM = (size_t)G * (V_ROW + O_ROW) + (size_t)NT * 8;
+    static constexpr int K = G == 8 ? 9 : (G == 4 ? 5 : (G == 2 ? 3 : 1));
     static constexpr int WB = T::NIN <= 4 ? 8 : (T::NIN <= 8 ? 4 : 2);
-    static constexpr int MINB = NT == 256 ? (NMAP <= 2 ? 4 : (NMAP <= 6 ? 3 : (NMAP <= 13 ? 2 : 1))) : 1;
+    static constexpr int MINB = NMAP <= 6 ? 2 : 1;
+    // dynamic smem for padded row length VP
+    static size_t smem(int VP) {
+        return (size_t)G * NMAP * VP * 8 + (size_t)G * NOUT * NT * 4 + (size_t)NT * 8;
+    }
 };
 
 // Epilogue of steps 3-4; writes NOUT values at dst[m * ostride].
@@ -261,19 +267,19 @@ struct StripEpilogue<MODE_MEAN, CI, CP> {
     }
 };
 
-// Loads the NIN inputs of one row for this thread's column; `at` points at plane 0.
+// Loads the NIN inputs of one row for this thread's column (32-bit in-image offsets).
 template <int MODE, int CI, int CP>
-__device__ __forceinline__ void load_row(const float* atI, const float* atP, long long planeI,
-                                         long long planeP, float* v) {
+__device__ __forceinline__ void load_row(const float* bI, const float* bP, int off, int planeI,
+                                         int planeP, float* v) {
     using T = StripTraits<MODE, CI, CP>;
     if (MODE == MODE_STATS) {
 #pragma unroll
-        for (int j = 0; j < CI; ++j) v[j] = __ldg(atI + j * planeI);
+        for (int j = 0; j < CI; ++j) v[j] = __ldg(bI + (off + j * planeI));
 #pragma unroll
-        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(atP + c * planeP);
+        for (int c = 0; c < CP; ++c) v[CI + c] = __ldg(bP + (off + c * planeP));
     } else {
 #pragma unroll
-        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(atI + m * planeI);
+        for (int m = 0; m < T::NIN; ++m) v[m] = __ldg(bI + (off + m * planeI));
     }
 }
 
@@ -286,15 +292,17 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     constexpr int NIN = T::NIN;
     constexpr int NOUT = T::NOUT;
     constexpr int G = C::G;
+    constexpr int K = C::K;
     extern __shared__ double smem_d[];
-    double* Vs = smem_d;                                                  // [G][NMAP][NT]
-    float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * NT);      // [G][NOUT][NT]
+    const int VP = P.VP;
+    double* Vs = smem_d;                                                  // [G][NMAP][VP]
+    float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * VP);      // [G][NOUT][NT]
     double* invx = reinterpret_cast<double*>(Os + (size_t)G * NOUT * NT);  // [NT]
 
     const int tid = threadIdx.x;
     const int img = blockIdx.z;
     const int h = P.h, w = P.w, R = P.R;
-    const size_t n = (size_t)h * w;
+    const int n = h * w;
     const int x0 = blockIdx.x * P.TW;
     const int xe = min(w, x0 + P.TW);
     const int y0 = blockIdx.y * P.TH;
@@ -304,21 +312,23 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     const int ocn = xe - x0;                 // output columns of this strip
     const int cbase = x0 - xs0;              // local column of output column 0
     const bool colthr = tid < ncol;
-    const int gx = xs0 + (colthr ? tid : 0);
-    const long long row = P.row, planeI = P.planeI, planeP = P.planeP;
-
-    const float* cI = P.srcI + img * P.imgI + gx * P.col;   // this column, row 0, plane 0
-    const float* cP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP + gx * P.col : cI;
+    const int offc = (xs0 + (colthr ? tid : 0)) * P.col;
+    const int row = P.row, planeI = P.planeI, planeP = P.planeP;
+    const float* bI = P.srcI + img * P.imgI;
+    const float* bP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP : bI;
     float* dst = P.dst + (size_t)img * NOUT * n + x0;
 
-    // 1 / (horizontal in-bounds count) per output column (R1).
+    // Zero the padded column-sum rows once: the pads make every horizontal window read
+    // in-bounds, and zeros contribute nothing, so sums equal the clipped sums (R1).
+    for (int i = tid; i < G * NMAP * VP; i += NT) Vs[i] = 0.0;
+    // 1 / (horizontal in-bounds count) per output column.
     if (tid < ocn) {
         const int c = cbase + tid;
         invx[tid] = 1.0 / (double)(min(ncol - 1, c + R) - max(0, c - R) + 1);
     }
 
     // Running vertical window sums of this thread's column (fp64; products of two floats are
-    // exact in fp64, and fma(x, y, acc) rounds once).
+    // exact in fp64).
     double acc[NMAP];
 #pragma unroll
     for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
@@ -329,10 +339,9 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
         const int wa = max(0, y0 - R - 1), wb = min(h - 1, y0 + R - 1);
         for (int y = wa; y <= wb; y += WB) {
             float v[WB][NIN];
-            const long long off = (long long)y * row;
 #pragma unroll
             for (int k = 0; k < WB; ++k)
-                if (y + k <= wb) load_row<MODE, CI, CP>(cI + off + k * row, cP + off + k * row, planeI, planeP, v[k]);
+                if (y + k <= wb) load_row<MODE, CI, CP>(bI, bP, (y + k) * row + offc, planeI, planeP, v[k]);
 #pragma unroll
             for (int k = 0; k < WB; ++k) {
                 if (y + k <= wb) {
@@ -346,22 +355,21 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
     }
 
     // Horizontal-phase mapping: warp -> row hg of the batch; the WPR warps of a row split it
-    // into 32*WPR runs of K consecutive output columns.
+    // into 32*WPR runs of K (odd) consecutive output columns, so the 16 lanes of a half-warp
+    // read 16 distinct fp64 banks.
     const int warp = tid >> 5, lane = tid & 31;
     const int hg = warp % G;
-    const int run = (warp / G) * 32 + lane;
-    const int oc0 = run * P.K;
+    const int oc0 = ((warp / G) * 32 + lane) * K;
 
     // Software pipeline: va/vs hold the add/subtract rows of the current batch.
     float va[G][NIN], vs[G][NIN];
     auto load_batch = [&](int yb) {
-        const long long oa = (long long)(yb + R) * row, os = (long long)(yb - R - 1) * row;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const int yo = yb + g;
             if (yo < ye) {
-                if (yo + R < h) load_row<MODE, CI, CP>(cI + oa + g * row, cP + oa + g * row, planeI, planeP, va[g]);
-                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(cI + os + g * row, cP + os + g * row, planeI, planeP, vs[g]);
+                if (yo + R < h) load_row<MODE, CI, CP>(bI, bP, (yo + R) * row + offc, planeI, planeP, va[g]);
+                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(bI, bP, (yo - R - 1) * row + offc, planeI, planeP, vs[g]);
             }
         }
     };
@@ -387,9 +395,9 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
 #pragma unroll
                         for (int m = 0; m < NMAP; ++m) acc[m] -= pr[m];
                     }
-                    double* vrow = Vs + (size_t)g * NMAP * NT + tid;
+                    double* vrow = Vs + (size_t)g * NMAP * VP + R + tid;
 #pragma unroll
-                    for (int m = 0; m < NMAP; ++m) vrow[m * NT] = acc[m];
+                    for (int m = 0; m < NMAP; ++m) vrow[m * VP] = acc[m];
                 }
             }
         }
@@ -407,32 +415,27 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box
         // ---- prefetch the next batch (in flight during the horizontal phase).
         if (colthr && yb + G < ye) load_batch(yb + G);
 
-        // ---- horizontal phase: sliding window along each snapshotted row.
+        // ---- horizontal phase: branch-free sliding window along each snapshotted row.
         const int yo = yb + hg;
         if (yo < ye && oc0 < ocn) {
-            const double* vrow = Vs + (size_t)hg * NMAP * NT;
+            const double* vr = Vs + (size_t)hg * NMAP * VP + R + cbase + oc0;  // local col of oc0
             const double invy = 1.0 / (double)(min(h - 1, yo + R) - max(0, yo - R) + 1);
-            int c = cbase + oc0;
-            const int lo = max(0, c - R), hi = min(ncol - 1, c + R);
             double S[NMAP];
 #pragma unroll
             for (int m = 0; m < NMAP; ++m) S[m] = 0.0;
-            for (int k = lo; k <= hi; ++k) {
+#pragma unroll 4
+            for (int k = -R; k <= R; ++k) {
 #pragma unroll
-                for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + k];
+                for (int m = 0; m < NMAP; ++m) S[m] += vr[m * VP + k];
             }
-            float* orow = Os + (size_t)hg * NOUT * NT;
-            const int oce = min(ocn, oc0 + P.K);
-            for (int oc = oc0; oc < oce; ++oc, ++c) {
-                StripEpilogue<MODE, CI, CP>::emit(S, invx[oc] * invy, P.eps, orow + oc, NT);
-                const int ca = c + R + 1, cs = c - R;
-                if (ca < ncol) {
+            float* orow = Os + (size_t)hg * NOUT * NT + oc0;
 #pragma unroll
-                    for (int m = 0; m < NMAP; ++m) S[m] += vrow[m * NT + ca];
-                }
-                if (cs >= 0) {
+            for (int i = 0; i < K; ++i) {
+                if (oc0 + i < ocn)
+                    StripEpilogue<MODE, CI, CP>::emit(S, invx[oc0 + i] * invy, P.eps, orow + i, NT);
+                if (i + 1 < K) {
 #pragma unroll
-                    for (int m = 0; m < NMAP; ++m) S[m] -= vrow[m * NT + cs];
+                    for (int m = 0; m < NMAP; ++m) S[m] += vr[m * VP + i + R + 1] - vr[m * VP + i - R];
                 }
             }
         }
@@ -515,33 +518,53 @@ struct VecT<4> {
 // Column walker.  Each thread owns PX consecutive pixels of a row and walks TR rows down
 // the image.  Their horizontal source coordinates are fixed, so the horizontally
 // interpolated coefficient rows H0 = Hx(y0), H1 = Hx(y1) live in registers and are
-// refreshed only when the low-res row pair changes (every ~s rows); per pixel and map the
-// upsample is then one FMA, A = H0 + fy (H1 - H0), and q_c = sum_j A_{c,j} I_j + A_{c,CI}
-// (P:84-86).  The vertical source coordinate is advanced incrementally in exact integers.
-// Full-resolution rows of I are prefetched U rows ahead (double-buffered registers) with
-// streaming (evict-first) loads; q is written with streaming stores.
-// grid (ceil(W / (256 PX)), ceil(H / TR), images), block 256.
+// refreshed only when the low-res row pair changes (every ~s rows; the row table is in
+// shared memory, so that test is CTA-uniform).  Per pixel and map the upsample is then
+// A = H0 + fy (H1 - H0) and q_c = sum_j A_{c,j} I_j + A_{c,CI}.  Full-resolution
+// rows of I are prefetched U rows ahead in a rolling register ring with streaming
+// (evict-first) loads; q is written with streaming stores.
+// grid (ceil(W / (256 PX)), ceil(H / TR), images), block 256, TR <= kMaxTR.
+constexpr int kMaxTR = 128;
+
 template <int CI, int CP, int PX>
-__global__ void __launch_bounds__(256, ((CI + 1) * CP * PX <= 8 ? 3 : 2)) output_kernel(OutParams P) {
-    constexpr int NC = (CI + 1) * CP;
-    constexpr int U = 4;
+struct OutCfg {
+    static constexpr int NC = (CI + 1) * CP;
+    static constexpr int U0 = 32 / (CI * PX);
+    static constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
+    static constexpr int MINB = NC * PX <= 8 ? 3 : 2;
+};
+
+template <int CI, int CP, int PX>
+__global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel(OutParams P) {
+    constexpr int NC = OutCfg<CI, CP, PX>::NC;
+    constexpr int U = OutCfg<CI, CP, PX>::U;
     using V = VecT<PX>;
     using VT = typename V::T;
+    __shared__ int s_ya[kMaxTR];
+    __shared__ float s_fy[kMaxTR];
     const int H = P.H, W = P.W, h = P.h, w = P.w;
+    const int Y0 = blockIdx.y * P.TR;
+    const int nrows = min(P.TR, H - Y0);
+    for (int t = threadIdx.x; t < nrows; t += 256) {
+        int ya, yb;
+        float fy;
+        src_coord(Y0 + t, h, H, ya, yb, fy);
+        s_ya[t] = ya;
+        s_fy[t] = fy;
+    }
+    __syncthreads();
     const int X = (blockIdx.x * 256 + threadIdx.x) * PX;
     if (X >= W) return;
     const int img = blockIdx.z;
     const size_t N = (size_t)H * W, n = (size_t)h * w;
-    const int Y0 = blockIdx.y * P.TR;
-    const int nrows = min(P.TR, H - Y0);
-    const float* Ib = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
-    float* qb = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
+    const float* Ip = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
+    float* qp = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
     const float* Mb = P.M + (size_t)img * NC * n;
 
-    int xa[PX], xb[PX];
+    int oa[PX], ob[PX];
     float fx[PX];
 #pragma unroll
-    for (int i = 0; i < PX; ++i) src_coord(min(X + i, W - 1), w, W, xa[i], xb[i], fx[i]);
+    for (int i = 0; i < PX; ++i) src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
 
     auto hrow = [&](int y, float (&out)[NC][PX]) {
         const float* mr = Mb + (size_t)y * w;
@@ -549,64 +572,31 @@ __global__ void __launch_bounds__(256, ((CI + 1) * CP * PX <= 8 ? 3 : 2)) output
         for (int m = 0; m < NC; ++m)
 #pragma unroll
             for (int i = 0; i < PX; ++i) {
-                const float va = __ldg(mr + m * n + xa[i]);
-                const float vb = __ldg(mr + m * n + xb[i]);
+                const float va = __ldg(mr + (m * (int)n + oa[i]));
+                const float vb = __ldg(mr + (m * (int)n + ob[i]));
                 out[m][i] = fmaf(fx[i], vb - va, va);
             }
     };
 
-    // Prefetch the first U rows.
     VT cur[U][CI];
 #pragma unroll
     for (int u = 0; u < U; ++u)
         if (u < nrows)
 #pragma unroll
-            for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ib + j * N + (size_t)u * W);
+            for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ip + j * N + (size_t)u * W);
+    const float* Ipf = Ip + (size_t)U * W;
 
-    // Vertical coordinate state: num = (2Y+1) h - H; when num > 0, num = qy * den + rem.
-    const long long den = 2LL * H, step = 2LL * h;
-    long long num = (long long)(2 * Y0 + 1) * h - H;
-    long long qy = 0, rem = 0;
-    bool have = false;
-    const float inv_den = 1.0f / (float)den;
-    int cy = -1;                     // low-res row of H0 currently held
-    float H0[NC][PX], H1[NC][PX], D[NC][PX];
-
+    int cy = -2;
+    float H0[NC][PX], H1[NC][PX];
     for (int rb = 0; rb < nrows; rb += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = rb + u;
             if (t < nrows) {
-                int ya;
-                float fy;
-                if (num <= 0) {
-                    ya = 0;
-                    fy = 0.0f;
-                } else {
-                    if (!have) {
-                        qy = num / den;
-                        rem = num - qy * den;
-                        have = true;
-                    }
-                    if (qy >= h - 1) {
-                        ya = h - 1;
-                        fy = 0.0f;
-                    } else {
-                        ya = (int)qy;
-                        fy = (float)rem * inv_den;
-                    }
-                }
-                num += step;
-                if (have) {
-                    rem += step;
-                    if (rem >= den) {
-                        rem -= den;
-                        ++qy;
-                    }
-                }
+                const int ya = s_ya[t];
+                const float fy = s_fy[t];
                 if (ya != cy) {
-                    const int y1 = min(ya + 1, h - 1);
-                    if (ya == cy + 1 && cy >= 0) {
+                    if (ya == cy + 1) {
 #pragma unroll
                         for (int m = 0; m < NC; ++m)
 #pragma unroll
@@ -614,32 +604,31 @@ __global__ void __launch_bounds__(256, ((CI + 1) * CP * PX <= 8 ? 3 : 2)) output
                     } else {
                         hrow(ya, H0);
                     }
-                    hrow(y1, H1);
-#pragma unroll
-                    for (int m = 0; m < NC; ++m)
-#pragma unroll
-                        for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+                    hrow(min(ya + 1, h - 1), H1);
                     cy = ya;
                 }
-                float* qrow = qb + (size_t)t * W;
 #pragma unroll
                 for (int c = 0; c < CP; ++c) {
+                    const int mb = c * (CI + 1);
                     float o[PX];
 #pragma unroll
                     for (int i = 0; i < PX; ++i) {
-                        const int mb = c * (CI + 1);
-                        float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+                        float acc = fmaf(fy, H1[mb + CI][i] - H0[mb + CI][i], H0[mb + CI][i]);
 #pragma unroll
-                        for (int j = 0; j < CI; ++j)
-                            acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
+                        for (int j = 0; j < CI; ++j) {
+                            const float a = fmaf(fy, H1[mb + j][i] - H0[mb + j][i], H0[mb + j][i]);
+                            acc = fmaf(a, V::get(cur[u][j], i), acc);
+                        }
                         o[i] = acc;
                     }
-                    V::st(qrow + c * N, o);
+                    V::st(qp + c * N, o);
                 }
+                qp += W;
                 // Rolling prefetch: this register slot now takes row t + U.
                 if (t + U < nrows)
 #pragma unroll
-                    for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ib + j * N + (size_t)(t + U) * W);
+                    for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ipf + j * N);
+                Ipf += W;
             }
         }
     }
