@@ -276,8 +276,37 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     return launch_output_px<CI, CP, 1>(op, images, P, st);
 }
 
+int g_num_sms = 0;
+
+template <int CI, int CP>
+int launch_output_tma(const float* I, const float* M, float* q, int images, const Plan& P,
+                      cudaStream_t st) {
+    using Cfg = TmaCfg<CI, CP>;
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    TmaOutParams tp{I, M, q, P.H, P.W, P.h, P.w, images, 32, (P.W + 1023) / 1024, 1};
+    const int bands = (P.H + tp.TR - 1) / tp.TR;
+    const long long items = (long long)images * bands;
+    tp.cpb = (int)std::max<long long>(1, std::min<long long>(items, g_num_sms / tp.ncb));
+    auto kern = output_tma_kernel<CI, CP>;
+    set_smem(kern, Cfg::SMEM);
+    ProfScope ps(KIND_OUT, st);
+    kern<<<tp.ncb * tp.cpb, 256, Cfg::SMEM, st>>>(tp);
+    ++g_last_launches;
+    return last_error();
+}
+
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
                   cudaStream_t st) {
+    const bool tma_ok = P.W % 4 == 0 && P.H >= 1 && getenv("FGF_NO_TMA") == nullptr &&
+                        ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
+    if (tma_ok && P.CI == 1 && P.CP == 1) return launch_output_tma<1, 1>(I, M, q, images, P, st);
+    if (tma_ok && P.CI == 1 && P.CP == 2) return launch_output_tma<1, 2>(I, M, q, images, P, st);
+    if (tma_ok && P.CI == 3 && P.CP == 1) return launch_output_tma<3, 1>(I, M, q, images, P, st);
     OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR};
     switch (P.CI * 10 + P.CP) {
         case 11: return launch_output_t<1, 1>(op, images, P, st);

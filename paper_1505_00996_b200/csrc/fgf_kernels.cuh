@@ -634,4 +634,241 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
     }
 }
 
+// ------------------------------------------------------------------ K4 (TMA pipeline)
+//
+// Persistent variant of K4 for 16-byte aligned rows (W % 4 == 0).  The image is cut into
+// column blocks of 1024 pixels; every CTA owns one column block (so each thread's four
+// horizontal source coordinates are computed once) and walks bands of TR rows of successive
+// images.  Thread 0 streams the rows of I into a ring of NSTAGE shared-memory stages with
+// 1-D bulk copies (cp.async.bulk, evict-first L2 policy) completing on per-stage mbarriers,
+// keeping NSTAGE * RPS rows (>= 96 KB) in flight per SM; the 256 threads read their float4
+// from shared memory, apply the register-resident coefficient rows, and stream q out.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+struct TmaOutParams {
+    const float* I;        // [img][CI][H][W]
+    const float* M;        // [img][(CI+1)CP][h][w]
+    float* q;              // [img][CP][H][W]
+    int H, W, h, w;
+    int images;            // images in this launch
+    int TR;                // rows per band
+    int ncb;               // column blocks of 1024 px
+    int cpb;               // CTAs per column block (gridDim.x = ncb * cpb)
+};
+
+template <int CI, int CP>
+struct TmaCfg {
+    static constexpr int NC = (CI + 1) * CP;
+    static constexpr int RPS = CI == 1 ? 4 : 2;        // rows per stage
+    static constexpr int NSTAGE = CI == 1 ? 8 : 6;
+    static constexpr int ROWF = 1024;                   // floats per row segment
+    static constexpr size_t STAGE_FLOATS = (size_t)RPS * CI * ROWF;
+    static constexpr size_t SMEM = NSTAGE * STAGE_FLOATS * 4 + NSTAGE * 8;
+};
+
+template <int CI, int CP>
+__global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
+    using Cfg = TmaCfg<CI, CP>;
+    constexpr int NC = Cfg::NC;
+    constexpr int RPS = Cfg::RPS;
+    constexpr int NS = Cfg::NSTAGE;
+    constexpr int ROWF = Cfg::ROWF;
+    extern __shared__ __align__(128) float tsm[];
+    float* buf = tsm;                                                   // [NS][RPS][CI][ROWF]
+    uint64_t* full = reinterpret_cast<uint64_t*>(tsm + NS * Cfg::STAGE_FLOATS);
+
+    const int H = P.H, W = P.W, h = P.h, w = P.w;
+    const int tid = threadIdx.x;
+    const int cb = blockIdx.x % P.ncb;
+    const int k0 = blockIdx.x / P.ncb;
+    const int X0 = cb * ROWF;
+    const int segf = min(ROWF, W - X0);                 // floats in this column block's rows
+    const uint32_t seg_bytes = (uint32_t)segf * 4u;
+    const int bands = (H + P.TR - 1) / P.TR;
+    const int items = P.images * bands;
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    // ---- producer state (thread 0): next (item, row) to stream.
+    int p_item = k0, p_row = 0;
+    uint64_t pol = 0;
+    if (tid == 0) pol = evict_first_policy();
+    auto produce = [&](int slot) {
+        // issue the next stage (<= RPS rows of the current item) into `slot`
+        if (p_item >= items) return;
+        const int img = p_item / bands, band = p_item % bands;
+        const int Yb = band * P.TR;
+        const int rows_item = min(P.TR, H - Yb);
+        const int nr = min(RPS, rows_item - p_row);
+        mbar_expect_tx(&full[slot], (uint32_t)nr * CI * seg_bytes);
+        float* dstb = buf + (size_t)slot * Cfg::STAGE_FLOATS;
+        for (int r = 0; r < nr; ++r)
+            for (int j = 0; j < CI; ++j)
+                bulk_g2s(dstb + ((size_t)r * CI + j) * ROWF,
+                         P.I + ((size_t)img * CI + j) * N + (size_t)(Yb + p_row + r) * W + X0,
+                         seg_bytes, &full[slot], pol);
+        p_row += nr;
+        if (p_row >= rows_item) {
+            p_row = 0;
+            p_item += P.cpb;
+        }
+    };
+    if (tid == 0)
+        for (int s = 0; s < NS; ++s) produce(s);
+
+    // ---- consumer: each thread owns pixels X0 + 4 tid .. + 3 of every row.
+    const int xl = tid * 4;
+    const bool act = xl < segf;
+    const int X = X0 + xl;
+    int oa[4], ob[4];
+    float fx[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
+
+    int stage = 0;                                       // global stage counter (ring position)
+    for (int item = k0; item < items; item += P.cpb) {
+        const int img = item / bands, band = item % bands;
+        const int Yb = band * P.TR;
+        const int rows_item = min(P.TR, H - Yb);
+        const float* Mb = P.M + (size_t)img * NC * n;
+        float* qb = P.q + (size_t)img * CP * N + (size_t)Yb * W + X;
+        // exact vertical source coordinate state for row Yb (R5): num = (2Y+1) h - H
+        const long long den = 2LL * H, step = 2LL * h;
+        long long num = (long long)(2 * Yb + 1) * h - H;
+        long long qy = 0, rem = 0;
+        bool have = false;
+        const float inv_den = 1.0f / (float)den;
+        int cy = -2;
+        float H0[NC][4], H1[NC][4];
+        auto hrow = [&](int y, float (&out)[NC][4]) {
+            const float* mr = Mb + (size_t)y * w;
+#pragma unroll
+            for (int m = 0; m < NC; ++m)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float va = __ldg(mr + (m * (int)n + oa[i]));
+                    const float vb = __ldg(mr + (m * (int)n + ob[i]));
+                    out[m][i] = fmaf(fx[i], vb - va, va);
+                }
+        };
+        for (int r0 = 0; r0 < rows_item; r0 += RPS, ++stage) {
+            const int slot = stage % NS;
+            mbar_wait(&full[slot], (uint32_t)((stage / NS) & 1));
+            const float* sb = buf + (size_t)slot * Cfg::STAGE_FLOATS + xl;
+            const int nr = min(RPS, rows_item - r0);
+#pragma unroll
+            for (int r = 0; r < RPS; ++r) {
+                if (r < nr) {
+                    int ya;
+                    float fy;
+                    if (num <= 0) {
+                        ya = 0;
+                        fy = 0.0f;
+                    } else {
+                        if (!have) {
+                            qy = num / den;
+                            rem = num - qy * den;
+                            have = true;
+                        }
+                        if (qy >= h - 1) {
+                            ya = h - 1;
+                            fy = 0.0f;
+                        } else {
+                            ya = (int)qy;
+                            fy = (float)rem * inv_den;
+                        }
+                    }
+                    num += step;
+                    if (have) {
+                        rem += step;
+                        if (rem >= den) {
+                            rem -= den;
+                            ++qy;
+                        }
+                    }
+                    if (act) {
+                        if (ya != cy) {
+                            if (ya == cy + 1) {
+#pragma unroll
+                                for (int m = 0; m < NC; ++m)
+#pragma unroll
+                                    for (int i = 0; i < 4; ++i) H0[m][i] = H1[m][i];
+                            } else {
+                                hrow(ya, H0);
+                            }
+                            hrow(min(ya + 1, h - 1), H1);
+                            cy = ya;
+                        }
+                        float4 iv[CI];
+#pragma unroll
+                        for (int j = 0; j < CI; ++j)
+                            iv[j] = *reinterpret_cast<const float4*>(sb + ((size_t)r * CI + j) * ROWF);
+                        float* qrow = qb + (size_t)(r0 + r) * W;
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            const int mb = c * (CI + 1);
+                            float o[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                float acc = fmaf(fy, H1[mb + CI][i] - H0[mb + CI][i], H0[mb + CI][i]);
+#pragma unroll
+                                for (int j = 0; j < CI; ++j) {
+                                    const float a = fmaf(fy, H1[mb + j][i] - H0[mb + j][i], H0[mb + j][i]);
+                                    const float v = i == 0 ? iv[j].x : (i == 1 ? iv[j].y : (i == 2 ? iv[j].z : iv[j].w));
+                                    acc = fmaf(a, v, acc);
+                                }
+                                o[i] = acc;
+                            }
+                            __stcs(reinterpret_cast<float4*>(qrow + c * N), make_float4(o[0], o[1], o[2], o[3]));
+                        }
+                    }
+                }
+            }
+            __syncthreads();                      // every thread is done with this slot
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                produce(slot);
+            }
+        }
+    }
+}
+
 }  // namespace fgf
