@@ -778,16 +778,28 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
         const float inv_den = 1.0f / (float)den;
         int cy = -2;
         float H0[NC][4], H1[NC][4];
-        auto hrow = [&](int y, float (&out)[NC][4]) {
+        float pa[NC][4], pb[NC][4];          // raw low-res values of the prefetched row
+        int py = -1;                          // low-res row held in pa/pb
+        auto fetch = [&](int y) {
             const float* mr = Mb + (size_t)y * w;
 #pragma unroll
             for (int m = 0; m < NC; ++m)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float va = __ldg(mr + (m * (int)n + oa[i]));
-                    const float vb = __ldg(mr + (m * (int)n + ob[i]));
-                    out[m][i] = fmaf(fx[i], vb - va, va);
+                    pa[m][i] = __ldg(mr + (m * (int)n + oa[i]));
+                    pb[m][i] = __ldg(mr + (m * (int)n + ob[i]));
                 }
+            py = y;
+        };
+        auto lerpx = [&](float (&out)[NC][4]) {
+#pragma unroll
+            for (int m = 0; m < NC; ++m)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) out[m][i] = fmaf(fx[i], pb[m][i] - pa[m][i], pa[m][i]);
+        };
+        auto hrow = [&](int y, float (&out)[NC][4]) {
+            if (py != y) fetch(y);
+            lerpx(out);
         };
         for (int r0 = 0; r0 < rows_item; r0 += RPS, ++stage) {
             const int slot = stage % NS;
@@ -826,6 +838,7 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
                     }
                     if (act) {
                         if (ya != cy) {
+                            const int y1 = min(ya + 1, h - 1);
                             if (ya == cy + 1) {
 #pragma unroll
                                 for (int m = 0; m < NC; ++m)
@@ -834,8 +847,10 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
                             } else {
                                 hrow(ya, H0);
                             }
-                            hrow(min(ya + 1, h - 1), H1);
+                            hrow(y1, H1);
                             cy = ya;
+                            // one row ahead: the loads fly while the next ~s rows are computed
+                            fetch(min(y1 + 1, h - 1));
                         }
                         float4 iv[CI];
 #pragma unroll
