@@ -553,8 +553,8 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
         s_fy[t] = fy;
     }
     __syncthreads();
-    const int X = (blockIdx.x * 256 + threadIdx.x) * PX;
-    if (X >= W) return;
+    const bool act = (blockIdx.x * 256 + threadIdx.x) * PX < W;
+    const int X = act ? (blockIdx.x * 256 + threadIdx.x) * PX : 0;
     const int img = blockIdx.z;
     const size_t N = (size_t)H * W, n = (size_t)h * w;
     const float* Ip = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
     VT cur[U][CI];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-        if (u < nrows)
+        if (act && u < nrows)
 #pragma unroll
             for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ip + j * N + (size_t)u * W);
     const float* Ipf = Ip + (size_t)U * W;
@@ -595,18 +595,21 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
             if (t < nrows) {
                 const int ya = s_ya[t];
                 const float fy = s_fy[t];
-                if (ya != cy) {
-                    if (ya == cy + 1) {
+                if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform: a real branch
+                    if (act) {
+                        if (ya == cy + 1) {
 #pragma unroll
-                        for (int m = 0; m < NC; ++m)
+                            for (int m = 0; m < NC; ++m)
 #pragma unroll
-                            for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
-                    } else {
-                        hrow(ya, H0);
+                                for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+                        } else {
+                            hrow(ya, H0);
+                        }
+                        hrow(min(ya + 1, h - 1), H1);
                     }
-                    hrow(min(ya + 1, h - 1), H1);
                     cy = ya;
                 }
+                if (!act) continue;
 #pragma unroll
                 for (int c = 0; c < CP; ++c) {
                     const int mb = c * (CI + 1);
@@ -709,6 +712,8 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
     extern __shared__ __align__(128) float tsm[];
     float* buf = tsm;                                                   // [NS][RPS][CI][ROWF]
     uint64_t* full = reinterpret_cast<uint64_t*>(tsm + NS * Cfg::STAGE_FLOATS);
+    __shared__ int s_ya[kMaxTR];
+    __shared__ float s_fy[kMaxTR];
 
     const int H = P.H, W = P.W, h = P.h, w = P.w;
     const int tid = threadIdx.x;
@@ -770,12 +775,15 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
         const int rows_item = min(P.TR, H - Yb);
         const float* Mb = P.M + (size_t)img * NC * n;
         float* qb = P.q + (size_t)img * CP * N + (size_t)Yb * W + X;
-        // exact vertical source coordinate state for row Yb (R5): num = (2Y+1) h - H
-        const long long den = 2LL * H, step = 2LL * h;
-        long long num = (long long)(2 * Yb + 1) * h - H;
-        long long qy = 0, rem = 0;
-        bool have = false;
-        const float inv_den = 1.0f / (float)den;
+        // Row table of this band (R5): low-res row and vertical weight of each row.
+        for (int t = tid; t < rows_item; t += 256) {
+            int a, b;
+            float f;
+            src_coord(Yb + t, h, H, a, b, f);
+            s_ya[t] = a;
+            s_fy[t] = f;
+        }
+        __syncthreads();
         int cy = -2;
         float H0[NC][4], H1[NC][4];
         float pa[NC][4], pb[NC][4];          // raw low-res values of the prefetched row
@@ -809,35 +817,11 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
 #pragma unroll
             for (int r = 0; r < RPS; ++r) {
                 if (r < nr) {
-                    int ya;
-                    float fy;
-                    if (num <= 0) {
-                        ya = 0;
-                        fy = 0.0f;
-                    } else {
-                        if (!have) {
-                            qy = num / den;
-                            rem = num - qy * den;
-                            have = true;
-                        }
-                        if (qy >= h - 1) {
-                            ya = h - 1;
-                            fy = 0.0f;
-                        } else {
-                            ya = (int)qy;
-                            fy = (float)rem * inv_den;
-                        }
-                    }
-                    num += step;
-                    if (have) {
-                        rem += step;
-                        if (rem >= den) {
-                            rem -= den;
-                            ++qy;
-                        }
-                    }
-                    if (act) {
-                        if (ya != cy) {
+                    const int ya = s_ya[r0 + r];
+                    const float fy = s_fy[r0 + r];
+                    // ya is the same for every thread (CTA-uniform): vote -> a real branch
+                    if (__any_sync(0xffffffffu, ya != cy)) {
+                        if (act) {
                             const int y1 = min(ya + 1, h - 1);
                             if (ya == cy + 1) {
 #pragma unroll
@@ -848,10 +832,12 @@ __global__ void __launch_bounds__(256, 1) output_tma_kernel(TmaOutParams P) {
                                 hrow(ya, H0);
                             }
                             hrow(y1, H1);
-                            cy = ya;
                             // one row ahead: the loads fly while the next ~s rows are computed
                             fetch(min(y1 + 1, h - 1));
                         }
+                        cy = ya;
+                    }
+                    if (act) {
                         float4 iv[CI];
 #pragma unroll
                         for (int j = 0; j < CI; ++j)
