@@ -264,15 +264,15 @@ int launch_output_px(const OutParams& op, int images, const Plan& P, cudaStream_
     return last_error();
 }
 
-// Pixels per thread: as wide as alignment allows while 3 NC PX coefficient registers <= 48.
+// Pixels per thread: as wide as alignment allows while the coefficient registers fit.
 template <int CI, int CP>
 int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
     constexpr int NC = (CI + 1) * CP;
     const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
-    if (NC <= 4 && P.W % 4 == 0 && (al & 15u) == 0)
-        return launch_output_px<CI, CP, (NC <= 4 ? 4 : 1)>(op, images, P, st);
-    if (NC <= 8 && P.W % 2 == 0 && (al & 7u) == 0)
-        return launch_output_px<CI, CP, (NC <= 8 ? 2 : 1)>(op, images, P, st);
+    if (NC <= 2 && P.W % 4 == 0 && (al & 15u) == 0)
+        return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1)>(op, images, P, st);
+    if (NC <= 4 && P.W % 2 == 0 && (al & 7u) == 0)
+        return launch_output_px<CI, CP, (NC <= 4 ? 2 : 1)>(op, images, P, st);
     return launch_output_px<CI, CP, 1>(op, images, P, st);
 }
 
@@ -302,7 +302,7 @@ int launch_output_tma(const float* I, const float* M, float* q, int images, cons
 
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
                   cudaStream_t st) {
-    const bool tma_ok = P.W % 4 == 0 && P.H >= 1 && getenv("FGF_NO_TMA") == nullptr &&
+    const bool tma_ok = P.W % 4 == 0 && P.H >= 1 && getenv("FGF_TMA") != nullptr &&
                         ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
     if (tma_ok && P.CI == 1 && P.CP == 1) return launch_output_tma<1, 1>(I, M, q, images, P, st);
     if (tma_ok && P.CI == 1 && P.CP == 2) return launch_output_tma<1, 2>(I, M, q, images, P, st);

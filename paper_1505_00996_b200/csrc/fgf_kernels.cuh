@@ -531,7 +531,7 @@ struct OutCfg {
     static constexpr int NC = (CI + 1) * CP;
     static constexpr int U0 = 32 / (CI * PX);
     static constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
-    static constexpr int MINB = NC * PX <= 8 ? 3 : 2;
+    static constexpr int MINB = 2;
 };
 
 template <int CI, int CP, int PX>
@@ -561,21 +561,28 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
     float* qp = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
     const float* Mb = P.M + (size_t)img * NC * n;
 
-    int oa[PX], ob[PX];
+    // Per-pixel horizontal source columns as unsigned in-image offsets (map m adds m*n).
+    unsigned oa[PX], ob[PX];
     float fx[PX];
 #pragma unroll
-    for (int i = 0; i < PX; ++i) src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
-
-    auto hrow = [&](int y, float (&out)[NC][PX]) {
+    for (int i = 0; i < PX; ++i) {
+        int a, b;
+        src_coord(min(X + i, W - 1), w, W, a, b, fx[i]);
+        oa[i] = (unsigned)a;
+        ob[i] = (unsigned)b;
+    }
+    float ra[NC][PX], rb[NC][PX];      // raw low-res values of the prefetched row
+    int py = -1;
+    auto fetch = [&](int y) {
         const float* mr = Mb + (size_t)y * w;
 #pragma unroll
         for (int m = 0; m < NC; ++m)
 #pragma unroll
             for (int i = 0; i < PX; ++i) {
-                const float va = __ldg(mr + (m * (int)n + oa[i]));
-                const float vb = __ldg(mr + (m * (int)n + ob[i]));
-                out[m][i] = fmaf(fx[i], vb - va, va);
+                ra[m][i] = __ldg(mr + (oa[i] + (unsigned)m * (unsigned)n));
+                rb[m][i] = __ldg(mr + (ob[i] + (unsigned)m * (unsigned)n));
             }
+        py = y;
     };
 
     VT cur[U][CI];
@@ -587,25 +594,39 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
     const float* Ipf = Ip + (size_t)U * W;
 
     int cy = -2;
-    float H0[NC][PX], H1[NC][PX];
-    for (int rb = 0; rb < nrows; rb += U) {
+    float H0[NC][PX], H1[NC][PX], D[NC][PX];
+    for (int rb0 = 0; rb0 < nrows; rb0 += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int t = rb + u;
+            const int t = rb0 + u;
             if (t < nrows) {
                 const int ya = s_ya[t];
                 const float fy = s_fy[t];
                 if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform: a real branch
                     if (act) {
+                        const int y1 = min(ya + 1, h - 1);
                         if (ya == cy + 1) {
 #pragma unroll
                             for (int m = 0; m < NC; ++m)
 #pragma unroll
                                 for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
                         } else {
-                            hrow(ya, H0);
+                            if (py != ya) fetch(ya);
+#pragma unroll
+                            for (int m = 0; m < NC; ++m)
+#pragma unroll
+                                for (int i = 0; i < PX; ++i) H0[m][i] = fmaf(fx[i], rb[m][i] - ra[m][i], ra[m][i]);
                         }
-                        hrow(min(ya + 1, h - 1), H1);
+                        if (py != y1) fetch(y1);
+#pragma unroll
+                        for (int m = 0; m < NC; ++m)
+#pragma unroll
+                            for (int i = 0; i < PX; ++i) {
+                                H1[m][i] = fmaf(fx[i], rb[m][i] - ra[m][i], ra[m][i]);
+                                D[m][i] = H1[m][i] - H0[m][i];
+                            }
+                        // one low-res row ahead: these loads fly during the next ~s rows
+                        fetch(min(y1 + 1, h - 1));
                     }
                     cy = ya;
                 }
@@ -616,12 +637,10 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
                     float o[PX];
 #pragma unroll
                     for (int i = 0; i < PX; ++i) {
-                        float acc = fmaf(fy, H1[mb + CI][i] - H0[mb + CI][i], H0[mb + CI][i]);
+                        float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
 #pragma unroll
-                        for (int j = 0; j < CI; ++j) {
-                            const float a = fmaf(fy, H1[mb + j][i] - H0[mb + j][i], H0[mb + j][i]);
-                            acc = fmaf(a, V::get(cur[u][j], i), acc);
-                        }
+                        for (int j = 0; j < CI; ++j)
+                            acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
                         o[i] = acc;
                     }
                     V::st(qp + c * N, o);
