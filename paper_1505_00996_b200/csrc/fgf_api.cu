@@ -255,11 +255,51 @@ int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t 
     return FGF_ERR_SHAPE;
 }
 
+// Largest low-res rectangle (rows x cols) a CTA of TR rows and `cols` pixels touches (R5).
+int lowres_span(int T, int n_dst, int n_src) {
+    auto lo = [&](int d) {
+        long long num = (long long)(2 * d + 1) * n_src - n_dst;
+        if (num <= 0) return 0;
+        long long q = num / (2LL * n_dst);
+        return (int)std::min<long long>(q, n_src - 1);
+    };
+    int best = 1;
+    for (int d0 = 0; d0 < n_dst; d0 += T) {
+        int dl = std::min(n_dst, d0 + T) - 1;
+        best = std::max(best, std::min(lo(dl) + 1, n_src - 1) - lo(d0) + 1);
+    }
+    return best;
+}
+
+constexpr size_t kOutSmemBudget = 44 * 1024;
+
 template <int CI, int CP, int PX>
-int launch_output_px(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
-    dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + P.TR - 1) / P.TR, images);
+int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream_t st) {
+    constexpr int NC = (CI + 1) * CP;
+    OutParams op = op0;
+    const bool s1 = P.h == P.H && P.w == P.W;
+    size_t smem = 0;
+    if (s1) {
+        op.TR = 64;
+    } else {
+        const int ncl = lowres_span(256 * PX, P.W, P.w);
+        op.TR = 8;
+        for (int tr = kMaxTR; tr >= 8; tr /= 2) {
+            const size_t b = (size_t)lowres_span(tr, P.H, P.h) * NC * ncl * sizeof(float);
+            if (b <= kOutSmemBudget) { op.TR = tr; break; }
+        }
+        smem = (size_t)lowres_span(op.TR, P.H, P.h) * NC * ncl * sizeof(float);
+        if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+    }
+    dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
     ProfScope ps(KIND_OUT, st);
-    output_kernel<CI, CP, PX><<<grid, 256, 0, st>>>(op);
+    if (s1) {
+        output_kernel<CI, CP, PX, true><<<grid, 256, 0, st>>>(op);
+    } else {
+        auto kern = output_kernel<CI, CP, PX, false>;
+        set_smem(kern, smem);
+        kern<<<grid, 256, smem, st>>>(op);
+    }
     ++g_last_launches;
     return last_error();
 }
@@ -268,7 +308,8 @@ int launch_output_px(const OutParams& op, int images, const Plan& P, cudaStream_
 template <int CI, int CP>
 int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
     constexpr int NC = (CI + 1) * CP;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
+    const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q) |
+                         reinterpret_cast<uintptr_t>(op.M);
     if (NC <= 2 && P.W % 4 == 0 && (al & 15u) == 0)
         return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1)>(op, images, P, st);
     if (NC <= 4 && P.W % 2 == 0 && (al & 7u) == 0)
@@ -276,37 +317,8 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     return launch_output_px<CI, CP, 1>(op, images, P, st);
 }
 
-int g_num_sms = 0;
-
-template <int CI, int CP>
-int launch_output_tma(const float* I, const float* M, float* q, int images, const Plan& P,
-                      cudaStream_t st) {
-    using Cfg = TmaCfg<CI, CP>;
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    TmaOutParams tp{I, M, q, P.H, P.W, P.h, P.w, images, 32, (P.W + 1023) / 1024, 1};
-    const int bands = (P.H + tp.TR - 1) / tp.TR;
-    const long long items = (long long)images * bands;
-    tp.cpb = (int)std::max<long long>(1, std::min<long long>(items, g_num_sms / tp.ncb));
-    auto kern = output_tma_kernel<CI, CP>;
-    set_smem(kern, Cfg::SMEM);
-    ProfScope ps(KIND_OUT, st);
-    kern<<<tp.ncb * tp.cpb, 256, Cfg::SMEM, st>>>(tp);
-    ++g_last_launches;
-    return last_error();
-}
-
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
                   cudaStream_t st) {
-    const bool tma_ok = P.W % 4 == 0 && P.H >= 1 && getenv("FGF_TMA") != nullptr &&
-                        ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(q)) & 15u) == 0;
-    if (tma_ok && P.CI == 1 && P.CP == 1) return launch_output_tma<1, 1>(I, M, q, images, P, st);
-    if (tma_ok && P.CI == 1 && P.CP == 2) return launch_output_tma<1, 2>(I, M, q, images, P, st);
-    if (tma_ok && P.CI == 3 && P.CP == 1) return launch_output_tma<3, 1>(I, M, q, images, P, st);
     OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR};
     switch (P.CI * 10 + P.CP) {
         case 11: return launch_output_t<1, 1>(op, images, P, st);

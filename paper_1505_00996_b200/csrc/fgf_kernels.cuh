@@ -515,132 +515,169 @@ struct VecT<4> {
     }
 };
 
-// Column walker.  Each thread owns PX consecutive pixels of a row and walks TR rows down
-// the image.  Their horizontal source coordinates are fixed, so the horizontally
+// Column walker.  Each thread owns PX consecutive pixels of a row and walks the TR rows of
+// its CTA's band.  Their horizontal source coordinates are fixed, so the horizontally
 // interpolated coefficient rows H0 = Hx(y0), H1 = Hx(y1) live in registers and are
 // refreshed only when the low-res row pair changes (every ~s rows; the row table is in
-// shared memory, so that test is CTA-uniform).  Per pixel and map the upsample is then
-// A = H0 + fy (H1 - H0) and q_c = sum_j A_{c,j} I_j + A_{c,CI}.  Full-resolution
-// rows of I are prefetched U rows ahead in a rolling register ring with streaming
-// (evict-first) loads; q is written with streaming stores.
-// grid (ceil(W / (256 PX)), ceil(H / TR), images), block 256, TR <= kMaxTR.
+// shared memory and the test is a warp vote, so the branch is CTA-uniform).  The low-res
+// coefficient rows the band touches are staged into shared memory once per CTA (coalesced
+// loads issued right after the first image rows), so refreshes never wait on L2.  Per pixel
+// and map the upsample is then A = H0 + fy (H1 - H0) and q_c = sum_j A_{c,j} I_j + A_{c,CI}
+// (P:84-86).  Full-resolution rows of I are prefetched U rows ahead in a rolling register
+// ring with streaming (evict-first) loads; q is written with streaming stores.
+// S1 (s = 1, h = H, w = W): the upsample is the identity, A = M; the maps are streamed with I.
+// grid (ceil(W / (256 PX)), ceil(H / TR), images), block 256, TR <= kMaxTR,
+// dynamic smem nrl * NC * ncl floats (host-computed maxima; none when S1).
 constexpr int kMaxTR = 128;
 
 template <int CI, int CP, int PX>
 struct OutCfg {
     static constexpr int NC = (CI + 1) * CP;
-    static constexpr int U0 = 32 / (CI * PX);
+    static constexpr int U0 = 16 / (CI * PX);
     static constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
-    static constexpr int MINB = 2;
+    static constexpr int MINB = NC * PX <= 8 ? 3 : 2;
 };
 
-template <int CI, int CP, int PX>
-__global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel(OutParams P) {
+// U_ / MINB_ override the defaults (rows in flight per thread, CTAs per SM for registers).
+// ABL: ablation switch for the development microbenchmark (0 = the real kernel; 1 = skip
+// the coefficient refresh; 2 = q = I copy in the same access pattern).
+template <int CI, int CP, int PX, bool S1, int U_ = 0, int MINB_ = 0, int ABL = 0>
+__global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB)) output_kernel(OutParams P) {
     constexpr int NC = OutCfg<CI, CP, PX>::NC;
-    constexpr int U = OutCfg<CI, CP, PX>::U;
+    constexpr int U = U_ ? U_ : OutCfg<CI, CP, PX>::U;
+    constexpr int NL = S1 ? CI + NC : CI;        // planes streamed per row
     using V = VecT<PX>;
     using VT = typename V::T;
     __shared__ int s_ya[kMaxTR];
     __shared__ float s_fy[kMaxTR];
+    extern __shared__ float Ms[];                // [nrl][NC][ncl]
     const int H = P.H, W = P.W, h = P.h, w = P.w;
     const int Y0 = blockIdx.y * P.TR;
     const int nrows = min(P.TR, H - Y0);
-    for (int t = threadIdx.x; t < nrows; t += 256) {
-        int ya, yb;
-        float fy;
-        src_coord(Y0 + t, h, H, ya, yb, fy);
-        s_ya[t] = ya;
-        s_fy[t] = fy;
-    }
-    __syncthreads();
-    const bool act = (blockIdx.x * 256 + threadIdx.x) * PX < W;
-    const int X = act ? (blockIdx.x * 256 + threadIdx.x) * PX : 0;
+    const int X0 = blockIdx.x * 256 * PX;
+    const bool act = X0 + threadIdx.x * PX < W;
+    const int X = act ? X0 + threadIdx.x * PX : X0;
     const int img = blockIdx.z;
     const size_t N = (size_t)H * W, n = (size_t)h * w;
     const float* Ip = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
     float* qp = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
     const float* Mb = P.M + (size_t)img * NC * n;
+    const float* Mp = Mb + (size_t)Y0 * W + X;   // S1 only: maps have the image's geometry
 
-    // Per-pixel horizontal source columns as unsigned in-image offsets (map m adds m*n).
-    unsigned oa[PX], ob[PX];
-    float fx[PX];
-#pragma unroll
-    for (int i = 0; i < PX; ++i) {
-        int a, b;
-        src_coord(min(X + i, W - 1), w, W, a, b, fx[i]);
-        oa[i] = (unsigned)a;
-        ob[i] = (unsigned)b;
-    }
-    float ra[NC][PX], rb[NC][PX];      // raw low-res values of the prefetched row
-    int py = -1;
-    auto fetch = [&](int y) {
-        const float* mr = Mb + (size_t)y * w;
-#pragma unroll
-        for (int m = 0; m < NC; ++m)
-#pragma unroll
-            for (int i = 0; i < PX; ++i) {
-                ra[m][i] = __ldg(mr + (oa[i] + (unsigned)m * (unsigned)n));
-                rb[m][i] = __ldg(mr + (ob[i] + (unsigned)m * (unsigned)n));
-            }
-        py = y;
+    // Plane j of the streamed row: I planes, then (S1) the coefficient maps.
+    auto plane_ptr = [&](const float* base_row, int j) -> const float* {
+        return (!S1 || j < CI) ? base_row + (size_t)j * N : Mp + (base_row - Ip) + (size_t)(j - CI) * n;
     };
 
-    VT cur[U][CI];
+    // Issue the first U rows before anything else.
+    VT cur[U][NL];
 #pragma unroll
     for (int u = 0; u < U; ++u)
         if (act && u < nrows)
 #pragma unroll
-            for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ip + j * N + (size_t)u * W);
-    const float* Ipf = Ip + (size_t)U * W;
+            for (int j = 0; j < NL; ++j) cur[u][j] = V::ld(plane_ptr(Ip + (size_t)u * W, j));
 
+    int oa[PX], ob[PX];
+    float fx[PX];
+    int ylo = 0, ncl = 0;
+    if (!S1) {
+        // Row table and the low-res rectangle [ylo, yhi] x [xlo, xhi] this CTA touches.
+        for (int t = threadIdx.x; t < nrows; t += 256) {
+            int ya, yb;
+            float fy;
+            src_coord(Y0 + t, h, H, ya, yb, fy);
+            s_ya[t] = ya;
+            s_fy[t] = fy;
+        }
+        int yd, yhi, xlo, xd, xhi;
+        float fd;
+        src_coord(Y0, h, H, ylo, yd, fd);
+        src_coord(Y0 + nrows - 1, h, H, yd, yhi, fd);
+        src_coord(X0, w, W, xlo, xd, fd);
+        src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
+        const int nrl = yhi - ylo + 1;
+        ncl = xhi - xlo + 1;
+        for (int idx = threadIdx.x; idx < nrl * NC * ncl; idx += 256) {
+            const int xx = idx % ncl, rm = idx / ncl;
+            const int m = rm % NC, rr = rm / NC;
+            Ms[idx] = __ldg(Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo + xx);
+        }
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+            src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
+            oa[i] -= xlo;      // local columns in the staged rectangle
+            ob[i] -= xlo;
+        }
+        __syncthreads();
+    }
+
+    const float* Ipf = Ip + (size_t)U * W;
     int cy = -2;
     float H0[NC][PX], H1[NC][PX], D[NC][PX];
+    auto hrow = [&](int y, float (&out)[NC][PX]) {
+        const float* mr = Ms + (size_t)(y - ylo) * NC * ncl;
+#pragma unroll
+        for (int m = 0; m < NC; ++m)
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                const float va = mr[m * ncl + oa[i]], vb = mr[m * ncl + ob[i]];
+                out[m][i] = fmaf(fx[i], vb - va, va);
+            }
+    };
     for (int rb0 = 0; rb0 < nrows; rb0 += U) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = rb0 + u;
             if (t < nrows) {
-                const int ya = s_ya[t];
-                const float fy = s_fy[t];
-                if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform: a real branch
-                    if (act) {
-                        const int y1 = min(ya + 1, h - 1);
-                        if (ya == cy + 1) {
+                float fy = 0.0f;
+                if (!S1) {
+                    const int ya = s_ya[t];
+                    fy = s_fy[t];
+                    if (ABL == 0 && __any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform branch
+                        if (act) {
+                            if (ya == cy + 1) {
 #pragma unroll
-                            for (int m = 0; m < NC; ++m)
+                                for (int m = 0; m < NC; ++m)
 #pragma unroll
-                                for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
-                        } else {
-                            if (py != ya) fetch(ya);
-#pragma unroll
-                            for (int m = 0; m < NC; ++m)
-#pragma unroll
-                                for (int i = 0; i < PX; ++i) H0[m][i] = fmaf(fx[i], rb[m][i] - ra[m][i], ra[m][i]);
-                        }
-                        if (py != y1) fetch(y1);
-#pragma unroll
-                        for (int m = 0; m < NC; ++m)
-#pragma unroll
-                            for (int i = 0; i < PX; ++i) {
-                                H1[m][i] = fmaf(fx[i], rb[m][i] - ra[m][i], ra[m][i]);
-                                D[m][i] = H1[m][i] - H0[m][i];
+                                    for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+                            } else {
+                                hrow(ya, H0);
                             }
-                        // one low-res row ahead: these loads fly during the next ~s rows
-                        fetch(min(y1 + 1, h - 1));
+                            hrow(min(ya + 1, h - 1), H1);
+#pragma unroll
+                            for (int m = 0; m < NC; ++m)
+#pragma unroll
+                                for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+                        }
+                        cy = ya;
                     }
-                    cy = ya;
                 }
                 if (!act) continue;
+                if (ABL != 0 && t == 0) {
+#pragma unroll
+                    for (int m = 0; m < NC; ++m)
+#pragma unroll
+                        for (int i = 0; i < PX; ++i) { H0[m][i] = 0.5f; D[m][i] = 0.25f; }
+                }
 #pragma unroll
                 for (int c = 0; c < CP; ++c) {
                     const int mb = c * (CI + 1);
                     float o[PX];
 #pragma unroll
                     for (int i = 0; i < PX; ++i) {
-                        float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+                        if (ABL == 2) { o[i] = V::get(cur[u][0], i); continue; }
+                        float acc;
+                        if (S1) {
+                            acc = V::get(cur[u][CI + mb + CI], i);
 #pragma unroll
-                        for (int j = 0; j < CI; ++j)
-                            acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
+                            for (int j = 0; j < CI; ++j)
+                                acc = fmaf(V::get(cur[u][CI + mb + j], i), V::get(cur[u][j], i), acc);
+                        } else {
+                            acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+#pragma unroll
+                            for (int j = 0; j < CI; ++j)
+                                acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
+                        }
                         o[i] = acc;
                     }
                     V::st(qp + c * N, o);
@@ -649,7 +686,7 @@ __global__ void __launch_bounds__(256, (OutCfg<CI, CP, PX>::MINB)) output_kernel
                 // Rolling prefetch: this register slot now takes row t + U.
                 if (t + U < nrows)
 #pragma unroll
-                    for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(Ipf + j * N);
+                    for (int j = 0; j < NL; ++j) cur[u][j] = V::ld(plane_ptr(Ipf, j));
                 Ipf += W;
             }
         }
