@@ -175,7 +175,8 @@ struct StripParams {
 };
 
 // Rows per batch G (each warp slides along one row of a batch), odd run length K, smem.
-template <int MODE, int CI, int CP, int NT>
+// G_ / MINB_ override the defaults (development microbenchmark).
+template <int MODE, int CI, int CP, int NT, int G_ = 0, int MINB_ = 0>
 struct StripConfig {
     using T = StripTraits<MODE, CI, CP>;
     static constexpr int NMAP = T::NMAP;
@@ -185,11 +186,12 @@ struct StripConfig {
     static constexpr int ROWB = NMAP * VPMAX * 8 + NOUT * NT * 4;
     static constexpr int G0 = (160 * 1024) / ROWB;
     static constexpr int G1 = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));
-    static constexpr int G = G1 > NW ? NW : G1;
+    static constexpr int G2 = (NMAP <= 6 && G1 > 4) ? 4 : G1;    // favour occupancy (measured)
+    static constexpr int G = G_ ? G_ : (G2 > NW ? NW : G2);
     static constexpr int WPR = NW / G;                           // warps per row
     static constexpr int K = G == 8 ? 9 : (G == 4 ? 5 : (G == 2 ? 3 : 1));
     static constexpr int WB = T::NIN <= 4 ? 8 : (T::NIN <= 8 ? 4 : 2);
-    static constexpr int MINB = NMAP <= 6 ? 2 : 1;
+    static constexpr int MINB = MINB_ ? MINB_ : (NMAP <= 6 ? (NT == 256 ? 4 : 2) : 1);
     // dynamic smem for padded row length VP
     static size_t smem(int VP) {
         return (size_t)G * NMAP * VP * 8 + (size_t)G * NOUT * NT * 4 + (size_t)NT * 8;
@@ -284,10 +286,10 @@ __device__ __forceinline__ void load_row(const float* bI, const float* bP, int o
 }
 
 // grid (strips, segments, images); block NT.
-template <int MODE, int CI, int CP, int NT>
-__global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT>::MINB)) box_strip_kernel(StripParams P) {
+template <int MODE, int CI, int CP, int NT, int G_ = 0, int MINB_ = 0>
+__global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>::MINB)) box_strip_kernel(StripParams P) {
     using T = StripTraits<MODE, CI, CP>;
-    using C = StripConfig<MODE, CI, CP, NT>;
+    using C = StripConfig<MODE, CI, CP, NT, G_, MINB_>;
     constexpr int NMAP = T::NMAP;
     constexpr int NIN = T::NIN;
     constexpr int NOUT = T::NOUT;
