@@ -351,7 +351,7 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except Exception:
         avail = 64 << 30
-    Be = int(max(1, min(B, (avail // max(1, world)) // 4 // per_img)))
+    Be = int(max(1, min(B, 64, (avail // max(1, world)) // 4 // per_img)))
     Id, pd = synth.make_batch(args.config, torch.device("cuda", local), batch=Be, first=rank * B)
     Ih = Id.cpu().pin_memory()
     ph = Ih if args.config == 0 else pd.cpu().pin_memory()
