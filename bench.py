@@ -141,7 +141,7 @@ def cpu_baseline(cfg, prm, budget_s=12.0):
     import oracle
     oracle.build()
     secs, px, n = 0.0, 0, 0
-    while secs < budget_s and n < 16:
+    while secs < budget_s and n < 64:
         s1, p1 = run_oracle_images(cfg, prm, 1, first=n)
         secs += s1
         px += p1
@@ -298,7 +298,7 @@ def main():
             tj = json.load(open(tpath))
             key = f"{c['name']}_s{s}"
             if key in tj:
-                traffic = tj[key]["dram_bytes_per_launch"]
+                traffic = tj[key]["dram_bytes_per_image"] * imgs_per_launch
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "kernel": "output_kernel (K4: bilinear upsample + q = A.I + B)",
