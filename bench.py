@@ -218,6 +218,9 @@ def main():
         if world > 1:
             dist.barrier()
 
+    if args.config == 5:
+        return band_main(args, fgf, torch, dist, world, rank, local, dev, barrier)
+
     c, prm, B = workload(args.config, args.s, args.batch)
     H, W, CI, CP = c["H"], c["W"], c["C_I"], c["C_p"]
     r, eps, s, sub = prm["r"], prm["eps"], prm["s"], prm["sub_mode"]
@@ -335,6 +338,58 @@ def main():
                 "roofline": roofline, "hbm_whole_filter": whole, "kernels": kern,
                 "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
                 "device": props.name}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
+    """BASELINE.json config 4b: ONE 16384^2 image split into row bands across the ranks, with
+    the 2r'+1-row low-res halo exchanged over torch.distributed P2P (NCCL over NVLink).  Strong
+    scaling (the image is fixed); value = the image's pixels / max-over-ranks step time."""
+    import synth
+    from paper_1505_00996_b200 import bands
+    c, prm, _ = workload(5, args.s, None)
+    H, W = c["H"], c["W"]
+    r, eps, s, sub = prm["r"], prm["eps"], prm["s"], prm["sub_mode"]
+    pl = bands.plan_band(H, W, r, s, world, rank)
+    I, p = synth.make_batch(5, dev)
+    I_own = I[:, :, pl.Y0:pl.Y1].contiguous()
+    p_own = p[:, :, pl.Y0:pl.Y1].contiguous()
+    del I, p
+    ex = bands.DistExchange(rank, world)
+    backend = bands.GpuBackend()
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return bands.filter_band(I_own, p_own, r, eps, s, sub, H, rank, world, ex, backend)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    if rank == 0:
+        line = {"metric": METRIC, "value": H * W / (ms / 1e3) / 1e6, "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": c["name"], "H": H, "W": W, "r": r, "eps": eps, "s": s,
+                           "parallelism": f"row bands x{world}, halo {pl.halo} low-res rows "
+                                          f"over torch.distributed P2P",
+                           "l2": "inputs larger than L2 (no flush needed)"}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -110,6 +110,35 @@ int fgf_coefficients(const float* I, const float* p, float* mean_ab, int batch, 
 int fgf_upsample_output(const float* I, const float* mean_ab, float* q, int batch, int H,
                         int W, int C_I, int C_p, int s, void* cuda_stream);
 
+/* ---- Stage entry points for the row-band (multi-GPU, single huge image) path ----
+ * A rank that owns full-resolution rows [Y0, Y0 + rows) of an H_total x W image subsamples
+ * them (fgf_subsample), exchanges 2r'+1 low-res halo rows of I', p' with its neighbours,
+ * runs fgf_lowres_mean on the extended low-res band, and finishes its own rows with
+ * fgf_upsample_output_rows, which applies the GLOBAL vertical map of R5. */
+
+/* Step 1 (R3/R4) on `planes` DEVICE planes of H x W -> ceil(H/s) x ceil(W/s).
+ * s = 1 copies.  Band rows must start on a multiple of s for the grid to be global. */
+int fgf_subsample(const float* src, float* dst, int planes, int H, int W, int s, int sub_mode,
+                  void* cuda_stream);
+
+/* Workspace bytes for fgf_lowres_mean. */
+size_t fgf_lowres_workspace_bytes(int batch, int h, int w, int C_I, int C_p);
+
+/* Steps 2-5 on given DEVICE low-res planes Is [batch][C_I][h][w] and
+ * ps [batch][C_p][h][w] with low-res radius r_low (= r'); writes mean_ab
+ * [batch][C_p][C_I+1][h][w].  Windows are clipped at the buffer's own bounds. */
+int fgf_lowres_mean(const float* Is, const float* ps, float* mean_ab, int batch, int h, int w,
+                    int C_I, int C_p, int r_low, double eps, void* workspace, size_t ws_bytes,
+                    void* cuda_stream);
+
+/* Steps 6-7 for full-resolution rows [Y0, Y0 + rows) of an image of height H_total
+ * (I, q: DEVICE [batch][C][rows][W]) whose low-res height is h_total and width w, from a maps
+ * buffer holding global low-res rows [y0_maps, y0_maps + h_maps) (DEVICE
+ * [batch][C_p][C_I+1][h_maps][w]).  FGF_ERR_PARAM if the rows need low-res rows outside it. */
+int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int batch, int rows,
+                             int W, int C_I, int C_p, int H_total, int h_total, int w, int Y0,
+                             int y0_maps, int h_maps, void* cuda_stream);
+
 /* Diagnostics (single-threaded use): per-kernel CUDA-event timing of the launches this
  * process enqueues.  fgf_profile_enable(1) clears old records and starts recording an event
  * pair around every kernel launch on its launching stream; fgf_profile_enable(0) stops.

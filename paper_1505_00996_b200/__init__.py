@@ -38,7 +38,8 @@ FGF_SUB_BILINEAR = 1
 # Every symbol include/fgf.h declares (tests check the library exports each one).
 EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_host",
            "fgf_coefficients", "fgf_upsample_output", "fgf_last_launch_count", "fgf_status_str",
-           "fgf_version", "fgf_profile_enable", "fgf_profile_read")
+           "fgf_version", "fgf_profile_enable", "fgf_profile_read", "fgf_subsample",
+           "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output")
 
 _P = ctypes.c_void_p
@@ -64,6 +65,14 @@ _lib.fgf_profile_enable.argtypes = [_i]
 _lib.fgf_profile_enable.restype = _i
 _lib.fgf_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int), _i]
 _lib.fgf_profile_read.restype = _i
+_lib.fgf_subsample.argtypes = [_P, _P, _i, _i, _i, _i, _i, _P]
+_lib.fgf_subsample.restype = _i
+_lib.fgf_lowres_workspace_bytes.argtypes = [_i, _i, _i, _i, _i]
+_lib.fgf_lowres_workspace_bytes.restype = _sz
+_lib.fgf_lowres_mean.argtypes = [_P, _P, _P, _i, _i, _i, _i, _i, _i, _d, _P, _sz, _P]
+_lib.fgf_lowres_mean.restype = _i
+_lib.fgf_upsample_output_rows.argtypes = [_P, _P, _P] + [_i] * 12 + [_P]
+_lib.fgf_upsample_output_rows.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -170,6 +179,35 @@ def fgf_upsample_output(I, mean_ab, q, batch, H, W, C_I, C_p, s, stream=None, ch
                                   _stream(stream))
     if check:
         _check(rc, "fgf_upsample_output")
+    return rc
+
+
+def fgf_subsample(src, dst, planes, H, W, s, sub_mode=FGF_SUB_NEAREST, stream=None, check=True):
+    rc = _lib.fgf_subsample(_addr(src), _addr(dst), planes, H, W, s, sub_mode, _stream(stream))
+    if check:
+        _check(rc, "fgf_subsample")
+    return rc
+
+
+def fgf_lowres_workspace_bytes(batch, h, w, C_I, C_p) -> int:
+    return _lib.fgf_lowres_workspace_bytes(batch, h, w, C_I, C_p)
+
+
+def fgf_lowres_mean(Is, ps, mean_ab, batch, h, w, C_I, C_p, r_low, eps, workspace, ws_bytes,
+                    stream=None, check=True):
+    rc = _lib.fgf_lowres_mean(_addr(Is), _addr(ps), _addr(mean_ab), batch, h, w, C_I, C_p, r_low,
+                              float(eps), _addr(workspace), ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_lowres_mean")
+    return rc
+
+
+def fgf_upsample_output_rows(I, mean_ab, q, batch, rows, W, C_I, C_p, H_total, h_total, w, Y0,
+                             y0_maps, h_maps, stream=None, check=True):
+    rc = _lib.fgf_upsample_output_rows(_addr(I), _addr(mean_ab), _addr(q), batch, rows, W, C_I, C_p,
+                                       H_total, h_total, w, Y0, y0_maps, h_maps, _stream(stream))
+    if check:
+        _check(rc, "fgf_upsample_output_rows")
     return rc
 
 

@@ -277,7 +277,7 @@ template <int CI, int CP, int PX>
 int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream_t st) {
     constexpr int NC = (CI + 1) * CP;
     OutParams op = op0;
-    const bool s1 = P.h == P.H && P.w == P.W;
+    const bool s1 = op.hg == op.Hg && P.w == P.W;
     size_t smem = 0;
     if (s1) {
         op.TR = 64;
@@ -285,10 +285,10 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         const int ncl = lowres_span(256 * PX, P.W, P.w);
         op.TR = 8;
         for (int tr = kMaxTR; tr >= 8; tr /= 2) {
-            const size_t b = (size_t)lowres_span(tr, P.H, P.h) * NC * ncl * sizeof(float);
+            const size_t b = (size_t)lowres_span(tr, op.Hg, op.hg) * NC * ncl * sizeof(float);
             if (b <= kOutSmemBudget) { op.TR = tr; break; }
         }
-        smem = (size_t)lowres_span(op.TR, P.H, P.h) * NC * ncl * sizeof(float);
+        smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
     }
     dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
@@ -317,9 +317,16 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     return launch_output_px<CI, CP, 1>(op, images, P, st);
 }
 
+// Row band of a taller image: I/q hold rows [Yoff, Yoff + P.H) of an image of height Hg;
+// the maps buffer holds low-res rows [yoff, yoff + hm) of a low-res image of height hg.
+struct Band {
+    int Hg, hg, Yoff, yoff, hm;
+};
+
 int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
-                  cudaStream_t st) {
-    OutParams op{I, M, q, P.H, P.W, P.h, P.w, P.TR};
+                  cudaStream_t st, const Band* band = nullptr) {
+    const Band b = band ? *band : Band{P.H, P.h, 0, 0, P.h};
+    OutParams op{I, M, q, P.H, P.W, b.hm, P.w, b.Hg, b.hg, b.Yoff, b.yoff, P.TR};
     switch (P.CI * 10 + P.CP) {
         case 11: return launch_output_t<1, 1>(op, images, P, st);
         case 12: return launch_output_t<1, 2>(op, images, P, st);
@@ -617,6 +624,81 @@ int fgf_upsample_output(const float* I, const float* mean_ab, float* q, int batc
         return FGF_ERR_ALIAS;
     if (!is_device_ptr(I) || !is_device_ptr(mean_ab) || !is_device_ptr(q)) return FGF_ERR_DEVICE;
     return launch_output(I, mean_ab, q, batch, P, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_subsample(const float* src, float* dst, int planes, int H, int W, int s, int sub_mode,
+                  void* cuda_stream) {
+    g_last_launches = 0;
+    if (planes < 1 || H < 1 || W < 1) return FGF_ERR_SHAPE;
+    if (s < 1 || (sub_mode != FGF_SUB_NEAREST && sub_mode != FGF_SUB_BILINEAR)) return FGF_ERR_PARAM;
+    if (!src || !dst) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 3u) return FGF_ERR_ALIGN;
+    if (!is_device_ptr(src) || !is_device_ptr(dst)) return FGF_ERR_DEVICE;
+    const size_t N = (size_t)H * W;
+    const size_t n = (size_t)lowres_dim(H, s) * lowres_dim(W, s);
+    if (overlaps(dst, (size_t)planes * n * 4, src, (size_t)planes * N * 4)) return FGF_ERR_ALIAS;
+    if (N >= (1ull << 31)) return FGF_ERR_UNSUPPORTED;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (s == 1) {
+        if (cudaMemcpyAsync(dst, src, (size_t)planes * N * 4, cudaMemcpyDeviceToDevice, st))
+            return FGF_ERR_CUDA;
+        return FGF_OK;
+    }
+    Plan P{};
+    P.H = H; P.W = W; P.s = s; P.sub = sub_mode;
+    P.h = lowres_dim(H, s); P.w = lowres_dim(W, s);
+    return launch_subsample(src, dst, planes, P, st);
+}
+
+size_t fgf_lowres_workspace_bytes(int batch, int h, int w, int C_I, int C_p) {
+    Plan P;
+    if (make_plan(P, batch, h, w, C_I, C_p, 1, 1.0, 1, FGF_SUB_NEAREST)) return 0;
+    return plan_ws(P, false);
+}
+
+int fgf_lowres_mean(const float* Is, const float* ps, float* mean_ab, int batch, int h, int w,
+                    int C_I, int C_p, int r_low, double eps, void* workspace, size_t ws_bytes,
+                    void* cuda_stream) {
+    // Steps 2-5 on given low-res planes: exactly the s = 1 path with radius r'.
+    return fgf_coefficients(Is, ps, mean_ab, batch, h, w, C_I, C_p, r_low, eps, 1,
+                            FGF_SUB_NEAREST, workspace, ws_bytes, cuda_stream);
+}
+
+int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int batch, int rows,
+                             int W, int C_I, int C_p, int H_total, int h_total, int w, int Y0,
+                             int y0_maps, int h_maps, void* cuda_stream) {
+    g_last_launches = 0;
+    if (batch < 1 || rows < 1 || W < 1 || w < 1 || w > W || H_total < 1 || h_total < 1 ||
+        h_total > H_total || h_maps < 1)
+        return FGF_ERR_SHAPE;
+    if ((C_I != 1 && C_I != 3) || C_p < 1 || C_p > 4) return FGF_ERR_SHAPE;
+    if (Y0 < 0 || Y0 + rows > H_total || y0_maps < 0 || y0_maps + h_maps > h_total)
+        return FGF_ERR_PARAM;
+    // The rows' low-res sources (R5, global map) must lie inside the maps buffer.
+    auto src_lo = [&](int Y) {
+        long long num = (long long)(2 * Y + 1) * h_total - H_total;
+        if (num <= 0) return 0;
+        return (int)std::min<long long>(num / (2LL * H_total), h_total - 1);
+    };
+    if (src_lo(Y0) < y0_maps || std::min(src_lo(Y0 + rows - 1) + 1, h_total - 1) >= y0_maps + h_maps)
+        return FGF_ERR_PARAM;
+    if (!I || !mean_ab || !q) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(mean_ab) |
+         reinterpret_cast<uintptr_t>(q)) & 3u)
+        return FGF_ERR_ALIGN;
+    const int NC = (C_I + 1) * C_p;
+    const size_t N = (size_t)rows * W, n = (size_t)h_maps * w;
+    if (N * std::max(C_I, C_p) >= (1ull << 31) || n * NC >= (1ull << 31)) return FGF_ERR_UNSUPPORTED;
+    const size_t bq = (size_t)batch * C_p * N * 4;
+    if (overlaps(q, bq, I, (size_t)batch * C_I * N * 4) ||
+        overlaps(q, bq, mean_ab, (size_t)batch * NC * n * 4))
+        return FGF_ERR_ALIAS;
+    if (!is_device_ptr(I) || !is_device_ptr(mean_ab) || !is_device_ptr(q)) return FGF_ERR_DEVICE;
+    Plan P{};
+    P.batch = batch; P.H = rows; P.W = W; P.CI = C_I; P.CP = C_p; P.NC = NC;
+    P.h = h_maps; P.w = w; P.N = N; P.n = n; P.TR = 32;
+    const Band band{H_total, h_total, Y0, y0_maps, h_maps};
+    return launch_output(I, mean_ab, q, batch, P, static_cast<cudaStream_t>(cuda_stream), &band);
 }
 
 int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,

@@ -458,10 +458,12 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
 // ------------------------------------------------------------------ K4: upsample + output
 
 struct OutParams {
-    const float* I;        // [img][CI][H][W]
-    const float* M;        // [img][(CI+1)CP][h][w] mean maps
+    const float* I;        // [img][CI][H][W]   (H rows of the image, or of a row band)
+    const float* M;        // [img][(CI+1)CP][hm][w] mean maps (hm low-res rows)
     float* q;              // [img][CP][H][W]
-    int H, W, h, w;
+    int H, W, hm, w;       // local buffer geometry
+    int Hg, hg;            // global full-res / low-res heights (the vertical map, R5)
+    int Yoff, yoff;        // global row of local row 0 of I/q, and of the maps buffer
     int TR;                // full-resolution rows walked by each thread
 };
 
@@ -551,9 +553,10 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     using V = VecT<PX>;
     using VT = typename V::T;
     __shared__ int s_ya[kMaxTR];
+    __shared__ int s_y1[kMaxTR];
     __shared__ float s_fy[kMaxTR];
     extern __shared__ float Ms[];                // [nrl][NC][ncl]
-    const int H = P.H, W = P.W, h = P.h, w = P.w;
+    const int H = P.H, W = P.W, h = P.hm, w = P.w;
     const int Y0 = blockIdx.y * P.TR;
     const int nrows = min(P.TR, H - Y0);
     const int X0 = blockIdx.x * 256 * PX;
@@ -564,7 +567,8 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     const float* Ip = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
     float* qp = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
     const float* Mb = P.M + (size_t)img * NC * n;
-    const float* Mp = Mb + (size_t)Y0 * W + X;   // S1 only: maps have the image's geometry
+    // S1 only: the maps have the image's geometry, shifted by the band offsets
+    const float* Mp = Mb + (size_t)(P.Yoff + Y0 - P.yoff) * W + X;
 
     // Plane j of the streamed row: I planes, then (S1) the coefficient maps.
     auto plane_ptr = [&](const float* base_row, int j) -> const float* {
@@ -584,17 +588,21 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     int ylo = 0, ncl = 0;
     if (!S1) {
         // Row table and the low-res rectangle [ylo, yhi] x [xlo, xhi] this CTA touches.
+        // (global vertical map, then local to the maps buffer)
         for (int t = threadIdx.x; t < nrows; t += 256) {
             int ya, yb;
             float fy;
-            src_coord(Y0 + t, h, H, ya, yb, fy);
-            s_ya[t] = ya;
+            src_coord(P.Yoff + Y0 + t, P.hg, P.Hg, ya, yb, fy);
+            s_ya[t] = ya - P.yoff;
+            s_y1[t] = yb - P.yoff;
             s_fy[t] = fy;
         }
         int yd, yhi, xlo, xd, xhi;
         float fd;
-        src_coord(Y0, h, H, ylo, yd, fd);
-        src_coord(Y0 + nrows - 1, h, H, yd, yhi, fd);
+        src_coord(P.Yoff + Y0, P.hg, P.Hg, ylo, yd, fd);
+        src_coord(P.Yoff + Y0 + nrows - 1, P.hg, P.Hg, yd, yhi, fd);
+        ylo -= P.yoff;
+        yhi -= P.yoff;
         src_coord(X0, w, W, xlo, xd, fd);
         src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
         const int nrl = yhi - ylo + 1;
@@ -614,7 +622,7 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     }
 
     const float* Ipf = Ip + (size_t)U * W;
-    int cy = -2;
+    int cy = -2, cy1 = -2;
     float H0[NC][PX], H1[NC][PX], D[NC][PX];
     auto hrow = [&](int y, float (&out)[NC][PX]) {
         const float* mr = Ms + (size_t)(y - ylo) * NC * ncl;
@@ -637,7 +645,7 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
                     fy = s_fy[t];
                     if (ABL == 0 && __any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform branch
                         if (act) {
-                            if (ya == cy + 1) {
+                            if (ya == cy1) {
 #pragma unroll
                                 for (int m = 0; m < NC; ++m)
 #pragma unroll
@@ -645,7 +653,8 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
                             } else {
                                 hrow(ya, H0);
                             }
-                            hrow(min(ya + 1, h - 1), H1);
+                            cy1 = s_y1[t];
+                            hrow(cy1, H1);
 #pragma unroll
                             for (int m = 0; m < NC; ++m)
 #pragma unroll
