@@ -71,7 +71,7 @@ _lib.fgf_lowres_workspace_bytes.argtypes = [_i, _i, _i, _i, _i]
 _lib.fgf_lowres_workspace_bytes.restype = _sz
 _lib.fgf_lowres_mean.argtypes = [_P, _P, _P, _i, _i, _i, _i, _i, _i, _d, _P, _sz, _P]
 _lib.fgf_lowres_mean.restype = _i
-_lib.fgf_upsample_output_rows.argtypes = [_P, _P, _P] + [_i] * 12 + [_P]
+_lib.fgf_upsample_output_rows.argtypes = [_P, _P, _P] + [_i] * 11 + [_P]
 _lib.fgf_upsample_output_rows.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p

@@ -99,3 +99,20 @@ def test_workspace_bytes():
     # unsupported strip geometry (r' > 240 with w > 512)
     assert fgf.fgf_workspace_bytes(1, 2048, 2048, 1, 1, 300, 1) == 0
     assert fgf.fgf_workspace_bytes(1, 512, 512, 1, 1, 300, 1) > 0
+
+
+def header_arities():
+    """{name: number of parameters} for every prototype in include/fgf.h."""
+    txt = open(os.path.join(ROOT, "include", "fgf.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    out = {}
+    for m in re.finditer(r"\b(fgf_[a-z_]+)\s*\(([^)]*)\)\s*;", txt):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_binding_argtypes_match_header():
+    lib = fgf._lib
+    for name, n in header_arities().items():
+        assert len(getattr(lib, name).argtypes) == n, name
