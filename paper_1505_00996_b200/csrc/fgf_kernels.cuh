@@ -206,19 +206,20 @@ struct StripEpilogue;
 template <int CP>
 struct StripEpilogue<MODE_STATS, 1, CP> {
     __device__ static void emit(const double* S, double inv, double eps, float* dst, int ostride) {
+        // The cancellations (var_I, cov_Ip: P:78-79) are formed in fp64; the quotient and b
+        // (Eq.2-3) are well conditioned and are formed in fp32.
         const double mI = S[0] * inv;
-        double var = S[1] * inv - mI * mI;           // var_I
+        double var = fma(-mI, mI, S[1] * inv);       // var_I
         var = var < 0.0 ? 0.0 : var;                 // R8
-        const double den = var + eps;
+        const float rden = __frcp_rn((float)(var + eps));
+        const float mIf = (float)mI;
 #pragma unroll
         for (int c = 0; c < CP; ++c) {
             const double mp = S[2 + c] * inv;
-            const double cov = S[2 + CP + c] * inv - mI * mp;  // cov_Ip
-            // Eq.2 / P:80: the cancellations above are fp64; the quotient only needs fp32.
-            const float a = __fdiv_rn((float)cov, (float)den);
-            const double b = mp - (double)a * mI;               // Eq.3 / P:81
+            const double cov = fma(-mI, mp, S[2 + CP + c] * inv);   // cov_Ip
+            const float a = (float)cov * rden;                    // Eq.2 / P:80
             dst[(2 * c) * ostride] = a;
-            dst[(2 * c + 1) * ostride] = (float)b;
+            dst[(2 * c + 1) * ostride] = fmaf(-a, mIf, (float)mp);  // Eq.3 / P:81
         }
     }
 };
@@ -363,15 +364,22 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
     const int hg = warp % G;
     const int oc0 = ((warp / G) * 32 + lane) * K;
 
-    // Software pipeline: va/vs hold the add/subtract rows of the current batch.
+    // Software pipeline: va/vs hold the add/subtract rows of the current batch.  Branch-free:
+    // row indices are clamped into the image and rows that must not contribute (beyond the
+    // bottom, before the top, past the segment) are zeroed, which adds exactly nothing.
     float va[G][NIN], vs[G][NIN];
     auto load_batch = [&](int yb) {
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             const int yo = yb + g;
-            if (yo < ye) {
-                if (yo + R < h) load_row<MODE, CI, CP>(bI, bP, (yo + R) * row + offc, planeI, planeP, va[g]);
-                if (yo - R - 1 >= 0) load_row<MODE, CI, CP>(bI, bP, (yo - R - 1) * row + offc, planeI, planeP, vs[g]);
+            const bool oka = yo < ye && yo + R < h;
+            const bool oks = yo < ye && yo - R - 1 >= 0;
+            load_row<MODE, CI, CP>(bI, bP, min(yo + R, h - 1) * row + offc, planeI, planeP, va[g]);
+            load_row<MODE, CI, CP>(bI, bP, max(yo - R - 1, 0) * row + offc, planeI, planeP, vs[g]);
+#pragma unroll
+            for (int k = 0; k < NIN; ++k) {
+                va[g][k] = oka ? va[g][k] : 0.0f;
+                vs[g][k] = oks ? vs[g][k] : 0.0f;
             }
         }
     };
@@ -384,22 +392,14 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
         if (colthr) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                const int yo = yb + g;
-                if (yo < ye) {
-                    double pr[NMAP];
-                    if (yo + R < h) {
-                        T::products(va[g], pr);
+                double pa[NMAP], ps[NMAP];
+                T::products(va[g], pa);
+                T::products(vs[g], ps);
+                double* vrow = Vs + (size_t)g * NMAP * VP + R + tid;
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) acc[m] += pr[m];
-                    }
-                    if (yo - R - 1 >= 0) {
-                        T::products(vs[g], pr);
-#pragma unroll
-                        for (int m = 0; m < NMAP; ++m) acc[m] -= pr[m];
-                    }
-                    double* vrow = Vs + (size_t)g * NMAP * VP + R + tid;
-#pragma unroll
-                    for (int m = 0; m < NMAP; ++m) vrow[m * VP] = acc[m];
+                for (int m = 0; m < NMAP; ++m) {
+                    acc[m] += pa[m] - ps[m];
+                    vrow[m * VP] = acc[m];
                 }
             }
         }
