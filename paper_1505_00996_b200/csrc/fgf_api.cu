@@ -272,6 +272,7 @@ int lowres_span(int T, int n_dst, int n_src) {
 }
 
 constexpr size_t kOutSmemBudget = 44 * 1024;
+int g_num_sms = 0;
 
 template <int CI, int CP, int PX>
 int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream_t st) {
@@ -290,6 +291,39 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         }
         smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+    }
+    if (!s1 && getenv("FGF_NO_PERSIST") == nullptr) {
+        // persistent walker: ~2 CTAs per SM, bands of 64 rows, double-buffered staging
+        using PC = PersistCfg<CI, CP, PX>;
+        PersistParams pp{op, images, (P.W + 256 * PX - 1) / (256 * PX), 1, 0, 0};
+        pp.o.TR = 64;
+        pp.ncl = lowres_span(256 * PX, P.W, P.w);
+        pp.nrl = lowres_span(pp.o.TR, op.Hg, op.hg);
+        size_t psm = 2 * (size_t)pp.nrl * NC * pp.ncl * sizeof(float);
+        while (psm > 150 * 1024 && pp.o.TR > 8) {
+            pp.o.TR /= 2;
+            pp.nrl = lowres_span(pp.o.TR, op.Hg, op.hg);
+            psm = 2 * (size_t)pp.nrl * NC * pp.ncl * sizeof(float);
+        }
+        if (psm <= 200 * 1024) {
+            if (g_num_sms == 0) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+                if (g_num_sms <= 0) g_num_sms = 148;
+            }
+            auto kern = output_persist_kernel<CI, CP, PX>;
+            set_smem(kern, psm);
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, psm);
+            occ = std::max(1, occ);
+            const long long items = (long long)images * ((P.H + pp.o.TR - 1) / pp.o.TR);
+            pp.cpb = (int)std::max<long long>(1, std::min<long long>(items, (long long)g_num_sms * occ / pp.ncb));
+            ProfScope ps(KIND_OUT, st);
+            kern<<<pp.ncb * pp.cpb, 256, psm, st>>>(pp);
+            ++g_last_launches;
+            return last_error();
+        }
     }
     dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
     ProfScope ps(KIND_OUT, st);

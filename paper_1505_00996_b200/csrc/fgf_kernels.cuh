@@ -704,6 +704,214 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     }
 }
 
+// ------------------------------------------------------------------ K4, persistent
+//
+// Persistent column walker (s > 1).  The grid is ncb x cpb CTAs (about two per SM); CTA
+// (cb, k) owns the 256 PX-pixel column block cb and walks the bands k, k + cpb, ... of all
+// images as one continuous stream of rows.  The low-res rectangle and row table of the NEXT
+// band are staged with cp.async into the other half of a double buffer while the current
+// band streams, and the rolling U-row register prefetch of I runs across band boundaries, so
+// neither the staging latency nor a band change ever idles the HBM pipe.
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct PersistParams {
+    OutParams o;           // geometry (TR = rows per band)
+    int images, ncb, cpb;
+    int nrl, ncl;          // staged rectangle capacity (rows, cols)
+};
+
+template <int CI, int CP, int PX>
+struct PersistCfg {
+    static constexpr int NC = (CI + 1) * CP;
+    static constexpr int U0 = 32 / (CI * PX);
+    static constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
+    static constexpr int MINB = NC * PX <= 8 ? 2 : 1;
+};
+
+template <int CI, int CP, int PX>
+__global__ void __launch_bounds__(256, (PersistCfg<CI, CP, PX>::MINB)) output_persist_kernel(PersistParams PP) {
+    constexpr int NC = PersistCfg<CI, CP, PX>::NC;
+    constexpr int U = PersistCfg<CI, CP, PX>::U;
+    using V = VecT<PX>;
+    using VT = typename V::T;
+    const OutParams& P = PP.o;
+    __shared__ int s_ya[2][kMaxTR];
+    __shared__ int s_y1[2][kMaxTR];
+    __shared__ float s_fy[2][kMaxTR];
+    extern __shared__ float Msh[];                    // [2][nrl][NC][ncl]
+    const int H = P.H, W = P.W, w = P.w, TR = P.TR;
+    const size_t N = (size_t)H * W, n = (size_t)P.hm * w;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int cb = blockIdx.x % PP.ncb;
+    const int k0 = blockIdx.x / PP.ncb;
+    const int bands = (H + TR - 1) / TR;
+    const int items = PP.images * bands;
+    if (k0 >= items) return;                           // CTA-uniform
+    const int X0 = cb * 256 * PX;
+    const bool act = X0 + tid * PX < W;
+    const int X = act ? X0 + tid * PX : X0;
+    const size_t bufsz = (size_t)PP.nrl * NC * PP.ncl;
+
+    // Horizontal geometry of this column block (fixed for the CTA's lifetime).
+    int xlo, xd, xhi;
+    float fd;
+    src_coord(X0, w, W, xlo, xd, fd);
+    src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
+    const int ncl = xhi - xlo + 1;
+    int oa[PX], ob[PX];
+    float fx[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
+        src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
+        oa[i] -= xlo;
+        ob[i] -= xlo;
+    }
+
+    auto band_rows = [&](int item) { return min(TR, H - (item % bands) * TR); };
+    // Stage band `item` (row table + low-res rectangle) into buffer `b` (cp.async, no wait).
+    int ylo_b[2] = {0, 0};
+    auto stage = [&](int item, int b) {
+        if (item >= items) return;
+        const int img = item / bands, Yb = (item % bands) * TR, nr = band_rows(item);
+        for (int t = tid; t < nr; t += 256) {
+            int ya, yb;
+            float fy;
+            src_coord(P.Yoff + Yb + t, P.hg, P.Hg, ya, yb, fy);
+            s_ya[b][t] = ya - P.yoff;
+            s_y1[b][t] = yb - P.yoff;
+            s_fy[b][t] = fy;
+        }
+        int ylo, yhi, yd2;
+        float f2;
+        src_coord(P.Yoff + Yb, P.hg, P.Hg, ylo, yd2, f2);
+        src_coord(P.Yoff + Yb + nr - 1, P.hg, P.Hg, yd2, yhi, f2);
+        ylo -= P.yoff;
+        yhi -= P.yoff;
+        ylo_b[b] = ylo;
+        const float* Mb = P.M + (size_t)img * NC * n + xlo;
+        float* dst = Msh + b * bufsz;
+        const int nrm = (yhi - ylo + 1) * NC;
+        for (int rm = warp; rm < nrm; rm += 8) {
+            const int rr = rm / NC, m = rm - rr * NC;
+            const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w;
+            float* d = dst + (size_t)rm * ncl;
+            for (int xx = lane; xx < ncl; xx += 32) cp_async4(d + xx, src + xx);
+        }
+        cp_async_commit();
+    };
+
+    // Row stream: (item, t) -> pointer to the PX pixels of plane 0 of I.
+    auto row_ptr = [&](int item, int t) {
+        const int img = item / bands, Yb = (item % bands) * TR;
+        return P.I + (size_t)img * CI * N + (size_t)(Yb + t) * W + X;
+    };
+
+    stage(k0, 0);
+    cp_async_wait_all();
+    __syncthreads();
+    stage(k0 + PP.cpb, 1);
+
+    int p_item = k0, p_t = 0;                          // prefetch cursor (U rows ahead)
+    VT cur[U][CI];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (p_item < items) {
+            if (act) {
+                const float* src = row_ptr(p_item, p_t);
+#pragma unroll
+                for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(src + j * N);
+            }
+            if (++p_t >= band_rows(p_item)) { p_t = 0; p_item += PP.cpb; }
+        }
+    }
+
+    int c_item = k0, c_t = 0, buf = 0, cy = -2, cy1 = -2;
+    float H0[NC][PX], H1[NC][PX], D[NC][PX];
+    auto hrow = [&](int y, float (&out)[NC][PX]) {
+        const float* mr = Msh + buf * bufsz + (size_t)(y - ylo_b[buf]) * NC * ncl;
+#pragma unroll
+        for (int m = 0; m < NC; ++m)
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                const float va = mr[m * ncl + oa[i]], vb = mr[m * ncl + ob[i]];
+                out[m][i] = fmaf(fx[i], vb - va, va);
+            }
+    };
+    while (c_item < items) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c_item < items) {
+                if (c_t == 0 && c_item != k0) {
+                    // new band: its staging (issued one band ago) must be complete, and every
+                    // thread must be done with the old buffer before it is refilled
+                    cp_async_wait_all();
+                    __syncthreads();
+                    buf ^= 1;
+                    cy = -2;
+                    stage(c_item + PP.cpb, buf ^ 1);
+                }
+                const int ya = s_ya[buf][c_t];
+                const float fy = s_fy[buf][c_t];
+                if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform branch
+                    if (act) {
+                        if (ya == cy1) {
+#pragma unroll
+                            for (int m = 0; m < NC; ++m)
+#pragma unroll
+                                for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+                        } else {
+                            hrow(ya, H0);
+                        }
+                        cy1 = s_y1[buf][c_t];
+                        hrow(cy1, H1);
+#pragma unroll
+                        for (int m = 0; m < NC; ++m)
+#pragma unroll
+                            for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+                    }
+                    cy = ya;
+                }
+                if (act) {
+                    const int img = c_item / bands, Yb = (c_item % bands) * TR;
+                    float* qrow = P.q + (size_t)img * CP * N + (size_t)(Yb + c_t) * W + X;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) {
+                        const int mb = c * (CI + 1);
+                        float o[PX];
+#pragma unroll
+                        for (int i = 0; i < PX; ++i) {
+                            float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+#pragma unroll
+                            for (int j = 0; j < CI; ++j)
+                                acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(cur[u][j], i), acc);
+                            o[i] = acc;
+                        }
+                        V::st(qrow + c * N, o);
+                    }
+                }
+                // rolling prefetch: this slot takes the stream row U ahead
+                if (p_item < items) {
+                    if (act) {
+                        const float* src = row_ptr(p_item, p_t);
+#pragma unroll
+                        for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(src + j * N);
+                    }
+                    if (++p_t >= band_rows(p_item)) { p_t = 0; p_item += PP.cpb; }
+                }
+                if (++c_t >= band_rows(c_item)) { c_t = 0; c_item += PP.cpb; }
+            }
+        }
+    }
+    cp_async_wait_all();
+}
+
 // ------------------------------------------------------------------ K4 (TMA pipeline)
 //
 // Persistent variant of K4 for 16-byte aligned rows (W % 4 == 0).  The image is cut into

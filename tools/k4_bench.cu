@@ -61,7 +61,7 @@ int main(int argc, char** argv) {
     }
     rep("cudaMemcpy D2D", timeit([&] { cudaMemcpyAsync(q, I, B * N * 4, cudaMemcpyDeviceToDevice); }), bytes_copy);
     for (int TR : {32, 64, 128}) {
-        OutParams op{I, M, q, H, W, h, w, TR};
+        OutParams op{I, M, q, H, W, h, w, H, h, 0, 0, TR};
         dim3 g4((W + 1023) / 1024, (H + TR - 1) / TR, B);
         const size_t sm = (size_t)(TR / 4 + 3) * 2 * 259 * 4;
         char nm[64];
@@ -78,10 +78,22 @@ int main(int argc, char** argv) {
     {
         float* M1;
         CK(cudaMalloc(&M1, (size_t)2 * 2 * N * 4));
-        OutParams op{I, M1, q, H, W, H, W, 64};
+        OutParams op{I, M1, q, H, W, H, W, H, H, 0, 0, 64};
         dim3 g4((W + 1023) / 1024, (H + 63) / 64, 2);
         rep("walker-s1 PX4 (2 images)", timeit([&] { output_kernel<1, 1, 4, true><<<g4, 256>>>(op); }), 2.0 * (4.0 * N * 4));
         cudaFree(M1);
+    }
+    for (int TR : {32, 64}) {
+        OutParams o{I, M, q, H, W, h, w, H, h, 0, 0, TR};
+        const int nrl = TR / 4 + 3, ncl = 259;
+        const size_t psm = 2 * (size_t)nrl * 2 * ncl * 4;
+        auto k = output_persist_kernel<1, 1, 4>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+        int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, psm);
+        PersistParams pp{o, B, 4, sms * occ / 4, nrl, ncl};
+        char nm[64];
+        snprintf(nm, 64, "persist PX4 TR=%d occ=%d", TR, occ);
+        rep(nm, timeit([&] { k<<<pp.ncb * pp.cpb, 256, psm>>>(pp); }), bytes_k4);
     }
     {
         using Cfg = TmaCfg<1, 1>;
