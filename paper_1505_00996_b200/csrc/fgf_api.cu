@@ -291,8 +291,11 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         }
         smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
+        // optional floor on the dynamic smem: caps K4 CTAs/SM so the low-res stream's CTAs
+        // can be co-resident (experiment knob)
+        if (const char* e = getenv("FGF_K4_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
     }
-    if (!s1 && getenv("FGF_NO_PERSIST") == nullptr) {
+    if (!s1 && getenv("FGF_PERSIST") != nullptr) {
         // persistent walker: ~2 CTAs per SM, bands of 64 rows, double-buffered staging
         using PC = PersistCfg<CI, CP, PX>;
         PersistParams pp{op, images, (P.W + 256 * PX - 1) / (256 * PX), 1, 0, 0};
@@ -435,7 +438,8 @@ int get_pipe(Pipe*& out) {
     if (!pp.init) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        if (cudaStreamCreateWithPriority(&pp.low, cudaStreamNonBlocking, hi) != cudaSuccess)
+        const int prio = getenv("FGF_LOWRES_LOWPRIO") ? lo : hi;
+        if (cudaStreamCreateWithPriority(&pp.low, cudaStreamNonBlocking, prio) != cudaSuccess)
             return FGF_ERR_CUDA;
         if (cudaEventCreateWithFlags(&pp.fork, cudaEventDisableTiming)) return FGF_ERR_CUDA;
         for (int k = 0; k < 2; ++k) {

@@ -807,10 +807,14 @@ __global__ void __launch_bounds__(256, (PersistCfg<CI, CP, PX>::MINB)) output_pe
         cp_async_commit();
     };
 
-    // Row stream: (item, t) -> pointer to the PX pixels of plane 0 of I.
-    auto row_ptr = [&](int item, int t) {
+    // Band bases: (item) -> pointer to row 0 of the band at this thread's pixels.
+    auto I_base = [&](int item) {
         const int img = item / bands, Yb = (item % bands) * TR;
-        return P.I + (size_t)img * CI * N + (size_t)(Yb + t) * W + X;
+        return P.I + (size_t)img * CI * N + (size_t)Yb * W + X;
+    };
+    auto q_base = [&](int item) {
+        const int img = item / bands, Yb = (item % bands) * TR;
+        return P.q + (size_t)img * CP * N + (size_t)Yb * W + X;
     };
 
     stage(k0, 0);
@@ -818,21 +822,32 @@ __global__ void __launch_bounds__(256, (PersistCfg<CI, CP, PX>::MINB)) output_pe
     __syncthreads();
     stage(k0 + PP.cpb, 1);
 
-    int p_item = k0, p_t = 0;                          // prefetch cursor (U rows ahead)
+    // prefetch cursor (U rows ahead): band item, row pointer, rows left in the band
+    int p_item = k0, p_left = band_rows(k0);
+    const float* p_ptr = I_base(k0);
+    auto p_advance = [&]() {
+        p_ptr += W;
+        if (--p_left == 0) {
+            p_item += PP.cpb;
+            if (p_item < items) {
+                p_left = band_rows(p_item);
+                p_ptr = I_base(p_item);
+            }
+        }
+    };
     VT cur[U][CI];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (p_item < items) {
-            if (act) {
-                const float* src = row_ptr(p_item, p_t);
+            if (act)
 #pragma unroll
-                for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(src + j * N);
-            }
-            if (++p_t >= band_rows(p_item)) { p_t = 0; p_item += PP.cpb; }
+                for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(p_ptr + j * N);
+            p_advance();
         }
     }
 
-    int c_item = k0, c_t = 0, buf = 0, cy = -2, cy1 = -2;
+    int c_item = k0, c_t = 0, c_rows = band_rows(k0), buf = 0, cy = -2, cy1 = -2;
+    float* c_q = q_base(k0);
     float H0[NC][PX], H1[NC][PX], D[NC][PX];
     auto hrow = [&](int y, float (&out)[NC][PX]) {
         const float* mr = Msh + buf * bufsz + (size_t)(y - ylo_b[buf]) * NC * ncl;
@@ -879,8 +894,7 @@ __global__ void __launch_bounds__(256, (PersistCfg<CI, CP, PX>::MINB)) output_pe
                     cy = ya;
                 }
                 if (act) {
-                    const int img = c_item / bands, Yb = (c_item % bands) * TR;
-                    float* qrow = P.q + (size_t)img * CP * N + (size_t)(Yb + c_t) * W + X;
+                    float* qrow = c_q;
 #pragma unroll
                     for (int c = 0; c < CP; ++c) {
                         const int mb = c * (CI + 1);
@@ -898,14 +912,20 @@ __global__ void __launch_bounds__(256, (PersistCfg<CI, CP, PX>::MINB)) output_pe
                 }
                 // rolling prefetch: this slot takes the stream row U ahead
                 if (p_item < items) {
-                    if (act) {
-                        const float* src = row_ptr(p_item, p_t);
+                    if (act)
 #pragma unroll
-                        for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(src + j * N);
-                    }
-                    if (++p_t >= band_rows(p_item)) { p_t = 0; p_item += PP.cpb; }
+                        for (int j = 0; j < CI; ++j) cur[u][j] = V::ld(p_ptr + j * N);
+                    p_advance();
                 }
-                if (++c_t >= band_rows(c_item)) { c_t = 0; c_item += PP.cpb; }
+                c_q += W;
+                if (++c_t >= c_rows) {
+                    c_t = 0;
+                    c_item += PP.cpb;
+                    if (c_item < items) {
+                        c_rows = band_rows(c_item);
+                        c_q = q_base(c_item);
+                    }
+                }
             }
         }
     }
