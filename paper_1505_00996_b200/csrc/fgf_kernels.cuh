@@ -471,6 +471,25 @@ struct OutParams {
 // integers: c = ((2d+1) n_src - n_dst) / (2 n_dst), clamped to [0, n_src-1].
 __device__ __forceinline__ void src_coord(int d, int n_src, int n_dst, int& i0, int& i1,
                                           float& f) {
+    if ((long long)(2 * n_dst + 1) * n_src < (1LL << 31)) {   // exact in 32-bit arithmetic
+        const int num = (2 * d + 1) * n_src - n_dst;
+        const int den = 2 * n_dst;
+        if (num <= 0) {
+            i0 = 0;
+            f = 0.0f;
+        } else {
+            const int q = (int)((unsigned)num / (unsigned)den);
+            if (q >= n_src - 1) {
+                i0 = n_src - 1;
+                f = 0.0f;
+            } else {
+                i0 = q;
+                f = (float)(num - q * den) / (float)den;
+            }
+        }
+        i1 = min(i0 + 1, n_src - 1);
+        return;
+    }
     const long long num = (long long)(2 * d + 1) * n_src - n_dst;
     const long long den = 2LL * n_dst;
     if (num <= 0) {
@@ -534,12 +553,15 @@ struct VecT<4> {
 // dynamic smem nrl * NC * ncl floats (host-computed maxima; none when S1).
 constexpr int kMaxTR = 128;
 
+// Defaults measured with tools/k4_bench.cu (profiles/round1/k4_microbench.txt): more
+// resident warps beat deeper per-thread prefetch; 4 CTAs/SM is the register limit before
+// spills.
 template <int CI, int CP, int PX>
 struct OutCfg {
     static constexpr int NC = (CI + 1) * CP;
-    static constexpr int U0 = 16 / (CI * PX);
+    static constexpr int U0 = 8 / (CI * PX);
     static constexpr int U = U0 > 8 ? 8 : (U0 < 2 ? 2 : U0);
-    static constexpr int MINB = NC * PX <= 8 ? 3 : 2;
+    static constexpr int MINB = NC * PX <= 8 ? 4 : 2;
 };
 
 // U_ / MINB_ override the defaults (rows in flight per thread, CTAs per SM for registers).
@@ -607,10 +629,12 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
         src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
         const int nrl = yhi - ylo + 1;
         ncl = xhi - xlo + 1;
-        for (int idx = threadIdx.x; idx < nrl * NC * ncl; idx += 256) {
-            const int xx = idx % ncl, rm = idx / ncl;
-            const int m = rm % NC, rr = rm / NC;
-            Ms[idx] = __ldg(Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo + xx);
+        // one warp per (row, map) line of the rectangle, lanes along the columns
+        for (int rm = threadIdx.x >> 5; rm < nrl * NC; rm += 8) {
+            const int rr = rm / NC, m = rm - rr * NC;
+            const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo;
+            float* d = Ms + (size_t)rm * ncl;
+            for (int xx = threadIdx.x & 31; xx < ncl; xx += 32) d[xx] = __ldg(src + xx);
         }
 #pragma unroll
         for (int i = 0; i < PX; ++i) {

@@ -60,20 +60,23 @@ int main(int argc, char** argv) {
         rep(nm, timeit([&] { copy_kernel<4, false><<<g, 256>>>((const float4*)I, (float4*)q, n4); }), bytes_copy);
     }
     rep("cudaMemcpy D2D", timeit([&] { cudaMemcpyAsync(q, I, B * N * 4, cudaMemcpyDeviceToDevice); }), bytes_copy);
-    for (int TR : {32, 64, 128}) {
+    for (int TR : {16, 32, 64}) {
         OutParams op{I, M, q, H, W, h, w, H, h, 0, 0, TR};
         dim3 g4((W + 1023) / 1024, (H + TR - 1) / TR, B);
         const size_t sm = (size_t)(TR / 4 + 3) * 2 * 259 * 4;
         char nm[64];
-        cudaFuncSetAttribute(output_kernel<1, 1, 4, false, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-        cudaFuncSetAttribute(output_kernel<1, 1, 4, false, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-        cudaFuncSetAttribute(output_kernel<1, 1, 4, false, 4, 3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
-        snprintf(nm, 64, "walker-staged PX4 U4 MINB3 TR=%d", TR);
-        rep(nm, timeit([&] { output_kernel<1, 1, 4, false, 4, 3><<<g4, 256, sm>>>(op); }), bytes_k4);
-        snprintf(nm, 64, "walker-staged PX4 U2 MINB4 TR=%d", TR);
-        rep(nm, timeit([&] { output_kernel<1, 1, 4, false, 2, 4><<<g4, 256, sm>>>(op); }), bytes_k4);
-        snprintf(nm, 64, "walker-norefresh PX4 U4 MINB3 TR=%d", TR);
-        rep(nm, timeit([&] { output_kernel<1, 1, 4, false, 4, 3, 1><<<g4, 256, sm>>>(op); }), bytes_k4);
+#define VAR(U, MB) \
+        cudaFuncSetAttribute(output_kernel<1, 1, 4, false, U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); \
+        snprintf(nm, 64, "walker-staged PX4 U%d MINB%d TR=%d", U, MB, TR); \
+        rep(nm, timeit([&] { output_kernel<1, 1, 4, false, U, MB><<<g4, 256, sm>>>(op); }), bytes_k4);
+        VAR(2, 4) VAR(2, 5) VAR(2, 6) VAR(3, 4) VAR(4, 4) VAR(1, 6)
+        dim3 g2((W + 511) / 512, (H + TR - 1) / TR, B);
+        const size_t sm2 = (size_t)(TR / 4 + 3) * 2 * 131 * 4;
+#define VAR2(U, MB) \
+        cudaFuncSetAttribute(output_kernel<1, 1, 2, false, U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000); \
+        snprintf(nm, 64, "walker-staged PX2 U%d MINB%d TR=%d", U, MB, TR); \
+        rep(nm, timeit([&] { output_kernel<1, 1, 2, false, U, MB><<<g2, 256, sm2>>>(op); }), bytes_k4);
+        VAR2(2, 6) VAR2(4, 4) VAR2(2, 8)
     }
     {
         float* M1;
