@@ -329,6 +329,18 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         }
     }
     dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
+    if (!s1 && getenv("FGF_NO_ASYNC") == nullptr) {
+        // cp.async ring variant: prefetch held in shared memory, not registers
+        const size_t asm_ = smem + AsyncCfg<CI, CP, PX>::RING_BYTES;
+        if (asm_ <= 200 * 1024) {
+            auto kern = output_async_kernel<CI, CP, PX>;
+            set_smem(kern, asm_);
+            ProfScope ps(KIND_OUT, st);
+            kern<<<grid, 256, asm_, st>>>(op);
+            ++g_last_launches;
+            return last_error();
+        }
+    }
     ProfScope ps(KIND_OUT, st);
     if (s1) {
         output_kernel<CI, CP, PX, true><<<grid, 256, 0, st>>>(op);

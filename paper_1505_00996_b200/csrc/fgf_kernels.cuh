@@ -728,6 +728,183 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
     }
 }
 
+// ------------------------------------------------------------------ K4, cp.async ring
+//
+// The column walker with its U-row prefetch of I kept in SHARED memory instead of registers:
+// each thread copies its own PX pixels of row t+U with cp.async (LDGSTS, L2 -> smem, no
+// register held while in flight) into a per-thread ring slot, one commit group per row, and
+// waits with cp.async.wait_group(U-1) before consuming row t.  With ~60 registers the SM
+// keeps 4 CTAs resident and U = 8 rows x 16 B x 1024 threads = 128 KB of I in flight.
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_px(void* dst, const float* src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else if (BYTES == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int CI, int CP, int PX>
+struct AsyncCfg {
+    static constexpr int NC = (CI + 1) * CP;
+    static constexpr int U = 8;                                  // rows in flight (power of 2)
+    static constexpr int MINB = NC * PX <= 8 ? 4 : 2;
+    static constexpr size_t RING_BYTES = (size_t)U * CI * 256 * PX * 4;
+};
+
+template <int CI, int CP, int PX>
+__global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX>::MINB)) output_async_kernel(OutParams P) {
+    using C = AsyncCfg<CI, CP, PX>;
+    constexpr int NC = C::NC;
+    constexpr int U = C::U;
+    using V = VecT<PX>;
+    using VT = typename V::T;
+    __shared__ int s_ya[kMaxTR];
+    __shared__ int s_y1[kMaxTR];
+    __shared__ float s_fy[kMaxTR];
+    extern __shared__ __align__(16) float smx[];
+    VT* ring = reinterpret_cast<VT*>(smx);                        // [U][CI][256]
+    float* Ms = smx + C::RING_BYTES / 4;                          // [nrl][NC][ncl]
+    const int H = P.H, W = P.W, h = P.hm, w = P.w;
+    const int tid = threadIdx.x;
+    const int Y0 = blockIdx.y * P.TR;
+    const int nrows = min(P.TR, H - Y0);
+    const int X0 = blockIdx.x * 256 * PX;
+    const bool act = X0 + tid * PX < W;
+    const int X = act ? X0 + tid * PX : X0;
+    const int img = blockIdx.z;
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+    const float* Ip = P.I + (size_t)img * CI * N + (size_t)Y0 * W + X;
+    float* qp = P.q + (size_t)img * CP * N + (size_t)Y0 * W + X;
+    const float* Mb = P.M + (size_t)img * NC * n;
+
+    // Issue the first U rows (one commit group per row, empty groups keep the count uniform).
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (act && u < nrows)
+#pragma unroll
+            for (int j = 0; j < CI; ++j)
+                cp_async_px<PX * 4>(&ring[(u * CI + j) * 256 + tid], Ip + j * N + (size_t)u * W);
+        cp_async_commit();
+    }
+
+    // Row table and staged low-res rectangle (as in output_kernel).
+    for (int t = tid; t < nrows; t += 256) {
+        int ya, yb;
+        float fy;
+        src_coord(P.Yoff + Y0 + t, P.hg, P.Hg, ya, yb, fy);
+        s_ya[t] = ya - P.yoff;
+        s_y1[t] = yb - P.yoff;
+        s_fy[t] = fy;
+    }
+    int ylo, yd, yhi, xlo, xd, xhi;
+    float fd;
+    src_coord(P.Yoff + Y0, P.hg, P.Hg, ylo, yd, fd);
+    src_coord(P.Yoff + Y0 + nrows - 1, P.hg, P.Hg, yd, yhi, fd);
+    ylo -= P.yoff;
+    yhi -= P.yoff;
+    src_coord(X0, w, W, xlo, xd, fd);
+    src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
+    const int nrl = yhi - ylo + 1, ncl = xhi - xlo + 1;
+    for (int rm = tid >> 5; rm < nrl * NC; rm += 8) {
+        const int rr = rm / NC, m = rm - rr * NC;
+        const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo;
+        float* d = Ms + (size_t)rm * ncl;
+        for (int xx = tid & 31; xx < ncl; xx += 32) d[xx] = __ldg(src + xx);
+    }
+    int oa[PX], ob[PX];
+    float fx[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
+        src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
+        oa[i] -= xlo;
+        ob[i] -= xlo;
+    }
+    __syncthreads();
+
+    int cy = -2, cy1 = -2;
+    float H0[NC][PX], H1[NC][PX], D[NC][PX];
+    auto hrow = [&](int y, float (&out)[NC][PX]) {
+        const float* mr = Ms + (size_t)(y - ylo) * NC * ncl;
+#pragma unroll
+        for (int m = 0; m < NC; ++m)
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                const float va = mr[m * ncl + oa[i]], vb = mr[m * ncl + ob[i]];
+                out[m][i] = fmaf(fx[i], vb - va, va);
+            }
+    };
+    const float* Ipf = Ip + (size_t)U * W;
+    for (int t = 0; t < nrows; ++t) {
+        const int ya = s_ya[t];
+        const float fy = s_fy[t];
+        if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform branch
+            if (act) {
+                if (ya == cy1) {
+#pragma unroll
+                    for (int m = 0; m < NC; ++m)
+#pragma unroll
+                        for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+                } else {
+                    hrow(ya, H0);
+                }
+                cy1 = s_y1[t];
+                hrow(cy1, H1);
+#pragma unroll
+                for (int m = 0; m < NC; ++m)
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+            }
+            cy = ya;
+        }
+        cp_async_wait<U - 1>();                     // row t has landed in this thread's slot
+        const int slot = t & (U - 1);
+        if (act) {
+            VT iv[CI];
+#pragma unroll
+            for (int j = 0; j < CI; ++j) iv[j] = ring[(slot * CI + j) * 256 + tid];
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+                const int mb = c * (CI + 1);
+                float o[PX];
+#pragma unroll
+                for (int i = 0; i < PX; ++i) {
+                    float acc = fmaf(fy, D[mb + CI][i], H0[mb + CI][i]);
+#pragma unroll
+                    for (int j = 0; j < CI; ++j)
+                        acc = fmaf(fmaf(fy, D[mb + j][i], H0[mb + j][i]), V::get(iv[j], i), acc);
+                    o[i] = acc;
+                }
+                V::st(qp + c * N, o);
+            }
+            // the slot's values are consumed (the stores above depend on them): refill it
+            if (t + U < nrows)
+#pragma unroll
+                for (int j = 0; j < CI; ++j)
+                    cp_async_px<PX * 4>(&ring[(slot * CI + j) * 256 + tid], Ipf + j * N);
+        }
+        cp_async_commit();
+        qp += W;
+        Ipf += W;
+    }
+    cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------ K4, persistent
 //
 // Persistent column walker (s > 1).  The grid is ncb x cpb CTAs (about two per SM); CTA
@@ -737,13 +914,6 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
 // band streams, and the rolling U-row register prefetch of I runs across band boundaries, so
 // neither the staging latency nor a band change ever idles the HBM pipe.
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct PersistParams {
     OutParams o;           // geometry (TR = rows per band)

@@ -78,6 +78,16 @@ int main(int argc, char** argv) {
         rep(nm, timeit([&] { output_kernel<1, 1, 2, false, U, MB><<<g2, 256, sm2>>>(op); }), bytes_k4);
         VAR2(2, 6) VAR2(4, 4) VAR2(2, 8)
     }
+    for (int TR : {16, 32, 64}) {
+        OutParams op{I, M, q, H, W, h, w, H, h, 0, 0, TR};
+        dim3 g4((W + 1023) / 1024, (H + TR - 1) / TR, B);
+        const size_t sm = (size_t)(TR / 4 + 3) * 2 * 259 * 4 + AsyncCfg<1, 1, 4>::RING_BYTES;
+        cudaFuncSetAttribute(output_async_kernel<1, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+        int occ = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, output_async_kernel<1, 1, 4>, 256, sm);
+        char nm[64];
+        snprintf(nm, 64, "async-ring PX4 U8 TR=%d occ=%d", TR, occ);
+        rep(nm, timeit([&] { output_async_kernel<1, 1, 4><<<g4, 256, sm>>>(op); }), bytes_k4);
+    }
     {
         float* M1;
         CK(cudaMalloc(&M1, (size_t)2 * 2 * N * 4));
