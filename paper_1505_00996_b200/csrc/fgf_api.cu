@@ -23,7 +23,7 @@ namespace {
 thread_local int g_last_launches = 0;
 
 constexpr size_t kAlign = 256;
-constexpr size_t kChunkTargetBytes = 1024u << 20;  // low-res workspace bytes per pipeline slot
+constexpr size_t kChunkTargetBytes = 8ull << 30;  // low-res workspace bytes per pipeline slot
 
 // ---- optional per-launch event timing (fgf_profile_*)
 enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, NKIND = 4 };
