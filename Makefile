@@ -5,7 +5,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v
 PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 SRCS := $(PKG)/csrc/fgf_api.cu
-HDRS := $(PKG)/csrc/fgf_kernels.cuh include/fgf.h
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
 ORACLE := oracle/libfgf_oracle.so
 
 all: $(LIB) $(ORACLE)

@@ -144,7 +144,7 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
  * pair around every kernel launch on its launching stream; fgf_profile_enable(0) stops.
  * fgf_profile_read() waits for the recorded events and writes, for each kernel kind
  * (0 = subsample K0, 1 = statistics + coefficients K1, 2 = box of a, b K3,
- * 3 = upsample + output K4), the summed device milliseconds and the launch count, then
+ * 3 = upsample + output K4, 4 = fused low-res chain K13 for gray guidance), the summed device milliseconds and the launch count, then
  * clears the records.  Returns the number of kinds written (<= max_kinds) or -FGF_ERR_CUDA. */
 int fgf_profile_enable(int on);
 int fgf_profile_read(double* ms, int* launches, int max_kinds);

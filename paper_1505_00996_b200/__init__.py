@@ -40,7 +40,7 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_coefficients", "fgf_upsample_output", "fgf_last_launch_count", "fgf_status_str",
            "fgf_version", "fgf_profile_enable", "fgf_profile_read", "fgf_subsample",
            "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows")
-KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output")
+KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
 _i, _d, _sz = ctypes.c_int, ctypes.c_double, ctypes.c_size_t
@@ -126,9 +126,10 @@ def fgf_profile_enable(on: bool) -> None:
 
 def fgf_profile_read():
     """{kind: (total_ms, launches)} for the launches recorded since fgf_profile_enable."""
-    ms = (ctypes.c_double * 4)()
-    n = (ctypes.c_int * 4)()
-    k = _lib.fgf_profile_read(ms, n, 4)
+    nk = len(KERNEL_KINDS)
+    ms = (ctypes.c_double * nk)()
+    n = (ctypes.c_int * nk)()
+    k = _lib.fgf_profile_read(ms, n, nk)
     if k < 0:
         raise FGFError(-k, "fgf_profile_read")
     return {KERNEL_KINDS[i]: (ms[i], n[i]) for i in range(k)}

@@ -16,6 +16,7 @@
 
 #include "../../include/fgf.h"
 #include "fgf_kernels.cuh"
+#include "fgf_lowres.cuh"
 
 namespace fgf {
 namespace {
@@ -26,7 +27,7 @@ constexpr size_t kAlign = 256;
 constexpr size_t kChunkTargetBytes = 8ull << 30;  // low-res workspace bytes per pipeline slot
 
 // ---- optional per-launch event timing (fgf_profile_*)
-enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, NKIND = 4 };
+enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, KIND_LOWRES = 4, NKIND = 5 };
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
@@ -389,6 +390,98 @@ int launch_output(const float* I, const float* M, float* q, int images, const Pl
     return FGF_ERR_SHAPE;
 }
 
+// ---- K13: fused low-res chain (gray guidance), fgf_lowres.cuh
+constexpr int kLrKA = 9, kLrKB = 9;
+constexpr size_t kLrSmemMax = 227 * 1024;
+
+// Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA; among the strip counts
+// that fit, the fewest total threads (halo overhead), then the smaller CTA.  G = 8 rows per
+// batch when its shared memory fits, else 4.
+struct LrGeom {
+    int NT = 0, TW = 0, strips = 0, TH = 0, G = 0;
+    size_t smem = 0;
+};
+
+template <int CP, int G>
+bool lowres_fits(LrGeom& g, int R) {
+    using C = LowresCfg<CP, G, kLrKA, kLrKB>;
+    const auto L = C::layout(g.NT, g.TW, g.TH, R);
+    if (L.total > kLrSmemMax || G * L.nrA > g.NT || G * L.nrB > g.NT) return false;
+    g.smem = L.total;
+    g.G = G;
+    return true;
+}
+
+template <int CP>
+bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
+    int want_nt = 0;
+    if (const char* e = getenv("FGF_LR_NT")) want_nt = atoi(e);
+    LrGeom best;
+    for (int ns = 1; ns <= w; ++ns) {
+        const int TW = (w + ns - 1) / ns;
+        if ((ns - 1) * TW >= w) continue;
+        const int NT = (TW + 4 * R + 31) / 32 * 32;
+        if (NT > 512) continue;
+        if (NT < 128 && ns > 1) break;
+        const long long tot = (long long)ns * NT;
+        bool better = best.NT == 0 || tot < (long long)best.strips * best.NT ||
+                      (tot == (long long)best.strips * best.NT && NT < best.NT);
+        if (want_nt > 0) better = best.NT == 0 || std::abs(NT - want_nt) < std::abs(best.NT - want_nt);
+        if (better) { best.NT = NT; best.TW = TW; best.strips = ns; }
+    }
+    if (best.NT == 0) return false;
+    // Segment height: enough CTAs for ~8 waves of one CTA per SM, at least 4R rows, <= 256.
+    const long long cols = (long long)best.strips * images;
+    long long th = ((long long)h * cols + 8 * 148 - 1) / (8 * 148);
+    th = std::max<long long>(th, std::max(4 * R, 32));
+    if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
+    best.TH = (int)std::max<long long>(1, std::min<long long>(std::min<long long>(th, 256), h));
+    int want_g = 0;
+    if (const char* e = getenv("FGF_LR_G")) want_g = atoi(e);
+    if (want_g != 4 && lowres_fits<CP, 8>(best, R)) { g = best; return true; }
+    if (lowres_fits<CP, 4>(best, R)) { g = best; return true; }
+    return false;
+}
+
+template <int CP, int G>
+int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
+                         cudaStream_t st) {
+    auto kern = lowres_gray_kernel<CP, G, kLrKA, kLrKB>;
+    set_smem(kern, g.smem);
+    dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
+    ProfScope ps(KIND_LOWRES, st);
+    kern<<<grid, g.NT, g.smem, st>>>(lp);
+    ++g_last_launches;
+    return last_error();
+}
+
+template <int CP>
+int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cudaStream_t st,
+                         bool dry) {
+    LrGeom g;
+    if (!lowres_geom<CP>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
+    if (dry) return FGF_OK;
+    LowresParams lp = lp0;
+    lp.TW = g.TW;
+    lp.TH = g.TH;
+    if (g.G == 8) return launch_lowres_gray_g<CP, 8>(lp, g, images, P, st);
+    return launch_lowres_gray_g<CP, 4>(lp, g, images, P, st);
+}
+
+// dry = true: only report whether K13 serves this plan (FGF_OK) or not.
+int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaStream_t st,
+                       bool dry = false) {
+    if (P.CI != 1) return FGF_ERR_UNSUPPORTED;
+    if (const char* e = getenv("FGF_LOWRES")) {
+        if (strcmp(e, "strip") == 0) return FGF_ERR_UNSUPPORTED;
+    }
+    switch (P.CP) {
+        case 1: return launch_lowres_gray_t<1>(lp, images, P, st, dry);
+        case 2: return launch_lowres_gray_t<2>(lp, images, P, st, dry);
+    }
+    return FGF_ERR_UNSUPPORTED;
+}
+
 // Steps 1-5 for images [b0, b0+nb): writes the mean maps into `mean`.
 int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, const Plan& P,
                char* slot, cudaStream_t st) {
@@ -398,6 +491,29 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
     float* planes = reinterpret_cast<float*>(slot);
     float* coef = reinterpret_cast<float*>(slot + P.ws_planes);
     int rc;
+
+    // Gray guidance: the fused K13 (steps 1-5 in one kernel; nearest samples read in place).
+    if (launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) {
+        LowresParams lp{};
+        lp.h = P.h; lp.w = P.w; lp.R = P.R; lp.eps = P.eps;
+        lp.dst = mean;
+        if (P.s > 1 && P.sub == FGF_SUB_BILINEAR) {
+            float* Is = planes;
+            float* ps = planes + (size_t)nb * P.n;
+            if ((rc = launch_subsample(Ib, Is, nb, P, st))) return rc;
+            if (p_is_I) ps = Is;
+            else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) return rc;
+            lp.srcI = Is; lp.imgI = (long long)P.n;
+            lp.srcP = ps; lp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; lp.planeP = (int)P.n;
+            lp.row = P.w; lp.col = 1;
+        } else {
+            // nearest (R3): sample (y, x) = I[y s][x s]; s = 1: the image itself
+            lp.srcI = Ib; lp.imgI = (long long)P.N;
+            lp.srcP = pb; lp.imgP = (long long)P.CP * P.N; lp.planeP = (int)P.N;
+            lp.row = P.s * P.W; lp.col = P.s;
+        }
+        return launch_lowres_gray(lp, nb, P, st);
+    }
 
     StripParams sp{};
     if (P.s > 1) {

@@ -1,0 +1,383 @@
+// fgf_lowres.cuh -- K13: the whole low-resolution chain of Alg. 2 for gray
+// guidance in ONE kernel.
+//
+//   step 1  I' = f_sub(I, s), p' = f_sub(p, s): the samples are read straight from
+//                      the source through (row, col) strides -- the full-resolution image at
+//                      the nearest sample sites I[y s][x s] (R3), the image itself at
+//                      s = 1, or K0's compact block-mean planes (R4);
+//   steps 2-4 (Eq.2-3)  mean_I, corr_I, mean_p, corr_Ip (box of radius r', R1),
+//                      var_I, cov_Ip, a = cov_Ip / (var_I + eps), b = mean_p - a mean_I;
+//   step 5  mean_a = f_mean(a), mean_b = f_mean(b) -> the only HBM write.
+//
+// A CTA owns a strip of TW output columns and a segment of TH output rows.  Stage A computes
+// a, b on the strip widened by r' (TW + 2r' columns) and the segment widened by r' rows,
+// which needs statistics over TW + 4r' sample columns; stage B boxes a, b into the outputs.
+// Both stages are the O(1)-per-pixel running-sum box of P:16: one thread per column keeps
+// fp64 vertical window sums in registers (add row y + r', subtract row y - r'), the sums of
+// G rows are snapshot to shared memory, and threads slide horizontal windows along runs of
+// K (odd: conflict-free fp64 banks) columns.  Stage B lags stage A by r' rows; a, b live in
+// a shared-memory ring of 2r' + G rows (fp32, as stored by the unfused path), the raw samples
+// in a per-thread ring of 2r' + 1 rows, so every sample is read from memory exactly once and
+// nothing but mean_a, mean_b ever reaches HBM.  Window clipping: columns / rows outside the
+// image contribute zeros and the divisor is the in-bounds count (R1).
+//
+// Precision (R13): fp64 statistics box sums (products of two floats are exact in
+// fp64), fp64 var_I / cov_Ip, fp32 quotient and b (as the unfused path), fp32 a, b storage and
+// fp32 box sums of a, b (stage B; R17: |a| <= sqrt(var_p)/(2 sqrt(eps)), so the
+// fp32 sums add errors of the same order as the fp32 storage of a, b itself).
+//
+// Nothing here is shared with oracle/ (the independent CPU reference).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fgf {
+
+struct LowresParams {
+    // Sample (y, x) of image b: srcI[b*imgI + y*row + x*col]; p channel c at
+    // srcP[b*imgP + c*planeP + y*row + x*col].  In-image offsets fit in 32 bits (validated).
+    const float* srcI;
+    const float* srcP;
+    long long imgI, imgP;
+    int planeP;
+    int row, col;
+    float* dst;            // [img][2CP][h][w]: mean_a_c at 2c, mean_b_c at 2c+1
+    int h, w, R;
+    int TW, TH;            // output columns per strip, output rows per segment
+    double eps;
+};
+
+template <int CP, int G, int KA, int KB>
+struct LowresCfg {
+    static constexpr int NIN = 1 + CP;          // I', p'_c
+    static constexpr int NMAP = 2 + 2 * CP;     // I', I'I', p'_c, I'p'_c
+    static constexpr int NAB = 2 * CP;          // a_c, b_c
+    // Shared-memory carve-up (bytes); identical on host and device.  Every horizontal run
+    // may read / write past the last valid column: the pitches are padded so those accesses
+    // stay inside zero-initialised (read) or scratch (write) padding.
+    struct Layout {
+        int NT, NCA, NCS, nrA, nrB, PA, PB, VPA, VPB, RBA, RBI;
+        size_t oVsA, oVsB, oInvxA, oInvxB, oABr, oINr, oOs, total;
+    };
+    __host__ __device__ static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+    __host__ __device__ static Layout layout(int NT, int TW, int TH, int R) {
+        Layout L;
+        L.NT = NT;
+        L.NCA = TW + 2 * R;                      // a, b columns
+        L.NCS = TW + 4 * R;                      // sample / statistics columns
+        L.nrA = (L.NCA + KA - 1) / KA;           // stage-A runs per row
+        L.nrB = (TW + KB - 1) / KB;              // stage-B runs per row
+        L.PA = L.nrA * KA;                       // padded a, b row (ABr, invxA)
+        L.PB = L.nrB * KB;                       // padded output row (Os, invxB)
+        L.VPA = L.PA + 2 * R + 1;                // sums pitch: every run's reads in bounds
+        if (L.VPA < NT) L.VPA = NT;
+        L.VPB = L.PB + 2 * R + 1;
+        if (L.VPB < L.PA) L.VPB = L.PA;
+        L.RBA = 2 * R + G;
+        L.RBI = 2 * R + 1;
+        size_t o = 0;
+        L.oVsA = o; o = al16(o + (size_t)G * NMAP * L.VPA * 8);
+        L.oVsB = o; o = al16(o + (size_t)G * NAB * L.VPB * 4);
+        L.oInvxA = o; o = al16(o + (size_t)L.PA * 8);
+        L.oInvxB = o; o = al16(o + (size_t)L.PB * 4);
+        L.oABr = o; o = al16(o + (size_t)L.RBA * NAB * L.PA * 4);
+        L.oINr = o; o = al16(o + (size_t)L.RBI * NIN * NT * 4);
+        L.oOs = o; o = al16(o + (size_t)G * NAB * L.PB * 4);
+        L.total = o;
+        return L;
+    }
+};
+
+// 1 / (number of in-bounds indices of the window [i - R, i + R] in [0, n)).
+__device__ __forceinline__ double inv_count(int i, int n, int R) {
+    return 1.0 / (double)(min(n - 1, i + R) - max(0, i - R) + 1);
+}
+
+// grid (strips, segments, images), block NT (>= TW + 4R, multiple of 32, G * nrA <= NT and
+// G * nrB <= NT), dynamic smem LowresCfg::layout(...).total.
+template <int CP, int G, int KA, int KB>
+__global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
+    using C = LowresCfg<CP, G, KA, KB>;
+    constexpr int NIN = C::NIN, NMAP = C::NMAP, NAB = C::NAB;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int NT = blockDim.x, tid = threadIdx.x;
+    const int h = P.h, w = P.w, R = P.R, TW = P.TW;
+    const auto L = C::layout(NT, TW, P.TH, R);
+    double* VsA = reinterpret_cast<double*>(smem + L.oVsA);     // [G][NMAP][VPA]
+    float* VsB = reinterpret_cast<float*>(smem + L.oVsB);       // [G][NAB][VPB]
+    double* invxA = reinterpret_cast<double*>(smem + L.oInvxA); // [PA], 0 = outside the image
+    float* invxB = reinterpret_cast<float*>(smem + L.oInvxB);   // [PB]
+    float* ABr = reinterpret_cast<float*>(smem + L.oABr);       // [RBA][NAB][PA]
+    float* INr = reinterpret_cast<float*>(smem + L.oINr);       // [RBI][NIN][NT]
+    float* Os = reinterpret_cast<float*>(smem + L.oOs);         // [G][NAB][PB]
+
+    const int img = blockIdx.z;
+    const int x0 = blockIdx.x * TW;
+    const int y0 = blockIdx.y * P.TH;
+    const int yB1 = min(h, y0 + P.TH);            // outputs [y0, yB1)
+    const int yA0 = max(0, y0 - R);               // a, b rows [yA0, yA1)
+    const int yA1 = min(h, yB1 + R);
+    const int VPA = L.VPA, VPB = L.VPB, PA = L.PA, PB = L.PB, RBA = L.RBA, RBI = L.RBI;
+
+    // ---- tables and zero pads (the zeros make out-of-image columns contribute nothing
+    // and make a = b = 0 there: inv = 0 turns every mean into 0)
+    for (int i = tid; i < G * NMAP * VPA; i += NT) VsA[i] = 0.0;
+    for (int i = tid; i < G * NAB * VPB; i += NT) VsB[i] = 0.0f;
+    for (int j = tid; j < PA; j += NT) {
+        const int ca = x0 - R + j;
+        invxA[j] = (j < L.NCA && ca >= 0 && ca < w) ? inv_count(ca, w, R) : 0.0;
+    }
+    for (int k = tid; k < PB; k += NT) invxB[k] = (float)inv_count(min(x0 + k, w - 1), w, R);
+
+    // ---- this thread's sample column (stage A column phase)
+    const int cs = x0 - 2 * R + tid;
+    const bool colS = tid < L.NCS;                // owns a statistics column (maybe outside)
+    const bool colA = colS && cs >= 0 && cs < w;  // ... inside the image
+    const int offc = (colA ? cs : 0) * P.col;
+    const float* bI = P.srcI + img * P.imgI + offc;
+    const float* bP = P.srcP + img * P.imgP + offc;
+    const int row = P.row, planeP = P.planeP;
+    auto load = [&](int y, float* v) {
+        const int o = y * row;
+        v[0] = __ldg(bI + o);
+#pragma unroll
+        for (int c = 0; c < CP; ++c) v[1 + c] = __ldg(bP + o + c * planeP);
+    };
+    // accumulate (sgn = +1) or remove (-1) one sample row: [I, II, p_c, Ip_c], exact products
+    auto accum = [&](double* acc, const float* v, bool sub) {
+        const double I = (double)v[0];
+        acc[0] = sub ? acc[0] - I : acc[0] + I;
+        acc[1] = sub ? fma(-I, I, acc[1]) : fma(I, I, acc[1]);
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double p = (double)v[1 + c];
+            acc[2 + c] = sub ? acc[2 + c] - p : acc[2 + c] + p;
+            acc[2 + CP + c] = sub ? fma(-I, p, acc[2 + CP + c]) : fma(I, p, acc[2 + CP + c]);
+        }
+    };
+    const int ringStride = NIN * NT;              // floats between ring slots
+    float* inr = INr + tid;                       // slot s, input k at inr[s*ringStride + k*NT]
+
+    double accA[NMAP];
+#pragma unroll
+    for (int m = 0; m < NMAP; ++m) accA[m] = 0.0;
+    // The row added when producing a, b row ya is ya + R, in slot (ya + R) mod RBI; the row
+    // subtracted, ya - R, sits in the next slot (RBI = 2R + 1).
+    int sAdd = (yA0 + R) % RBI;
+    if (colA) {
+        // warm-up: rows [yA0 - R, yA0 + R - 1] clipped, kept in their ring slots
+        const int wa = max(0, yA0 - R), wb = min(h, yA0 + R);
+        for (int y = wa; y < wb; ++y) {
+            float v[NIN];
+            load(y, v);
+            int sl = sAdd + (y - yA0 - R);
+            if (sl < 0) sl += RBI;
+#pragma unroll
+            for (int k = 0; k < NIN; ++k) inr[sl * ringStride + k * NT] = v[k];
+            accum(accA, v, false);
+        }
+    }
+    // prefetch of the add rows of the next batch
+    float nv[G][NIN];
+    const long long dP = bP - bI;
+    auto load_batch = [&](int ya) {
+        const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
+        if (!colA) return;
+        const float* pi = bI + (long long)(ya + R) * row;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (g < ng) {
+                nv[g][0] = __ldg(pi);
+#pragma unroll
+                for (int c = 0; c < CP; ++c) nv[g][1 + c] = __ldg(pi + dP + c * planeP);
+            }
+            pi += row;
+        }
+    };
+    load_batch(yA0);
+
+    // stage B column state: a, b column j = tid (local), ca = x0 - R + j
+    const bool colB = tid < L.NCA;
+    float accB[NAB];
+#pragma unroll
+    for (int m = 0; m < NAB; ++m) accB[m] = 0.0f;
+    bool warmB = false;
+
+    // fixed horizontal task of this thread: row g of a batch, run of K columns
+    const int gA = tid / L.nrA, jA0 = (tid - gA * L.nrA) * KA;
+    const int gB = tid / L.nrB, kB0 = (tid - gB * L.nrB) * KB;
+    const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0;
+    const float* hvB = VsB + (size_t)gB * NAB * VPB + kB0;
+
+    int yA = yA0, yb = y0;
+    int sA = yA0 % RBA;                           // ring slot of a, b row yA
+    int prevB = 0, prevYb = 0;                    // outputs staged in Os, not yet stored
+    const size_t n = (size_t)h * w;
+    float* dstimg = P.dst + (size_t)img * NAB * n;
+
+    auto store_prev = [&]() {
+        if (prevB > 0 && tid < TW && x0 + tid < w) {
+            float* d = dstimg + (size_t)prevYb * w + x0 + tid;
+            const float* os = Os + tid;
+            for (int g = 0; g < prevB; ++g) {
+#pragma unroll
+                for (int m = 0; m < NAB; ++m) d[(size_t)m * n] = os[m * PB];
+                d += w;
+                os += NAB * PB;
+            }
+        }
+    };
+
+    __syncthreads();
+    while (yb < yB1) {
+        const int nA = max(0, min(G, yA1 - yA));
+        // ---- stage A, column phase: G rows of vertical sums -> VsA
+        if (nA > 0 && colS) {
+            int s = sAdd;
+            double* vcol = VsA + tid;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g < nA) {
+                    const int ya = yA + g;
+                    const int ss = (s + 1 == RBI) ? 0 : s + 1;
+                    if (colA && ya + R < h) {
+                        float* slot = inr + s * ringStride;
+#pragma unroll
+                        for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
+                        accum(accA, nv[g], false);
+                    }
+#pragma unroll
+                    for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
+                    if (colA && ya - R >= 0) {
+                        const float* slot = inr + ss * ringStride;
+                        float v[NIN];
+#pragma unroll
+                        for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
+                        accum(accA, v, true);
+                    }
+                    s = ss;
+                }
+            }
+            sAdd = s;
+        }
+        __syncthreads();
+        store_prev();
+        prevB = 0;
+        if (nA > 0) load_batch(yA + nA);
+
+        // ---- stage A, horizontal phase + coefficient epilogue -> a, b ring rows
+        if (gA < nA) {
+            const int ya = yA + gA;
+            const double invy = inv_count(ya, h, R);
+            int sl = sA + gA;
+            if (sl >= RBA) sl -= RBA;
+            float* ab = ABr + (size_t)sl * NAB * PA + jA0;
+            const double* ix = invxA + jA0;
+            const double* vw = hvA + 2 * R + 1;
+            double S[NMAP];
+#pragma unroll
+            for (int m = 0; m < NMAP; ++m) S[m] = 0.0;
+#pragma unroll 4
+            for (int k = 0; k <= 2 * R; ++k)
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m) S[m] += hvA[m * VPA + k];
+#pragma unroll
+            for (int i = 0; i < KA; ++i) {
+                const double inv = ix[i] * invy;           // 0 outside the image -> a = b = 0
+                const double mI = S[0] * inv;
+                double var = fma(-mI, mI, S[1] * inv);     // var_I
+                var = var < 0.0 ? 0.0 : var;               // R8
+                const float rden = __fdividef(1.0f, (float)(var + P.eps));
+                const float mIf = (float)mI;
+#pragma unroll
+                for (int c = 0; c < CP; ++c) {
+                    const double mp = S[2 + c] * inv;
+                    const double cov = fma(-mI, mp, S[2 + CP + c] * inv);   // cov_Ip
+                    const float a = (float)cov * rden;                    // Eq.2 / P:80
+                    ab[(2 * c) * PA + i] = a;
+                    ab[(2 * c + 1) * PA + i] = fmaf(-a, mIf, (float)mp);  // Eq.3 / P:81
+                }
+                if (i + 1 < KA) {
+#pragma unroll
+                    for (int m = 0; m < NMAP; ++m) S[m] += vw[m * VPA + i] - hvA[m * VPA + i];
+                }
+            }
+        }
+        __syncthreads();
+        yA += nA;
+        sA += nA;
+        if (sA >= RBA) sA -= RBA;
+
+        // ---- stage B: outputs whose a, b windows are complete
+        const int allowed = (yA >= yA1) ? yB1 : min(yB1, yA - R);
+        const int nB = min(G, allowed - yb);
+        if (nB > 0) {
+            if (colB) {
+                auto slotp = [&](int y) {         // a, b row y (y >= yA - RBA), this column
+                    int s = sA - (yA - y);
+                    s = s < 0 ? s + RBA : s;
+                    return ABr + (size_t)s * NAB * PA + tid;
+                };
+                if (!warmB) {
+                    for (int y = max(0, y0 - R); y < min(h, y0 + R); ++y) {
+                        const float* r = slotp(y);
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) accB[m] += r[m * PA];
+                    }
+                }
+                float* vcol = VsB + tid;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (g < nB) {
+                        const int y = yb + g;
+                        if (y + R < h) {
+                            const float* r = slotp(y + R);
+#pragma unroll
+                            for (int m = 0; m < NAB; ++m) accB[m] += r[m * PA];
+                        }
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) vcol[(g * NAB + m) * VPB] = accB[m];
+                        if (y - R >= 0) {
+                            const float* r = slotp(y - R);
+#pragma unroll
+                            for (int m = 0; m < NAB; ++m) accB[m] -= r[m * PA];
+                        }
+                    }
+                }
+            }
+            warmB = true;
+            __syncthreads();
+            if (gB < nB) {
+                const float invy = (float)inv_count(yb + gB, h, R);
+                const float* ix = invxB + kB0;
+                const float* vw = hvB + 2 * R + 1;
+                float S[NAB];
+#pragma unroll
+                for (int m = 0; m < NAB; ++m) S[m] = 0.0f;
+#pragma unroll 4
+                for (int k = 0; k <= 2 * R; ++k)
+#pragma unroll
+                    for (int m = 0; m < NAB; ++m) S[m] += hvB[m * VPB + k];
+                float* o = Os + (size_t)gB * NAB * PB + kB0;
+#pragma unroll
+                for (int i = 0; i < KB; ++i) {
+                    const float inv = ix[i] * invy;
+#pragma unroll
+                    for (int m = 0; m < NAB; ++m) o[m * PB + i] = S[m] * inv;
+                    if (i + 1 < KB) {
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) S[m] += vw[m * VPB + i] - hvB[m * VPB + i];
+                    }
+                }
+            }
+            prevB = nB;
+            prevYb = yb;
+            yb += nB;
+        }
+    }
+    __syncthreads();
+    store_prev();
+}
+
+}  // namespace fgf
