@@ -391,30 +391,50 @@ int launch_output(const float* I, const float* M, float* q, int images, const Pl
 }
 
 // ---- K13: fused low-res chain (gray guidance), fgf_lowres.cuh
-constexpr int kLrKA = 9, kLrKB = 9;
 constexpr size_t kLrSmemMax = 227 * 1024;
 
-// Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA; among the strip counts
-// that fit, the fewest total threads (halo overhead), then the smaller CTA.  G = 8 rows per
-// batch when its shared memory fits, else 4.
+// Kernel variants (rows per batch G, horizontal run lengths KA / KB); the first that fits
+// is used unless FGF_LR_V selects one (development sweep).
+//   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
+//   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
+//   4: as 3 with lane-pair split horizontal phases      5: as 0 with the split
+constexpr int kLrNumVariants = 6;
+
+// Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
 struct LrGeom {
-    int NT = 0, TW = 0, strips = 0, TH = 0, G = 0;
+    int NT = 0, TW = 0, strips = 0, TH = 0, V = -1;
     size_t smem = 0;
 };
 
-template <int CP, int G>
-bool lowres_fits(LrGeom& g, int R) {
-    using C = LowresCfg<CP, G, kLrKA, kLrKB>;
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, bool SPLIT = false>
+bool lowres_fits(LrGeom& g, int R, int v) {
+    using C = LowresCfg<CP, G, KA, KB, RING>;
     const auto L = C::layout(g.NT, g.TW, g.TH, R);
-    if (L.total > kLrSmemMax || G * L.nrA > g.NT || G * L.nrB > g.NT) return false;
+    const int ta = (SPLIT ? 2 : 1) * G * L.nrA, tb = (SPLIT ? 2 * CP : 1) * G * L.nrB;
+    if (L.total > kLrSmemMax || ta > g.NT || tb > g.NT || g.NT > MAXT) return false;
     g.smem = L.total;
-    g.G = G;
+    g.V = v;
     return true;
 }
 
 template <int CP>
+bool lowres_fits_v(LrGeom& g, int R, int v) {
+    if (CP > 1 && v != 0) return false;          // one variant for several p channels
+    switch (v) {
+        case 0: return lowres_fits<CP, 4, 9, 9>(g, R, v);
+        case 1: return lowres_fits<CP, 8, 9, 9>(g, R, v);
+        case 2: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
+        case 3: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
+        case 4: return lowres_fits<CP, 4, 9, 9, false, 160, true>(g, R, v);
+        case 5: return lowres_fits<CP, 4, 9, 9, true, 512, true>(g, R, v);
+    }
+    return false;
+}
+
+template <int CP>
 bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
-    int want_nt = 0;
+    // Target ~160 threads (5 warps) per CTA: three CTAs per SM, halo overhead (TW + 4R) / TW.
+    int want_nt = 160;
     if (const char* e = getenv("FGF_LR_NT")) want_nt = atoi(e);
     LrGeom best;
     for (int ns = 1; ns <= w; ++ns) {
@@ -422,35 +442,43 @@ bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
         if ((ns - 1) * TW >= w) continue;
         const int NT = (TW + 4 * R + 31) / 32 * 32;
         if (NT > 512) continue;
-        if (NT < 128 && ns > 1) break;
-        const long long tot = (long long)ns * NT;
-        bool better = best.NT == 0 || tot < (long long)best.strips * best.NT ||
-                      (tot == (long long)best.strips * best.NT && NT < best.NT);
-        if (want_nt > 0) better = best.NT == 0 || std::abs(NT - want_nt) < std::abs(best.NT - want_nt);
+        const long long tot = (long long)ns * NT, btot = (long long)best.strips * best.NT;
+        // closest to the target size; on ties the fewer total threads
+        const bool better = best.NT == 0 || std::abs(NT - want_nt) < std::abs(best.NT - want_nt) ||
+                            (std::abs(NT - want_nt) == std::abs(best.NT - want_nt) && tot < btot);
         if (better) { best.NT = NT; best.TW = TW; best.strips = ns; }
+        if (NT < 64) break;
     }
     if (best.NT == 0) return false;
-    // Segment height: enough CTAs for ~8 waves of one CTA per SM, at least 4R rows, <= 256.
+    // Segment height: long segments amortise the r' warm-up rows; keep >= ~8 waves.
     const long long cols = (long long)best.strips * images;
-    long long th = ((long long)h * cols + 8 * 148 - 1) / (8 * 148);
-    th = std::max<long long>(th, std::max(4 * R, 32));
+    long long th = ((long long)h * cols + 8 * 3 * 148 - 1) / (8 * 3 * 148);
+    th = std::max<long long>(th, 256);
     if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
-    best.TH = (int)std::max<long long>(1, std::min<long long>(std::min<long long>(th, 256), h));
-    int want_g = 0;
-    if (const char* e = getenv("FGF_LR_G")) want_g = atoi(e);
-    if (want_g != 4 && lowres_fits<CP, 8>(best, R)) { g = best; return true; }
-    if (lowres_fits<CP, 4>(best, R)) { g = best; return true; }
+    best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
+    if (const char* e = getenv("FGF_LR_V")) {
+        if (lowres_fits_v<CP>(best, R, atoi(e))) { g = best; return true; }
+        return false;
+    }
+    static const int order[kLrNumVariants] = {3, 0, 1, 2, 4, 5};   // measured: 3 fastest (config 4)
+    for (int v : order)
+        if (lowres_fits_v<CP>(best, R, v)) { g = best; return true; }
     return false;
 }
 
-template <int CP, int G>
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
+          bool SPLIT = false>
 int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
                          cudaStream_t st) {
-    auto kern = lowres_gray_kernel<CP, G, kLrKA, kLrKB>;
-    set_smem(kern, g.smem);
+    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, SPLIT>;
+    size_t smem = g.smem;
+    // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
+    // previous chunk can be co-resident (overlap experiment knob)
+    if (const char* e = getenv("FGF_LR_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
+    set_smem(kern, smem);
     dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
     ProfScope ps(KIND_LOWRES, st);
-    kern<<<grid, g.NT, g.smem, st>>>(lp);
+    kern<<<grid, g.NT, smem, st>>>(lp);
     ++g_last_launches;
     return last_error();
 }
@@ -464,8 +492,16 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
     LowresParams lp = lp0;
     lp.TW = g.TW;
     lp.TH = g.TH;
-    if (g.G == 8) return launch_lowres_gray_g<CP, 8>(lp, g, images, P, st);
-    return launch_lowres_gray_g<CP, 4>(lp, g, images, P, st);
+    if (CP > 1) return launch_lowres_gray_g<CP, 4, 9, 9>(lp, g, images, P, st);
+    switch (g.V) {
+        case 0: return launch_lowres_gray_g<1, 4, 9, 9>(lp, g, images, P, st);
+        case 1: return launch_lowres_gray_g<1, 8, 9, 9>(lp, g, images, P, st);
+        case 2: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 4>(lp, g, images, P, st);
+        case 3: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3>(lp, g, images, P, st);
+        case 4: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, true>(lp, g, images, P, st);
+        case 5: return launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, true>(lp, g, images, P, st);
+    }
+    return FGF_ERR_UNSUPPORTED;
 }
 
 // dry = true: only report whether K13 serves this plan (FGF_OK) or not.

@@ -48,7 +48,7 @@ struct LowresParams {
     double eps;
 };
 
-template <int CP, int G, int KA, int KB>
+template <int CP, int G, int KA, int KB, bool RING = true>
 struct LowresCfg {
     static constexpr int NIN = 1 + CP;          // I', p'_c
     static constexpr int NMAP = 2 + 2 * CP;     // I', I'I', p'_c, I'p'_c
@@ -82,7 +82,7 @@ struct LowresCfg {
         L.oInvxA = o; o = al16(o + (size_t)L.PA * 8);
         L.oInvxB = o; o = al16(o + (size_t)L.PB * 4);
         L.oABr = o; o = al16(o + (size_t)L.RBA * NAB * L.PA * 4);
-        L.oINr = o; o = al16(o + (size_t)L.RBI * NIN * NT * 4);
+        L.oINr = o; o = al16(o + (RING ? (size_t)L.RBI * NIN * NT * 4 : 0));
         L.oOs = o; o = al16(o + (size_t)G * NAB * L.PB * 4);
         L.total = o;
         return L;
@@ -96,9 +96,16 @@ __device__ __forceinline__ double inv_count(int i, int n, int R) {
 
 // grid (strips, segments, images), block NT (>= TW + 4R, multiple of 32, G * nrA <= NT and
 // G * nrB <= NT), dynamic smem LowresCfg::layout(...).total.
-template <int CP, int G, int KA, int KB>
-__global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
-    using C = LowresCfg<CP, G, KA, KB>;
+// RING = false: no sample ring; the subtracted row is re-read from global memory (L2) and
+// prefetched together with the added row.  MAXT / MINB: launch bounds.
+// SPLIT (CP = 1): the two lanes of a pair share each horizontal run -- stage A: lane 0 slides
+// I', I'I', lane 1 slides p', I'p', and they swap (mean, second moment) by shuffle for the
+// epilogue; stage B: one map per lane -- so twice as many threads work in those phases.
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
+          bool SPLIT = false>
+__global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P) {
+    static_assert(!SPLIT || CP == 1, "lane-pair split is for one p channel");
+    using C = LowresCfg<CP, G, KA, KB, RING>;
     constexpr int NIN = C::NIN, NMAP = C::NMAP, NAB = C::NAB;
     extern __shared__ __align__(16) unsigned char smem[];
     const int NT = blockDim.x, tid = threadIdx.x;
@@ -171,15 +178,18 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
         for (int y = wa; y < wb; ++y) {
             float v[NIN];
             load(y, v);
-            int sl = sAdd + (y - yA0 - R);
-            if (sl < 0) sl += RBI;
+            if (RING) {
+                int sl = sAdd + (y - yA0 - R);
+                if (sl < 0) sl += RBI;
 #pragma unroll
-            for (int k = 0; k < NIN; ++k) inr[sl * ringStride + k * NT] = v[k];
+                for (int k = 0; k < NIN; ++k) inr[sl * ringStride + k * NT] = v[k];
+            }
             accum(accA, v, false);
         }
     }
-    // prefetch of the add rows of the next batch
+    // prefetch of the add rows (and without the ring, the subtract rows) of the next batch
     float nv[G][NIN];
+    float sv[RING ? 1 : G][NIN];
     const long long dP = bP - bI;
     auto load_batch = [&](int ya) {
         const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
@@ -194,6 +204,20 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
             }
             pi += row;
         }
+        if (!RING) {
+            const int g0 = max(0, R - ya);                 // subtract rows ya + g - R >= 0
+            const int g1 = min(G, yA1 - ya);
+            const float* ps = bI + (long long)(ya - R) * row;
+#pragma unroll
+            for (int g = 0; g < (RING ? 1 : G); ++g) {
+                if (g >= g0 && g < g1) {
+                    sv[g][0] = __ldg(ps);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) sv[g][1 + c] = __ldg(ps + dP + c * planeP);
+                }
+                ps += row;
+            }
+        }
     };
     load_batch(yA0);
 
@@ -205,10 +229,13 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
     bool warmB = false;
 
     // fixed horizontal task of this thread: row g of a batch, run of K columns
-    const int gA = tid / L.nrA, jA0 = (tid - gA * L.nrA) * KA;
-    const int gB = tid / L.nrB, kB0 = (tid - gB * L.nrB) * KB;
-    const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0;
-    const float* hvB = VsB + (size_t)gB * NAB * VPB + kB0;
+    // (SPLIT: task tid / 2, half tid % 2)
+    const int tq = SPLIT ? tid >> 1 : tid, hf = SPLIT ? tid & 1 : 0;
+    const int gA = tq / L.nrA, jA0 = (tq - gA * L.nrA) * KA;
+    const int tB = SPLIT ? tid / NAB : tid, mB = SPLIT ? tid - tB * NAB : 0;
+    const int gB = tB / L.nrB, kB0 = (tB - gB * L.nrB) * KB;
+    const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0 + (SPLIT ? 2 * hf * VPA : 0);
+    const float* hvB = VsB + (size_t)gB * NAB * VPB + kB0 + (SPLIT ? mB * VPB : 0);
 
     int yA = yA0, yb = y0;
     int sA = yA0 % RBA;                           // ring slot of a, b row yA
@@ -242,19 +269,25 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
                     const int ya = yA + g;
                     const int ss = (s + 1 == RBI) ? 0 : s + 1;
                     if (colA && ya + R < h) {
-                        float* slot = inr + s * ringStride;
+                        if (RING) {
+                            float* slot = inr + s * ringStride;
 #pragma unroll
-                        for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
+                            for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
+                        }
                         accum(accA, nv[g], false);
                     }
 #pragma unroll
                     for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
                     if (colA && ya - R >= 0) {
-                        const float* slot = inr + ss * ringStride;
-                        float v[NIN];
+                        if (RING) {
+                            const float* slot = inr + ss * ringStride;
+                            float v[NIN];
 #pragma unroll
-                        for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
-                        accum(accA, v, true);
+                            for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
+                            accum(accA, v, true);
+                        } else {
+                            accum(accA, sv[RING ? 0 : g], true);
+                        }
                     }
                     s = ss;
                 }
@@ -267,7 +300,46 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
         if (nA > 0) load_batch(yA + nA);
 
         // ---- stage A, horizontal phase + coefficient epilogue -> a, b ring rows
-        if (gA < nA) {
+        if (SPLIT) {
+            const unsigned act = __ballot_sync(0xffffffffu, gA < nA);
+            if (gA < nA) {
+                const int ya = yA + gA;
+                const double invy = inv_count(ya, h, R);
+                int sl = sA + gA;
+                if (sl >= RBA) sl -= RBA;
+                float* ab = ABr + (size_t)(sl * NAB + hf) * PA + jA0;   // lane 0: a, lane 1: b
+                const double* ix = invxA + jA0;
+                const double* vw = hvA + 2 * R + 1;
+                double S0 = 0.0, S1 = 0.0;
+#pragma unroll 4
+                for (int k = 0; k <= 2 * R; ++k) {
+                    S0 += hvA[k];
+                    S1 += hvA[VPA + k];
+                }
+#pragma unroll
+                for (int i = 0; i < KA; ++i) {
+                    const double inv = ix[i] * invy;       // 0 outside the image -> a = b = 0
+                    const double u = S0 * inv, v = S1 * inv;   // lane 0: mean_I, corr_I
+                    double y = v;                              // lane 1: mean_p, corr_Ip
+                    if (hf == 0) {
+                        y = fma(-u, u, v);                     // var_I
+                        y = y < 0.0 ? 0.0 : y;                 // R8
+                    }
+                    const double xo = __shfl_xor_sync(act, u, 1);
+                    const double yo = __shfl_xor_sync(act, y, 1);
+                    const double mI = hf ? xo : u, mp = hf ? u : xo;
+                    const double var = hf ? yo : y, cIp = hf ? v : yo;
+                    const double cov = fma(-mI, mp, cIp);       // cov_Ip
+                    const float rden = __fdividef(1.0f, (float)(var + P.eps));
+                    const float a = (float)cov * rden;          // Eq.2 / P:80
+                    ab[i] = hf ? fmaf(-a, (float)mI, (float)mp) : a;   // Eq.3 / P:81
+                    if (i + 1 < KA) {
+                        S0 += vw[i] - hvA[i];
+                        S1 += vw[VPA + i] - hvA[VPA + i];
+                    }
+                }
+            }
+        } else if (gA < nA) {
             const int ya = yA + gA;
             const double invy = inv_count(ya, h, R);
             int sl = sA + gA;
@@ -348,7 +420,20 @@ __global__ void __launch_bounds__(512) lowres_gray_kernel(LowresParams P) {
             }
             warmB = true;
             __syncthreads();
-            if (gB < nB) {
+            if (SPLIT && gB < nB) {                    // one map per lane
+                const float invy = (float)inv_count(yb + gB, h, R);
+                const float* ix = invxB + kB0;
+                const float* vw = hvB + 2 * R + 1;
+                float S = 0.0f;
+#pragma unroll 4
+                for (int k = 0; k <= 2 * R; ++k) S += hvB[k];
+                float* o = Os + (size_t)(gB * NAB + mB) * PB + kB0;
+#pragma unroll
+                for (int i = 0; i < KB; ++i) {
+                    o[i] = S * (ix[i] * invy);
+                    if (i + 1 < KB) S += vw[i] - hvB[i];
+                }
+            } else if (!SPLIT && gB < nB) {
                 const float invy = (float)inv_count(yb + gB, h, R);
                 const float* ix = invxB + kB0;
                 const float* vw = hvB + 2 * R + 1;

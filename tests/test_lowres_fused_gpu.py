@@ -68,18 +68,29 @@ CASES = [
 ]
 
 
+# kernel variants (fgf_api.cu kLrNumVariants): 0 = sample ring, G 4; 1 = G 8; 2 / 3 = no ring
+VARIANTS = [None, "0", "1", "2", "4", "5"]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("case", CASES)
-def test_fused_lowres_vs_oracle(case):
+def test_fused_lowres_vs_oracle(case, variant):
     B, H, W, CP, r, eps, s, sub, TH, NT = case
+    if variant is not None and CP > 1:
+        pytest.skip("one kernel variant for several p channels")
+    if variant in ("2", "3", "4"):
+        NT = 128 if NT is None else min(NT, 160)
     g = torch.Generator(device="cuda").manual_seed(abs(hash(case)) % (2 ** 31))
     I = torch.rand((B, 1, H, W), device="cuda", generator=g)
     p = torch.rand((B, CP, H, W), device="cuda", generator=g)
-    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None):
+    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None, FGF_LR_V=variant):
         fgf.fgf_profile_enable(True)
         q = fgf.filter(I, p, r, eps, s, sub)
         torch.cuda.synchronize()
         prof = fgf.fgf_profile_read()
         fgf.fgf_profile_enable(False)
+    if variant is not None and prof["lowres_fused"][1] == 0:
+        pytest.skip("geometry outside this variant's limits")
     assert prof["lowres_fused"][1] == 1, prof       # the fused kernel served this call
     assert prof["stats_coef"][1] == 0, prof
     err = oracle_err(I, p, q, r, eps, s, sub)
