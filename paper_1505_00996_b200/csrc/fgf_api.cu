@@ -397,8 +397,7 @@ constexpr size_t kLrSmemMax = 227 * 1024;
 // is used unless FGF_LR_V selects one (development sweep).
 //   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
 //   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
-//   4: as 3 with lane-pair split horizontal phases      5: as 0 with the split
-constexpr int kLrNumVariants = 6;
+constexpr int kLrNumVariants = 4;
 
 // Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
 struct LrGeom {
@@ -406,12 +405,12 @@ struct LrGeom {
     size_t smem = 0;
 };
 
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, bool SPLIT = false>
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512>
 bool lowres_fits(LrGeom& g, int R, int v) {
     using C = LowresCfg<CP, G, KA, KB, RING>;
     const auto L = C::layout(g.NT, g.TW, g.TH, R);
-    const int ta = (SPLIT ? 2 : 1) * G * L.nrA, tb = (SPLIT ? 2 * CP : 1) * G * L.nrB;
-    if (L.total > kLrSmemMax || ta > g.NT || tb > g.NT || g.NT > MAXT) return false;
+    // both horizontal phases run concurrently on disjoint threads
+    if (L.total > kLrSmemMax || G * (L.nrA + L.nrB) > g.NT || g.NT > MAXT) return false;
     g.smem = L.total;
     g.V = v;
     return true;
@@ -425,8 +424,6 @@ bool lowres_fits_v(LrGeom& g, int R, int v) {
         case 1: return lowres_fits<CP, 8, 9, 9>(g, R, v);
         case 2: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
         case 3: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
-        case 4: return lowres_fits<CP, 4, 9, 9, false, 160, true>(g, R, v);
-        case 5: return lowres_fits<CP, 4, 9, 9, true, 512, true>(g, R, v);
     }
     return false;
 }
@@ -460,17 +457,16 @@ bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
         if (lowres_fits_v<CP>(best, R, atoi(e))) { g = best; return true; }
         return false;
     }
-    static const int order[kLrNumVariants] = {3, 0, 1, 2, 4, 5};   // measured: 3 fastest (config 4)
+    static const int order[kLrNumVariants] = {3, 0, 1, 2};   // measured: 3 fastest (config 4)
     for (int v : order)
         if (lowres_fits_v<CP>(best, R, v)) { g = best; return true; }
     return false;
 }
 
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
-          bool SPLIT = false>
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1>
 int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
                          cudaStream_t st) {
-    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, SPLIT>;
+    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB>;
     size_t smem = g.smem;
     // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
     // previous chunk can be co-resident (overlap experiment knob)
@@ -498,8 +494,6 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
         case 1: return launch_lowres_gray_g<1, 8, 9, 9>(lp, g, images, P, st);
         case 2: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 4>(lp, g, images, P, st);
         case 3: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3>(lp, g, images, P, st);
-        case 4: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, true>(lp, g, images, P, st);
-        case 5: return launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, true>(lp, g, images, P, st);
     }
     return FGF_ERR_UNSUPPORTED;
 }

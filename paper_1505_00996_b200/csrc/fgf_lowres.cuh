@@ -94,17 +94,19 @@ __device__ __forceinline__ double inv_count(int i, int n, int R) {
     return 1.0 / (double)(min(n - 1, i + R) - max(0, i - R) + 1);
 }
 
-// grid (strips, segments, images), block NT (>= TW + 4R, multiple of 32, G * nrA <= NT and
-// G * nrB <= NT), dynamic smem LowresCfg::layout(...).total.
+// grid (strips, segments, images), block NT (>= TW + 4R, multiple of 32), dynamic smem
+// LowresCfg::layout(...).total.
 // RING = false: no sample ring; the subtracted row is re-read from global memory (L2) and
 // prefetched together with the added row.  MAXT / MINB: launch bounds.
-// SPLIT (CP = 1): the two lanes of a pair share each horizontal run -- stage A: lane 0 slides
-// I', I'I', lane 1 slides p', I'p', and they swap (mean, second moment) by shuffle for the
-// epilogue; stage B: one map per lane -- so twice as many threads work in those phases.
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
-          bool SPLIT = false>
+//
+// Schedule: two barrier intervals per batch of G rows.
+//   X (column threads):  stage-B column phase of the batch of outputs whose a, b windows are
+//                        complete, then the stage-A column phase of the next G a, b rows;
+//   Y (run threads):     stage-A horizontal phase + epilogue of those a, b rows on threads
+//                        [0, TA), and concurrently the stage-B horizontal phase of the outputs
+//                        on threads [TA, TA + TB); then the staged outputs are stored.
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1>
 __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P) {
-    static_assert(!SPLIT || CP == 1, "lane-pair split is for one p channel");
     using C = LowresCfg<CP, G, KA, KB, RING>;
     constexpr int NIN = C::NIN, NMAP = C::NMAP, NAB = C::NAB;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -145,13 +147,14 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     const float* bI = P.srcI + img * P.imgI + offc;
     const float* bP = P.srcP + img * P.imgP + offc;
     const int row = P.row, planeP = P.planeP;
+    const long long dP = bP - bI;
     auto load = [&](int y, float* v) {
-        const int o = y * row;
-        v[0] = __ldg(bI + o);
+        const float* pi = bI + (long long)y * row;
+        v[0] = __ldg(pi);
 #pragma unroll
-        for (int c = 0; c < CP; ++c) v[1 + c] = __ldg(bP + o + c * planeP);
+        for (int c = 0; c < CP; ++c) v[1 + c] = __ldg(pi + dP + c * planeP);
     };
-    // accumulate (sgn = +1) or remove (-1) one sample row: [I, II, p_c, Ip_c], exact products
+    // add (sub = false) or remove one sample row: [I, II, p_c, Ip_c], exact products in fp64
     auto accum = [&](double* acc, const float* v, bool sub) {
         const double I = (double)v[0];
         acc[0] = sub ? acc[0] - I : acc[0] + I;
@@ -163,7 +166,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             acc[2 + CP + c] = sub ? fma(-I, p, acc[2 + CP + c]) : fma(I, p, acc[2 + CP + c]);
         }
     };
-    const int ringStride = NIN * NT;              // floats between ring slots
+    const int ringStride = NIN * NT;              // floats between sample-ring slots
     float* inr = INr + tid;                       // slot s, input k at inr[s*ringStride + k*NT]
 
     double accA[NMAP];
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     // subtracted, ya - R, sits in the next slot (RBI = 2R + 1).
     int sAdd = (yA0 + R) % RBI;
     if (colA) {
-        // warm-up: rows [yA0 - R, yA0 + R - 1] clipped, kept in their ring slots
+        // warm-up: rows [yA0 - R, yA0 + R - 1] clipped (kept in their ring slots)
         const int wa = max(0, yA0 - R), wb = min(h, yA0 + R);
         for (int y = wa; y < wb; ++y) {
             float v[NIN];
@@ -187,13 +190,12 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             accum(accA, v, false);
         }
     }
-    // prefetch of the add rows (and without the ring, the subtract rows) of the next batch
+    // prefetch of the add rows (and without the ring, the subtract rows) of a batch
     float nv[G][NIN];
     float sv[RING ? 1 : G][NIN];
-    const long long dP = bP - bI;
     auto load_batch = [&](int ya) {
-        const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
         if (!colA) return;
+        const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
         const float* pi = bI + (long long)(ya + R) * row;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -219,127 +221,74 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             }
         }
     };
-    load_batch(yA0);
+    // stage-A column phase: vertical sums of a, b rows [ya, ya + nA) -> VsA
+    auto column_A = [&](int ya0, int nA) {
+        if (!colS) return;
+        int s = sAdd;
+        double* vcol = VsA + tid;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (g < nA) {
+                const int ya = ya0 + g;
+                const int ss = (s + 1 == RBI) ? 0 : s + 1;
+                if (colA && ya + R < h) {
+                    if (RING) {
+                        float* slot = inr + s * ringStride;
+#pragma unroll
+                        for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
+                    }
+                    accum(accA, nv[g], false);
+                }
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
+                if (colA && ya - R >= 0) {
+                    if (RING) {
+                        const float* slot = inr + ss * ringStride;
+                        float v[NIN];
+#pragma unroll
+                        for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
+                        accum(accA, v, true);
+                    } else {
+                        accum(accA, sv[RING ? 0 : g], true);
+                    }
+                }
+                s = ss;
+            }
+        }
+        sAdd = s;
+    };
 
-    // stage B column state: a, b column j = tid (local), ca = x0 - R + j
+    // stage-B column state: a, b column j = tid (local), ca = x0 - R + j
     const bool colB = tid < L.NCA;
     float accB[NAB];
 #pragma unroll
     for (int m = 0; m < NAB; ++m) accB[m] = 0.0f;
-    bool warmB = false;
 
-    // fixed horizontal task of this thread: row g of a batch, run of K columns
-    // (SPLIT: task tid / 2, half tid % 2)
-    const int tq = SPLIT ? tid >> 1 : tid, hf = SPLIT ? tid & 1 : 0;
-    const int gA = tq / L.nrA, jA0 = (tq - gA * L.nrA) * KA;
-    const int tB = SPLIT ? tid / NAB : tid, mB = SPLIT ? tid - tB * NAB : 0;
-    const int gB = tB / L.nrB, kB0 = (tB - gB * L.nrB) * KB;
-    const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0 + (SPLIT ? 2 * hf * VPA : 0);
-    const float* hvB = VsB + (size_t)gB * NAB * VPB + kB0 + (SPLIT ? mB * VPB : 0);
+    // horizontal tasks: q < TA -> stage A (row gA, run jA0), TA <= q < TA + TB -> stage B
+    const int TA = G * L.nrA, TB = G * L.nrB;
+    const int qB = tid - TA;
+    const int gA = tid / L.nrA, jA0 = (tid - gA * L.nrA) * KA;
+    const int gB = qB / L.nrB, kB0 = (qB - gB * L.nrB) * KB;
+    const bool runA = tid < TA, runB = qB >= 0 && qB < TB;
+    const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0;
+    const float* hvB = VsB + (size_t)(runB ? gB : 0) * NAB * VPB + (runB ? kB0 : 0);
 
-    int yA = yA0, yb = y0;
-    int sA = yA0 % RBA;                           // ring slot of a, b row yA
-    int prevB = 0, prevYb = 0;                    // outputs staged in Os, not yet stored
     const size_t n = (size_t)h * w;
     float* dstimg = P.dst + (size_t)img * NAB * n;
 
-    auto store_prev = [&]() {
-        if (prevB > 0 && tid < TW && x0 + tid < w) {
-            float* d = dstimg + (size_t)prevYb * w + x0 + tid;
-            const float* os = Os + tid;
-            for (int g = 0; g < prevB; ++g) {
-#pragma unroll
-                for (int m = 0; m < NAB; ++m) d[(size_t)m * n] = os[m * PB];
-                d += w;
-                os += NAB * PB;
-            }
-        }
-    };
+    int yA = yA0;                                 // first a, b row of the batch in VsA
+    int sA = yA0 % RBA;                           // ring slot of a, b row yA
+    int nA = max(0, min(G, yA1 - yA));            // a, b rows in VsA
+    int yb = y0;                                  // next output row
+    int hbY = 0, hbN = 0;                         // outputs whose vertical sums are in VsB
 
+    load_batch(yA);
+    column_A(yA, nA);
+    if (nA > 0) load_batch(yA + nA);
     __syncthreads();
-    while (yb < yB1) {
-        const int nA = max(0, min(G, yA1 - yA));
-        // ---- stage A, column phase: G rows of vertical sums -> VsA
-        if (nA > 0 && colS) {
-            int s = sAdd;
-            double* vcol = VsA + tid;
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                if (g < nA) {
-                    const int ya = yA + g;
-                    const int ss = (s + 1 == RBI) ? 0 : s + 1;
-                    if (colA && ya + R < h) {
-                        if (RING) {
-                            float* slot = inr + s * ringStride;
-#pragma unroll
-                            for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
-                        }
-                        accum(accA, nv[g], false);
-                    }
-#pragma unroll
-                    for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
-                    if (colA && ya - R >= 0) {
-                        if (RING) {
-                            const float* slot = inr + ss * ringStride;
-                            float v[NIN];
-#pragma unroll
-                            for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
-                            accum(accA, v, true);
-                        } else {
-                            accum(accA, sv[RING ? 0 : g], true);
-                        }
-                    }
-                    s = ss;
-                }
-            }
-            sAdd = s;
-        }
-        __syncthreads();
-        store_prev();
-        prevB = 0;
-        if (nA > 0) load_batch(yA + nA);
-
-        // ---- stage A, horizontal phase + coefficient epilogue -> a, b ring rows
-        if (SPLIT) {
-            const unsigned act = __ballot_sync(0xffffffffu, gA < nA);
-            if (gA < nA) {
-                const int ya = yA + gA;
-                const double invy = inv_count(ya, h, R);
-                int sl = sA + gA;
-                if (sl >= RBA) sl -= RBA;
-                float* ab = ABr + (size_t)(sl * NAB + hf) * PA + jA0;   // lane 0: a, lane 1: b
-                const double* ix = invxA + jA0;
-                const double* vw = hvA + 2 * R + 1;
-                double S0 = 0.0, S1 = 0.0;
-#pragma unroll 4
-                for (int k = 0; k <= 2 * R; ++k) {
-                    S0 += hvA[k];
-                    S1 += hvA[VPA + k];
-                }
-#pragma unroll
-                for (int i = 0; i < KA; ++i) {
-                    const double inv = ix[i] * invy;       // 0 outside the image -> a = b = 0
-                    const double u = S0 * inv, v = S1 * inv;   // lane 0: mean_I, corr_I
-                    double y = v;                              // lane 1: mean_p, corr_Ip
-                    if (hf == 0) {
-                        y = fma(-u, u, v);                     // var_I
-                        y = y < 0.0 ? 0.0 : y;                 // R8
-                    }
-                    const double xo = __shfl_xor_sync(act, u, 1);
-                    const double yo = __shfl_xor_sync(act, y, 1);
-                    const double mI = hf ? xo : u, mp = hf ? u : xo;
-                    const double var = hf ? yo : y, cIp = hf ? v : yo;
-                    const double cov = fma(-mI, mp, cIp);       // cov_Ip
-                    const float rden = __fdividef(1.0f, (float)(var + P.eps));
-                    const float a = (float)cov * rden;          // Eq.2 / P:80
-                    ab[i] = hf ? fmaf(-a, (float)mI, (float)mp) : a;   // Eq.3 / P:81
-                    if (i + 1 < KA) {
-                        S0 += vw[i] - hvA[i];
-                        S1 += vw[VPA + i] - hvA[VPA + i];
-                    }
-                }
-            }
-        } else if (gA < nA) {
+    for (;;) {
+        // ================= Y: horizontal phases
+        if (runA && gA < nA) {
             const int ya = yA + gA;
             const double invy = inv_count(ya, h, R);
             int sl = sA + gA;
@@ -376,12 +325,49 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                 }
             }
         }
+        if (runB && gB < hbN) {
+            const float invy = (float)inv_count(hbY + gB, h, R);
+            const float* ix = invxB + kB0;
+            const float* vw = hvB + 2 * R + 1;
+            float S[NAB];
+#pragma unroll
+            for (int m = 0; m < NAB; ++m) S[m] = 0.0f;
+#pragma unroll 4
+            for (int k = 0; k <= 2 * R; ++k)
+#pragma unroll
+                for (int m = 0; m < NAB; ++m) S[m] += hvB[m * VPB + k];
+            float* o = Os + (size_t)gB * NAB * PB + kB0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+                const float inv = ix[i] * invy;
+#pragma unroll
+                for (int m = 0; m < NAB; ++m) o[m * PB + i] = S[m] * inv;
+                if (i + 1 < KB) {
+#pragma unroll
+                    for (int m = 0; m < NAB; ++m) S[m] += vw[m * VPB + i] - hvB[m * VPB + i];
+                }
+            }
+        }
         __syncthreads();
+        // coalesced store of the outputs staged in Os
+        if (hbN > 0 && tid < TW && x0 + tid < w) {
+            float* d = dstimg + (size_t)hbY * w + x0 + tid;
+            const float* os = Os + tid;
+            for (int g = 0; g < hbN; ++g) {
+#pragma unroll
+                for (int m = 0; m < NAB; ++m) d[(size_t)m * n] = os[m * PB];
+                d += w;
+                os += NAB * PB;
+            }
+        }
+        hbN = 0;
+        if (yb >= yB1) break;
         yA += nA;
         sA += nA;
         if (sA >= RBA) sA -= RBA;
 
-        // ---- stage B: outputs whose a, b windows are complete
+        // ================= X: column phases
+        // stage B: outputs whose a, b windows [y - R, y + R] are complete (rows < yA)
         const int allowed = (yA >= yA1) ? yB1 : min(yB1, yA - R);
         const int nB = min(G, allowed - yb);
         if (nB > 0) {
@@ -391,7 +377,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                     s = s < 0 ? s + RBA : s;
                     return ABr + (size_t)s * NAB * PA + tid;
                 };
-                if (!warmB) {
+                if (yb == y0) {                   // warm-up: rows [y0 - R, y0 + R - 1]
                     for (int y = max(0, y0 - R); y < min(h, y0 + R); ++y) {
                         const float* r = slotp(y);
 #pragma unroll
@@ -418,51 +404,18 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                     }
                 }
             }
-            warmB = true;
-            __syncthreads();
-            if (SPLIT && gB < nB) {                    // one map per lane
-                const float invy = (float)inv_count(yb + gB, h, R);
-                const float* ix = invxB + kB0;
-                const float* vw = hvB + 2 * R + 1;
-                float S = 0.0f;
-#pragma unroll 4
-                for (int k = 0; k <= 2 * R; ++k) S += hvB[k];
-                float* o = Os + (size_t)(gB * NAB + mB) * PB + kB0;
-#pragma unroll
-                for (int i = 0; i < KB; ++i) {
-                    o[i] = S * (ix[i] * invy);
-                    if (i + 1 < KB) S += vw[i] - hvB[i];
-                }
-            } else if (!SPLIT && gB < nB) {
-                const float invy = (float)inv_count(yb + gB, h, R);
-                const float* ix = invxB + kB0;
-                const float* vw = hvB + 2 * R + 1;
-                float S[NAB];
-#pragma unroll
-                for (int m = 0; m < NAB; ++m) S[m] = 0.0f;
-#pragma unroll 4
-                for (int k = 0; k <= 2 * R; ++k)
-#pragma unroll
-                    for (int m = 0; m < NAB; ++m) S[m] += hvB[m * VPB + k];
-                float* o = Os + (size_t)gB * NAB * PB + kB0;
-#pragma unroll
-                for (int i = 0; i < KB; ++i) {
-                    const float inv = ix[i] * invy;
-#pragma unroll
-                    for (int m = 0; m < NAB; ++m) o[m * PB + i] = S[m] * inv;
-                    if (i + 1 < KB) {
-#pragma unroll
-                        for (int m = 0; m < NAB; ++m) S[m] += vw[m * VPB + i] - hvB[m * VPB + i];
-                    }
-                }
-            }
-            prevB = nB;
-            prevYb = yb;
+            hbY = yb;
+            hbN = nB;
             yb += nB;
         }
+        // stage A: the next batch of a, b rows
+        nA = max(0, min(G, yA1 - yA));
+        if (nA > 0) {
+            column_A(yA, nA);
+            load_batch(yA + nA);
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    store_prev();
 }
 
 }  // namespace fgf

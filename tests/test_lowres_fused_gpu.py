@@ -69,7 +69,7 @@ CASES = [
 
 
 # kernel variants (fgf_api.cu kLrNumVariants): 0 = sample ring, G 4; 1 = G 8; 2 / 3 = no ring
-VARIANTS = [None, "0", "1", "2", "4", "5"]
+VARIANTS = [None, "0", "1", "2"]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -78,7 +78,7 @@ def test_fused_lowres_vs_oracle(case, variant):
     B, H, W, CP, r, eps, s, sub, TH, NT = case
     if variant is not None and CP > 1:
         pytest.skip("one kernel variant for several p channels")
-    if variant in ("2", "3", "4"):
+    if variant in ("2", "3"):
         NT = 128 if NT is None else min(NT, 160)
     g = torch.Generator(device="cuda").manual_seed(abs(hash(case)) % (2 ** 31))
     I = torch.rand((B, 1, H, W), device="cuda", generator=g)
