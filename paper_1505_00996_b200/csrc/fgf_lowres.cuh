@@ -74,8 +74,8 @@ struct LowresCfg {
         if (L.VPA < NT) L.VPA = NT;
         L.VPB = L.PB + 2 * R + 1;
         if (L.VPB < L.PA) L.VPB = L.PA;
-        L.RBA = 2 * R + G;
-        L.RBI = 2 * R + 1;
+        L.RBA = 2 * R + G + 1;                   // a, b rows [yb - R - 1, yA) live at once
+        L.RBI = 2 * R + 2;                       // sample rows [ya - R - 1, ya + R]
         size_t o = 0;
         L.oVsA = o; o = al16(o + (size_t)G * NMAP * L.VPA * 8);
         L.oVsB = o; o = al16(o + (size_t)G * NAB * L.VPB * 4);
@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     const int x0 = blockIdx.x * TW;
     const int y0 = blockIdx.y * P.TH;
     const int yB1 = min(h, y0 + P.TH);            // outputs [y0, yB1)
-    const int yA0 = max(0, y0 - R);               // a, b rows [yA0, yA1)
+    // a, b rows [yA0, yA1): the output windows need [y0 - R, yB1 + R); one more row on top
+    // because stage B's first step removes row y0 - R - 1 from its running window
+    const int yA0 = max(0, y0 - R - 1);
     const int yA1 = min(h, yB1 + R);
     const int VPA = L.VPA, VPB = L.VPB, PA = L.PA, PB = L.PB, RBA = L.RBA, RBI = L.RBI;
 
@@ -172,12 +174,13 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     double accA[NMAP];
 #pragma unroll
     for (int m = 0; m < NMAP; ++m) accA[m] = 0.0;
-    // The row added when producing a, b row ya is ya + R, in slot (ya + R) mod RBI; the row
-    // subtracted, ya - R, sits in the next slot (RBI = 2R + 1).
+    // The window of a, b row ya moves down by one row: add sample row ya + R, remove row
+    // ya - R - 1.  Ring slots: row ya + R in slot (ya + R) mod RBI, row ya - R - 1 in the next
+    // slot (RBI = 2R + 2).
     int sAdd = (yA0 + R) % RBI;
     if (colA) {
-        // warm-up: rows [yA0 - R, yA0 + R - 1] clipped (kept in their ring slots)
-        const int wa = max(0, yA0 - R), wb = min(h, yA0 + R);
+        // warm-up: the window of row yA0 - 1, rows [yA0 - R - 1, yA0 + R - 1] clipped
+        const int wa = max(0, yA0 - R - 1), wb = min(h, yA0 + R);
         for (int y = wa; y < wb; ++y) {
             float v[NIN];
             load(y, v);
@@ -197,61 +200,91 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         if (!colA) return;
         const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
         const float* pi = bI + (long long)(ya + R) * row;
+        if (ng >= G) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            if (g < ng) {
+            for (int g = 0; g < G; ++g) {
                 nv[g][0] = __ldg(pi);
 #pragma unroll
                 for (int c = 0; c < CP; ++c) nv[g][1 + c] = __ldg(pi + dP + c * planeP);
+                pi += row;
             }
-            pi += row;
+        } else {
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                if (g < ng) {
+                    nv[g][0] = __ldg(pi);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) nv[g][1 + c] = __ldg(pi + dP + c * planeP);
+                }
+                pi += row;
+            }
         }
         if (!RING) {
-            const int g0 = max(0, R - ya);                 // subtract rows ya + g - R >= 0
+            const int g0 = max(0, R + 1 - ya);             // subtract rows ya + g - R - 1 >= 0
             const int g1 = min(G, yA1 - ya);
-            const float* ps = bI + (long long)(ya - R) * row;
+            const float* ps = bI + (long long)(ya - R - 1) * row;
+            if (g0 == 0 && g1 == G) {
 #pragma unroll
-            for (int g = 0; g < (RING ? 1 : G); ++g) {
-                if (g >= g0 && g < g1) {
+                for (int g = 0; g < (RING ? 1 : G); ++g) {
                     sv[g][0] = __ldg(ps);
 #pragma unroll
                     for (int c = 0; c < CP; ++c) sv[g][1 + c] = __ldg(ps + dP + c * planeP);
+                    ps += row;
                 }
-                ps += row;
+            } else {
+#pragma unroll
+                for (int g = 0; g < (RING ? 1 : G); ++g) {
+                    if (g >= g0 && g < g1) {
+                        sv[g][0] = __ldg(ps);
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) sv[g][1 + c] = __ldg(ps + dP + c * planeP);
+                    }
+                    ps += row;
+                }
             }
         }
     };
-    // stage-A column phase: vertical sums of a, b rows [ya, ya + nA) -> VsA
+    // one row step: acc += f(add row) - f(sub row), as one difference per map (short chains)
+    auto step = [&](const float* va, const float* vs, bool hasA, bool hasS) {
+        const double Ia = hasA ? (double)va[0] : 0.0, Is = hasS ? (double)vs[0] : 0.0;
+        accA[0] += Ia - Is;
+        accA[1] += fma(Ia, Ia, -(Is * Is));
+#pragma unroll
+        for (int c = 0; c < CP; ++c) {
+            const double pa = hasA ? (double)va[1 + c] : 0.0, ps = hasS ? (double)vs[1 + c] : 0.0;
+            accA[2 + c] += pa - ps;
+            accA[2 + CP + c] += fma(Ia, pa, -(Is * ps));
+        }
+    };
+    // stage-A column phase: vertical sums of a, b rows [ya0, ya0 + nA) -> VsA.  Columns
+    // outside the image keep the zeros written at the start.
     auto column_A = [&](int ya0, int nA) {
-        if (!colS) return;
+        if (!colA) return;
         int s = sAdd;
         double* vcol = VsA + tid;
+        const bool full = nA == G && ya0 - R - 1 >= 0 && ya0 + G - 1 + R < h;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            if (g < nA) {
+            if (full || g < nA) {
                 const int ya = ya0 + g;
                 const int ss = (s + 1 == RBI) ? 0 : s + 1;
-                if (colA && ya + R < h) {
-                    if (RING) {
+                const bool hasA = full || ya + R < h, hasS = full || ya - R - 1 >= 0;
+                float vsub[NIN];
+                if (RING) {
+                    if (hasA) {
                         float* slot = inr + s * ringStride;
 #pragma unroll
                         for (int k = 0; k < NIN; ++k) slot[k * NT] = nv[g][k];
                     }
-                    accum(accA, nv[g], false);
-                }
-#pragma unroll
-                for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
-                if (colA && ya - R >= 0) {
-                    if (RING) {
+                    if (hasS) {
                         const float* slot = inr + ss * ringStride;
-                        float v[NIN];
 #pragma unroll
-                        for (int k = 0; k < NIN; ++k) v[k] = slot[k * NT];
-                        accum(accA, v, true);
-                    } else {
-                        accum(accA, sv[RING ? 0 : g], true);
+                        for (int k = 0; k < NIN; ++k) vsub[k] = slot[k * NT];
                     }
                 }
+                step(nv[g], RING ? vsub : sv[RING ? 0 : g], hasA, hasS);
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m) vcol[(g * NMAP + m) * VPA] = accA[m];
                 s = ss;
             }
         }
@@ -260,6 +293,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
 
     // stage-B column state: a, b column j = tid (local), ca = x0 - R + j
     const bool colB = tid < L.NCA;
+    const bool colBv = colB && x0 - R + tid >= 0 && x0 - R + tid < w;   // inside the image
     float accB[NAB];
 #pragma unroll
     for (int m = 0; m < NAB; ++m) accB[m] = 0.0f;
@@ -371,36 +405,38 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         const int allowed = (yA >= yA1) ? yB1 : min(yB1, yA - R);
         const int nB = min(G, allowed - yb);
         if (nB > 0) {
-            if (colB) {
-                auto slotp = [&](int y) {         // a, b row y (y >= yA - RBA), this column
+            if (colBv) {
+                // row y of the a, b ring (y >= yA - RBA) for this column
+                auto slotp = [&](int y) {
                     int s = sA - (yA - y);
                     s = s < 0 ? s + RBA : s;
                     return ABr + (size_t)s * NAB * PA + tid;
                 };
-                if (yb == y0) {                   // warm-up: rows [y0 - R, y0 + R - 1]
-                    for (int y = max(0, y0 - R); y < min(h, y0 + R); ++y) {
+                const float* ring_end = ABr + (size_t)RBA * NAB * PA + tid;
+                const int rstep = NAB * PA, rlen = RBA * NAB * PA;
+                if (yb == y0) {                   // warm-up: window of y0 - 1
+                    for (int y = max(0, y0 - R - 1); y < min(h, y0 + R); ++y) {
                         const float* r = slotp(y);
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) accB[m] += r[m * PA];
                     }
                 }
+                const float* pa = slotp(min(yb + R, h - 1));
+                const float* ps = slotp(max(yb - R - 1, 0));
                 float* vcol = VsB + tid;
+                const bool full = nB == G && yb - R - 1 >= 0 && yb + G - 1 + R < h;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    if (g < nB) {
+                    if (full || g < nB) {
                         const int y = yb + g;
-                        if (y + R < h) {
-                            const float* r = slotp(y + R);
+                        const bool hasA = full || y + R < h, hasS = full || y - R - 1 >= 0;
 #pragma unroll
-                            for (int m = 0; m < NAB; ++m) accB[m] += r[m * PA];
-                        }
+                        for (int m = 0; m < NAB; ++m)
+                            accB[m] += (hasA ? pa[m * PA] : 0.0f) - (hasS ? ps[m * PA] : 0.0f);
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) vcol[(g * NAB + m) * VPB] = accB[m];
-                        if (y - R >= 0) {
-                            const float* r = slotp(y - R);
-#pragma unroll
-                            for (int m = 0; m < NAB; ++m) accB[m] -= r[m * PA];
-                        }
+                        if (hasA) { pa += rstep; if (pa >= ring_end) pa -= rlen; }
+                        if (hasS) { ps += rstep; if (ps >= ring_end) ps -= rlen; }
                     }
                 }
             }
