@@ -397,6 +397,8 @@ constexpr size_t kLrSmemMax = 227 * 1024;
 // is used unless FGF_LR_V selects one (development sweep).
 //   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
 //   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
+// (measured on config 4, profiles/round1/k13_variants.txt: G 8 / K 17 and G 6 / K 13 without
+// the ring, and a lane-pair split of the runs, were slower)
 constexpr int kLrNumVariants = 4;
 
 // Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
