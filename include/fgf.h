@@ -39,8 +39,9 @@
  * deterministic (no atomics; fixed reduction order) and independent of batch size and of
  * how a batch is split across calls or devices.
  *
- * PRECISION.  fp32 storage; box statistics, var/cov, the 3x3 solve and a, b in fp64;
- * box of a, b accumulated in fp64; upsample + output in fp32.
+ * PRECISION.  fp32 storage; box statistics, var/cov and the 3x3 solve in fp64; a, b stored
+ * in fp32; the box of a, b accumulated in fp64 (colour guidance) or fp32 (gray guidance,
+ * DESIGN.md R17); upsample + output in fp32.
  */
 #ifndef FGF_H
 #define FGF_H
