@@ -504,6 +504,12 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
 int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaStream_t st,
                        bool dry = false) {
     if (P.CI != 1) return FGF_ERR_UNSUPPORTED;
+    // K13's horizontal restarts cost (2r' + 1) / K per output and its a, b ring 2r' + G + 1
+    // rows: measured faster than the strip engine at r' = 4 and 8, slower at r' = 16 and 32
+    // (config 4 at s = 8, 4, 2, 1), so wide windows take the strip engine.
+    int rmax = 12;
+    if (const char* e = getenv("FGF_LR_RMAX")) rmax = atoi(e);
+    if (P.R > rmax) return FGF_ERR_UNSUPPORTED;
     if (const char* e = getenv("FGF_LOWRES")) {
         if (strcmp(e, "strip") == 0) return FGF_ERR_UNSUPPORTED;
     }
