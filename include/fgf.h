@@ -140,6 +140,19 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
                              int W, int C_I, int C_p, int H_total, int h_total, int w, int Y0,
                              int y0_maps, int h_maps, void* cuda_stream);
 
+/* Detail enhancement, the application of PAPER.md Fig. 2 ("enhanced images with x5
+ * detail"; SPEC S:303-311 enhance): out = (I - q) * gain + q, with q the SELF-guided fast
+ * guided filter of I (p = I, C_p = C_I = C in {1, 3}) with these r, eps, s, sub_mode.  Since
+ * out = gain I + (1 - gain)(mean_a^T I + mean_b), the enhancement is folded into the mean
+ * maps as they are written (a_cc -> (1 - gain) a_cc + gain, the rest scaled by 1 - gain):
+ * same kernels, same HBM bytes as fgf_filter_ws.  gain = 1 returns I exactly, gain = 0 is
+ * the filter.  DEVICE buffers I, out: [batch][C][H][W]; out may not overlap I; no clamp
+ * (S:266).  Workspace as fgf_filter_ws (fgf_workspace_bytes(batch, H, W, C, C, r, s)).
+ * Errors: as fgf_filter_ws; gain < 0 or not finite -> FGF_ERR_PARAM. */
+int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, int r,
+                   double eps, int s, int sub_mode, double gain, void* workspace,
+                   size_t ws_bytes, void* cuda_stream);
+
 /* Diagnostics (single-threaded use): per-kernel CUDA-event timing of the launches this
  * process enqueues.  fgf_profile_enable(1) clears old records and starts recording an event
  * pair around every kernel launch on its launching stream; fgf_profile_enable(0) stops.

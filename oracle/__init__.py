@@ -183,3 +183,14 @@ def fast_guided_filter(I, p, r: int, eps: float, s: int, sub_mode: int = NEAREST
 def guided_filter(I, p, r: int, eps: float) -> np.ndarray:
     """Alg. 1: the s = 1 case of Alg. 2."""
     return fast_guided_filter(I, p, r, eps, 1, NEAREST)
+
+
+def enhance(I, gain: float, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
+    """Detail enhancement (PAPER.md Fig. 2 caption P:95-97, "enhanced images with x5 detail";
+    SPEC S:303-306 enhance): base = the self-guided filter of the image (I = p), then
+    out = (I - base) * gain + base, in double, unclamped (S:266)."""
+    I = _f32(I)
+    if I.ndim == 2:
+        I = I[None, None]
+    base = fast_guided_filter(I, I, r, eps, s, sub_mode)
+    return (I.astype(np.float64) - base) * gain + base

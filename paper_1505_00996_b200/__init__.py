@@ -39,7 +39,8 @@ FGF_SUB_BILINEAR = 1
 EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_host",
            "fgf_coefficients", "fgf_upsample_output", "fgf_last_launch_count", "fgf_status_str",
            "fgf_version", "fgf_profile_enable", "fgf_profile_read", "fgf_subsample",
-           "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows")
+           "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows",
+           "fgf_enhance_ws")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -73,6 +74,8 @@ _lib.fgf_lowres_mean.argtypes = [_P, _P, _P, _i, _i, _i, _i, _i, _i, _d, _P, _sz
 _lib.fgf_lowres_mean.restype = _i
 _lib.fgf_upsample_output_rows.argtypes = [_P, _P, _P] + [_i] * 11 + [_P]
 _lib.fgf_upsample_output_rows.restype = _i
+_lib.fgf_enhance_ws.argtypes = [_P, _P, _i, _i, _i, _i, _i, _d, _i, _i, _d, _P, _sz, _P]
+_lib.fgf_enhance_ws.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -212,6 +215,15 @@ def fgf_upsample_output_rows(I, mean_ab, q, batch, rows, W, C_I, C_p, H_total, h
     return rc
 
 
+def fgf_enhance_ws(I, out, batch, H, W, C, r, eps, s, sub_mode, gain, workspace, ws_bytes,
+                   stream=None, check=True):
+    rc = _lib.fgf_enhance_ws(_addr(I), _addr(out), batch, H, W, C, r, float(eps), s, sub_mode,
+                             float(gain), _addr(workspace), ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_enhance_ws")
+    return rc
+
+
 # ----------------------------------------------------------------- torch convenience layer
 
 def _geom(I, p):
@@ -280,3 +292,23 @@ def upsample_output(I, mean_ab, s, stream=None):
     st = stream if stream is not None else torch.cuda.current_stream(I.device)
     fgf_upsample_output(I, mean_ab.contiguous(), q, B, H, W, C_I, C_p, s, st)
     return q
+
+
+def enhance(I, gain=5.0, r=16, eps=0.01, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None,
+            workspace=None):
+    """Detail enhancement (Fig. 2; defaults = its r=16, eps=0.1^2, s=4, x5):
+    out = (I - q) gain + q with q the self-guided fast guided filter of I [B, C, H, W]."""
+    import torch
+    if I.dim() != 4 or not I.is_cuda or I.dtype != torch.float32 or not I.is_contiguous():
+        raise ValueError("I must be a contiguous float32 CUDA tensor [B, C, H, W]")
+    B, C, H, W = I.shape
+    if out is None:
+        out = torch.empty_like(I)
+    ws = workspace or Workspace()
+    nbytes = fgf_workspace_bytes(B, H, W, C, C, r, s)
+    if nbytes == 0:
+        _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
+    buf = ws.get(nbytes, I.device)
+    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    fgf_enhance_ws(I, out, B, H, W, C, r, eps, s, sub_mode, gain, buf, buf.numel(), st)
+    return out

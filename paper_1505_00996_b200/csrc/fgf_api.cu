@@ -80,6 +80,7 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct Plan {
     int batch, H, W, CI, CP, r, s, sub;
     double eps;
+    float k1 = 1.0f, k0 = 0.0f;   // mean-map fold (detail enhancement), identity by default
     int h, w, R, NC;
     size_t N, n;
     int chunk;
@@ -534,6 +535,7 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
     if (launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) {
         LowresParams lp{};
         lp.h = P.h; lp.w = P.w; lp.R = P.R; lp.eps = P.eps;
+        lp.k1 = P.k1; lp.k0 = P.k0;
         lp.dst = mean;
         if (P.s > 1 && P.sub == FGF_SUB_BILINEAR) {
             float* Is = planes;
@@ -571,6 +573,7 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
         sp.row = P.W; sp.col = 1;
     }
     sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
+    sp.k1 = 1.0f; sp.k0 = 0.0f;
 
     // Steps 2-4: statistics + coefficients a, b.
     sp.dst = coef;
@@ -583,6 +586,7 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
     mp.row = P.w; mp.col = 1;
     mp.dst = mean;
     mp.h = P.h; mp.w = P.w; mp.R = P.R; mp.eps = P.eps;
+    mp.k1 = P.k1; mp.k0 = P.k0;
     return launch_strip<MODE_MEAN>(mp, nb, P, st);
 }
 
@@ -765,6 +769,21 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
     if (rc) return rc;
     if ((rc = check_pointers(I, p, q, P, true))) return rc;
     return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, int r,
+                   double eps, int s, int sub_mode, double gain, void* workspace,
+                   size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C, C, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if (!std::isfinite(gain) || gain < 0.0) return FGF_ERR_PARAM;
+    if ((rc = check_pointers(I, I, out, P, true))) return rc;
+    // out = (I - q) gain + q = gain I + (1 - gain)(mean_a^T I + mean_b): fold into the maps
+    P.k1 = (float)(1.0 - gain);
+    P.k0 = (float)gain;
+    return run_all(I, I, out, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,

@@ -172,6 +172,10 @@ struct StripParams {
     int TW, TH;             // output columns per strip, output rows per segment
     int VP;                 // padded fp64 row length in shared memory: NT + 2R + K + 1
     double eps;
+    // MEAN only: the written maps are k1 * mean + k0 on the diagonal a maps (a_c for guide
+    // channel c), k1 * mean otherwise -- the detail-enhancement fold (fgf_enhance_ws);
+    // k1 = 1, k0 = 0 writes the means unchanged.
+    float k1, k0;
 };
 
 // Rows per batch G (each warp slides along one row of a batch), odd run length K, smem.
@@ -205,7 +209,9 @@ struct StripEpilogue;
 // Gray: a = cov/(max(var,0)+eps), b = mean_p - a mean_I (Eq.2-3, R8).
 template <int CP>
 struct StripEpilogue<MODE_STATS, 1, CP> {
-    __device__ static void emit(const double* S, double inv, double eps, float* dst, int ostride) {
+    __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
+                                int ostride) {
+        const double eps = P.eps;
         // The cancellations (var_I, cov_Ip: P:78-79) are formed in fp64; the quotient and b
         // (Eq.2-3) are well conditioned and are formed in fp32.
         const double mI = S[0] * inv;
@@ -228,7 +234,9 @@ struct StripEpilogue<MODE_STATS, 1, CP> {
 // v_c = corr_Ip_c - mu p_bar_c, b_c = p_bar_c - a_c^T mu; all fp64.
 template <int CP>
 struct StripEpilogue<MODE_STATS, 3, CP> {
-    __device__ static void emit(const double* S, double inv, double eps, float* dst, int ostride) {
+    __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
+                                int ostride) {
+        const double eps = P.eps;
         const double m0 = S[0] * inv, m1 = S[1] * inv, m2 = S[2] * inv;
         const double s00 = S[3] * inv - m0 * m0 + eps;
         const double s01 = S[4] * inv - m0 * m1;
@@ -264,9 +272,13 @@ struct StripEpilogue<MODE_STATS, 3, CP> {
 
 template <int CI, int CP>
 struct StripEpilogue<MODE_MEAN, CI, CP> {
-    __device__ static void emit(const double* S, double inv, double, float* dst, int ostride) {
+    __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
+                                int ostride) {
 #pragma unroll
-        for (int m = 0; m < (CI + 1) * CP; ++m) dst[m * ostride] = (float)(S[m] * inv);
+        for (int m = 0; m < (CI + 1) * CP; ++m) {
+            const int c = m / (CI + 1), j = m - c * (CI + 1);
+            dst[m * ostride] = fmaf(P.k1, (float)(S[m] * inv), j == c ? P.k0 : 0.0f);
+        }
     }
 };
 
@@ -434,7 +446,7 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
 #pragma unroll
             for (int i = 0; i < K; ++i) {
                 if (oc0 + i < ocn)
-                    StripEpilogue<MODE, CI, CP>::emit(S, invx[oc0 + i] * invy, P.eps, orow + i, NT);
+                    StripEpilogue<MODE, CI, CP>::emit(S, invx[oc0 + i] * invy, P, orow + i, NT);
                 if (i + 1 < K) {
 #pragma unroll
                     for (int m = 0; m < NMAP; ++m) S[m] += vr[m * VP + i + R + 1] - vr[m * VP + i - R];

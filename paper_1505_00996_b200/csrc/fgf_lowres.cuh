@@ -46,6 +46,7 @@ struct LowresParams {
     int h, w, R;
     int TW, TH;            // output columns per strip, output rows per segment
     double eps;
+    float k1, k0;          // written maps: k1 mean_a + k0 (map 0), k1 mean (others); 1, 0 = plain
 };
 
 template <int CP, int G, int KA, int KB, bool RING = true>
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             for (int i = 0; i < KB; ++i) {
                 const float inv = ix[i] * invy;
 #pragma unroll
-                for (int m = 0; m < NAB; ++m) o[m * PB + i] = S[m] * inv;
+                for (int m = 0; m < NAB; ++m) o[m * PB + i] = fmaf(P.k1, S[m] * inv, m == 0 ? P.k0 : 0.0f);
                 if (i + 1 < KB) {
 #pragma unroll
                     for (int m = 0; m < NAB; ++m) S[m] += vw[m * VPB + i] - hvB[m * VPB + i];

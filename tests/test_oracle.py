@@ -342,3 +342,19 @@ def test_rejects_invalid():
     # s = 1 on a 1-pixel-high image is accepted (R7)
     J = np.random.default_rng(0).random((1, 1, 1, 9)).astype(np.float32)
     assert np.isfinite(oracle.fast_guided_filter(J, J, 2, 0.1, 1)).all()
+
+
+# ---------------------------------------------------------------- application: enhancement
+
+def test_enhance_identities():
+    """gain = 1 returns the input exactly, gain = 0 returns the base layer; and the
+    detail layer scales linearly with the gain."""
+    rng = np.random.default_rng(31)
+    I = rng.random((1, 1, 40, 52)).astype(np.float32)
+    base = oracle.fast_guided_filter(I, I, 8, 0.01, 4)
+    assert np.allclose(oracle.enhance(I, 1.0, 8, 0.01, 4), I.astype(np.float64), rtol=0, atol=1e-15)
+    assert np.array_equal(oracle.enhance(I, 0.0, 8, 0.01, 4), base)
+    e5 = oracle.enhance(I, 5.0, 8, 0.01, 4)
+    assert np.allclose(e5 - base, 5.0 * (I - base), atol=1e-12)
+    I3 = rng.random((1, 3, 20, 24)).astype(np.float32)
+    assert np.allclose(oracle.enhance(I3, 1.0, 4, 0.01, 2), I3.astype(np.float64), rtol=0, atol=1e-15)
