@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--band-impl", choices=["c", "torch"], default="c",
+                    help="config 5 (4b): C-ABI band call with NCCL inside, or the Python stages")
     return ap.parse_args()
 
 
@@ -357,12 +359,30 @@ def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
     I_own = I[:, :, pl.Y0:pl.Y1].contiguous()
     p_own = p[:, :, pl.Y0:pl.Y1].contiguous()
     del I, p
-    ex = bands.DistExchange(rank, world)
-    backend = bands.GpuBackend()
     stream = torch.cuda.current_stream(dev)
+    comm = None
+    if args.band_impl == "c":
+        # fgf_filter_band: subsample, NCCL halo exchange and the rest inside libfgf.so; the
+        # NCCL unique id travels over the torch.distributed process group
+        if world > 1:
+            uid = [fgf.fgf_nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = fgf.fgf_nccl_comm_init(uid[0], rank, world)
+        rows = pl.Y1 - pl.Y0
+        q_own = torch.empty_like(p_own)
+        nb = fgf.fgf_band_workspace_bytes(H, W, pl.Y0, rows, 1, 1, r, s, world)
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
 
-    def step():
-        return bands.filter_band(I_own, p_own, r, eps, s, sub, H, rank, world, ex, backend)
+        def step():
+            fgf.fgf_filter_band(I_own, p_own, q_own, H, W, pl.Y0, rows, 1, 1, r, eps, s, sub,
+                                comm, rank, world, ws, nb, stream)
+            return q_own
+    else:
+        ex = bands.DistExchange(rank, world)
+        backend = bands.GpuBackend()
+
+        def step():
+            return bands.filter_band(I_own, p_own, r, eps, s, sub, H, rank, world, ex, backend)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -388,9 +408,13 @@ def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": c["name"], "H": H, "W": W, "r": r, "eps": eps, "s": s,
                            "parallelism": f"row bands x{world}, halo {pl.halo} low-res rows "
-                                          f"over torch.distributed P2P",
+                                          + ("fgf_filter_band (NCCL P2P inside libfgf.so)"
+                                             if args.band_impl == "c" else
+                                             "over torch.distributed P2P"),
                            "l2": "inputs larger than L2 (no flush needed)"}}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        fgf.fgf_nccl_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
 

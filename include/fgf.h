@@ -140,6 +140,45 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
                              int W, int C_I, int C_p, int H_total, int h_total, int w, int Y0,
                              int y0_maps, int h_maps, void* cuda_stream);
 
+/* ---------------------------------------------------------------------------------------
+ * One image split into row bands across ranks (BASELINE.json config 4b).
+ * Rank `rank` of `nranks` owns full-resolution rows [row0, row0 + rows) of an image of
+ * H_total x W (row0 a multiple of s; rows a multiple of s unless the band ends at H_total);
+ * with more than one rank every band must span at least 2r'+1 low-res rows.  I_band: DEVICE
+ * [C_I][rows][W], p_band: [C_p][rows][W] (may equal I_band when C_I = C_p = 1), q_band:
+ * [C_p][rows][W], all holding exactly the band's rows.  The call subsamples its rows, sends
+ * 2r'+1 low-res rows of I', p' to rank-1 / rank+1 and receives theirs (ncclSend / ncclRecv in
+ * one group on nccl_comm, enqueued on cuda_stream; one exchange, the single-step variant of
+ * DESIGN.md §7), runs the low-res chain on the extended band with global window clipping
+ * (R1) and writes q for its own rows with the global upsampling map (R5): the result equals
+ * the whole-image filter's rows.  nccl_comm is an ncclComm_t (fgf_nccl_comm_init); it may be
+ * NULL when nranks = 1.  Workspace: fgf_band_workspace_bytes(), caller-owned device memory.
+ * Errors: FGF_ERR_PARAM (band geometry, rank), FGF_ERR_SHAPE, FGF_ERR_NULL, FGF_ERR_ALIGN,
+ * FGF_ERR_ALIAS, FGF_ERR_DEVICE, FGF_ERR_NOMEM, FGF_ERR_NCCL (NCCL missing or a call failed),
+ * FGF_ERR_CUDA.  The NCCL library is loaded at run time (dlopen "libnccl.so.2"). */
+size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
+                                int s, int nranks);
+int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int H_total, int W,
+                    int row0, int rows, int C_I, int C_p, int r, double eps, int s, int sub_mode,
+                    void* nccl_comm, int rank, int nranks, void* workspace, size_t ws_bytes,
+                    void* cuda_stream);
+/* NCCL bootstrap for fgf_filter_band: rank 0 creates a 128-byte unique id, the caller
+ * distributes it (e.g. torch.distributed broadcast), every rank creates its communicator on
+ * its current device.  Return FGF_OK, FGF_ERR_NULL, FGF_ERR_PARAM or FGF_ERR_NCCL. */
+int fgf_nccl_unique_id(void* id_out);
+int fgf_nccl_comm_init(void** comm_out, const void* id, int rank, int nranks);
+int fgf_nccl_comm_destroy(void* comm);
+/* Test driver of the band path on ONE device: the nranks bands of a whole image [C][H][W]
+ * (batch 1) are filtered one after another with the halo rows copied between the bands'
+ * buffers (the same halo geometry fgf_filter_band sends over NCCL), and stitched into q.
+ * Band k owns low-res rows [k h / nranks, (k+1) h / nranks).  Workspace:
+ * fgf_bands_loopback_workspace_bytes(). */
+size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r, int s,
+                                          int nranks);
+int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, int W, int C_I,
+                              int C_p, int r, double eps, int s, int sub_mode, int nranks,
+                              void* workspace, size_t ws_bytes, void* cuda_stream);
+
 /* Detail enhancement, the application of PAPER.md Fig. 2 ("enhanced images with x5
  * detail"; SPEC S:303-311 enhance): out = (I - q) * gain + q, with q the SELF-guided fast
  * guided filter of I (p = I, C_p = C_I = C in {1, 3}) with these r, eps, s, sub_mode.  Since

@@ -40,7 +40,9 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_coefficients", "fgf_upsample_output", "fgf_last_launch_count", "fgf_status_str",
            "fgf_version", "fgf_profile_enable", "fgf_profile_read", "fgf_subsample",
            "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows",
-           "fgf_enhance_ws")
+           "fgf_enhance_ws", "fgf_band_workspace_bytes", "fgf_filter_band", "fgf_nccl_unique_id",
+           "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
+           "fgf_filter_bands_loopback")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -76,6 +78,20 @@ _lib.fgf_upsample_output_rows.argtypes = [_P, _P, _P] + [_i] * 11 + [_P]
 _lib.fgf_upsample_output_rows.restype = _i
 _lib.fgf_enhance_ws.argtypes = [_P, _P, _i, _i, _i, _i, _i, _d, _i, _i, _d, _P, _sz, _P]
 _lib.fgf_enhance_ws.restype = _i
+_lib.fgf_band_workspace_bytes.argtypes = [_i] * 9
+_lib.fgf_band_workspace_bytes.restype = _sz
+_lib.fgf_filter_band.argtypes = [_P, _P, _P] + [_i] * 7 + [_d, _i, _i, _P, _i, _i, _P, _sz, _P]
+_lib.fgf_filter_band.restype = _i
+_lib.fgf_nccl_unique_id.argtypes = [_P]
+_lib.fgf_nccl_unique_id.restype = _i
+_lib.fgf_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), _P, _i, _i]
+_lib.fgf_nccl_comm_init.restype = _i
+_lib.fgf_nccl_comm_destroy.argtypes = [_P]
+_lib.fgf_nccl_comm_destroy.restype = _i
+_lib.fgf_bands_loopback_workspace_bytes.argtypes = [_i] * 7
+_lib.fgf_bands_loopback_workspace_bytes.restype = _sz
+_lib.fgf_filter_bands_loopback.argtypes = [_P, _P, _P] + [_i] * 5 + [_d, _i, _i, _i, _P, _sz, _P]
+_lib.fgf_filter_bands_loopback.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -221,6 +237,52 @@ def fgf_enhance_ws(I, out, batch, H, W, C, r, eps, s, sub_mode, gain, workspace,
                              float(gain), _addr(workspace), ws_bytes, _stream(stream))
     if check:
         _check(rc, "fgf_enhance_ws")
+    return rc
+
+
+def fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks) -> int:
+    return _lib.fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks)
+
+
+def fgf_filter_band(I_band, p_band, q_band, H_total, W, row0, rows, C_I, C_p, r, eps, s,
+                    sub_mode, nccl_comm, rank, nranks, workspace, ws_bytes, stream=None,
+                    check=True):
+    rc = _lib.fgf_filter_band(_addr(I_band), _addr(p_band), _addr(q_band), H_total, W, row0, rows,
+                              C_I, C_p, r, float(eps), s, sub_mode, nccl_comm, rank, nranks,
+                              _addr(workspace), ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_band")
+    return rc
+
+
+def fgf_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fgf_nccl_unique_id(buf), "fgf_nccl_unique_id")
+    return buf.raw
+
+
+def fgf_nccl_comm_init(uid: bytes, rank: int, nranks: int) -> int:
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(_lib.fgf_nccl_comm_init(ctypes.byref(comm), buf, rank, nranks), "fgf_nccl_comm_init")
+    return comm.value
+
+
+def fgf_nccl_comm_destroy(comm) -> None:
+    _check(_lib.fgf_nccl_comm_destroy(comm), "fgf_nccl_comm_destroy")
+
+
+def fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks) -> int:
+    return _lib.fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks)
+
+
+def fgf_filter_bands_loopback(I, p, q, H, W, C_I, C_p, r, eps, s, sub_mode, nranks, workspace,
+                              ws_bytes, stream=None, check=True):
+    rc = _lib.fgf_filter_bands_loopback(_addr(I), _addr(p), _addr(q), H, W, C_I, C_p, r,
+                                        float(eps), s, sub_mode, nranks, _addr(workspace),
+                                        ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_bands_loopback")
     return rc
 
 

@@ -702,6 +702,8 @@ std::vector<HostPipe> g_host;
 }  // namespace
 }  // namespace fgf
 
+#include "fgf_band.cuh"
+
 using namespace fgf;
 
 extern "C" {
@@ -769,6 +771,172 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
     if (rc) return rc;
     if ((rc = check_pointers(I, p, q, P, true))) return rc;
     return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+}
+
+int fgf_nccl_unique_id(void* id_out) {
+    if (!id_out) return FGF_ERR_NULL;
+    const Nccl* n = nccl();
+    if (!n) return FGF_ERR_NCCL;
+    return n->getUniqueId(static_cast<ncclUniqueId*>(id_out)) == ncclSuccess ? FGF_OK : FGF_ERR_NCCL;
+}
+
+int fgf_nccl_comm_init(void** comm_out, const void* id, int rank, int nranks) {
+    if (!comm_out || !id) return FGF_ERR_NULL;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return FGF_ERR_PARAM;
+    const Nccl* n = nccl();
+    if (!n) return FGF_ERR_NCCL;
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    if (n->commInitRank(&c, nranks, uid, rank) != ncclSuccess) return FGF_ERR_NCCL;
+    *comm_out = c;
+    return FGF_OK;
+}
+
+int fgf_nccl_comm_destroy(void* comm) {
+    if (!comm) return FGF_ERR_NULL;
+    const Nccl* n = nccl();
+    if (!n) return FGF_ERR_NCCL;
+    return n->commDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? FGF_OK : FGF_ERR_NCCL;
+}
+
+size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
+                                int s, int nranks) {
+    BandPlan B;
+    if (band_plan(B, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false))
+        return 0;
+    return B.ws_total;
+}
+
+int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int H_total, int W,
+                    int row0, int rows, int C_I, int C_p, int r, double eps, int s, int sub_mode,
+                    void* nccl_comm, int rank, int nranks, void* workspace, size_t ws_bytes,
+                    void* cuda_stream) {
+    g_last_launches = 0;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return FGF_ERR_PARAM;
+    const bool self = I_band == p_band && C_I == 1 && C_p == 1;
+    BandPlan B;
+    int rc = band_plan(B, H_total, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self);
+    if (rc) return rc;
+    if (!I_band || !p_band || !q_band || !workspace) return FGF_ERR_NULL;
+    if (nranks > 1 && !nccl_comm) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I_band) | reinterpret_cast<uintptr_t>(p_band) |
+         reinterpret_cast<uintptr_t>(q_band)) & 3u)
+        return FGF_ERR_ALIGN;
+    const size_t own = (size_t)rows * W * 4;
+    if (overlaps(q_band, C_p * own, I_band, C_I * own) || overlaps(q_band, C_p * own, p_band, C_p * own))
+        return FGF_ERR_ALIAS;
+    if (!is_device_ptr(I_band) || !is_device_ptr(p_band) || !is_device_ptr(q_band) ||
+        !is_device_ptr(workspace))
+        return FGF_ERR_DEVICE;
+    if (ws_bytes < B.ws_total) return FGF_ERR_NOMEM;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    char* ws = static_cast<char*>(workspace);
+    if ((rc = band_prepare(B, I_band, p_band, ws, st))) return rc;
+    if (nranks > 1) {
+        const Nccl* n = nccl();
+        if (!n) return FGF_ERR_NCCL;
+        ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+        if (n->groupStart() != ncclSuccess) return FGF_ERR_NCCL;
+        ncclResult_t e = ncclSuccess;
+        for (int j = 0; j < B.NPL && e == ncclSuccess; ++j) {
+            const Halo hl = band_halo(B, ws, j, rank, nranks);
+            if (hl.n_up) {
+                e = n->send(hl.send_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
+                if (e == ncclSuccess) e = n->recv(hl.recv_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
+            }
+            if (hl.n_down && e == ncclSuccess) {
+                e = n->send(hl.send_down, hl.n_down, ncclFloat32, rank + 1, comm, st);
+                if (e == ncclSuccess) e = n->recv(hl.recv_down, hl.n_down, ncclFloat32, rank + 1, comm, st);
+            }
+        }
+        if (n->groupEnd() != ncclSuccess || e != ncclSuccess) return FGF_ERR_NCCL;
+    }
+    return band_finish(B, I_band, q_band, ws, st, self);
+}
+
+size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r, int s,
+                                          int nranks) {
+    if (nranks < 1 || s < 1 || H < 1 || W < 1) return 0;
+    const int h = lowres_dim(H, s);
+    size_t tot = 0;
+    for (int k = 0; k < nranks; ++k) {
+        const int y0 = (int)((long long)k * h / nranks), y1 = (int)((long long)(k + 1) * h / nranks);
+        const int row0 = y0 * s, rows = std::min(H, y1 * s) - row0;
+        BandPlan B;
+        if (band_plan(B, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false))
+            return 0;
+        tot += B.ws_total + 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
+    }
+    return tot;
+}
+
+int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, int W, int C_I,
+                              int C_p, int r, double eps, int s, int sub_mode, int nranks,
+                              void* workspace, size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    if (nranks < 1) return FGF_ERR_PARAM;
+    Plan P0;
+    int rc = make_plan(P0, 1, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if ((rc = check_pointers(I, p, q, P0, true))) return rc;
+    if (!workspace) return FGF_ERR_NULL;
+    if (ws_bytes < fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks))
+        return FGF_ERR_NOMEM;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const bool self = I == p && C_I == 1 && C_p == 1;
+    const int h = P0.h;
+    std::vector<BandPlan> Bs(nranks);
+    std::vector<char*> wss(nranks);
+    std::vector<float*> Ib(nranks), pb(nranks), qb(nranks);
+    char* cur = static_cast<char*>(workspace);
+    int launches = 0;
+    for (int k = 0; k < nranks; ++k) {
+        const int y0 = (int)((long long)k * h / nranks), y1 = (int)((long long)(k + 1) * h / nranks);
+        const int row0 = y0 * s, rows = std::min(H, y1 * s) - row0;
+        if ((rc = band_plan(Bs[k], H, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self)))
+            return rc;
+        wss[k] = cur;
+        cur += Bs[k].ws_total;
+        // the band's own rows, contiguous per plane, as a rank would hold them
+        Ib[k] = reinterpret_cast<float*>(cur);
+        pb[k] = self ? Ib[k] : Ib[k] + (size_t)C_I * rows * W;
+        qb[k] = Ib[k] + (size_t)(C_I + C_p) * rows * W;
+        cur += 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
+        for (int j = 0; j < C_I; ++j)
+            if (cudaMemcpyAsync(Ib[k] + (size_t)j * rows * W, I + ((size_t)j * H + row0) * W,
+                                (size_t)rows * W * 4, cudaMemcpyDeviceToDevice, st))
+                return FGF_ERR_CUDA;
+        if (!self)
+            for (int j = 0; j < C_p; ++j)
+                if (cudaMemcpyAsync(pb[k] + (size_t)j * rows * W, p + ((size_t)j * H + row0) * W,
+                                    (size_t)rows * W * 4, cudaMemcpyDeviceToDevice, st))
+                    return FGF_ERR_CUDA;
+        if ((rc = band_prepare(Bs[k], Ib[k], pb[k], wss[k], st))) return rc;
+        launches += g_last_launches;
+        g_last_launches = 0;
+    }
+    // the exchange, rank k <-> k+1, with the same halo geometry the NCCL path sends
+    for (int k = 0; k + 1 < nranks; ++k)
+        for (int j = 0; j < Bs[k].NPL; ++j) {
+            const Halo a = band_halo(Bs[k], wss[k], j, k, nranks);
+            const Halo b = band_halo(Bs[k + 1], wss[k + 1], j, k + 1, nranks);
+            if (a.n_down != b.n_up) return FGF_ERR_PARAM;   // both sides agree on the depth
+            if (cudaMemcpyAsync(a.recv_down, b.send_up, b.n_up * 4, cudaMemcpyDeviceToDevice, st) ||
+                cudaMemcpyAsync(b.recv_up, a.send_down, a.n_down * 4, cudaMemcpyDeviceToDevice, st))
+                return FGF_ERR_CUDA;
+        }
+    for (int k = 0; k < nranks; ++k) {
+        if ((rc = band_finish(Bs[k], Ib[k], qb[k], wss[k], st, self))) return rc;
+        launches += g_last_launches;
+        g_last_launches = 0;
+        for (int j = 0; j < C_p; ++j)
+            if (cudaMemcpyAsync(q + ((size_t)j * H + Bs[k].row0) * W, qb[k] + (size_t)j * Bs[k].rows * W,
+                                (size_t)Bs[k].rows * W * 4, cudaMemcpyDeviceToDevice, st))
+                return FGF_ERR_CUDA;
+    }
+    g_last_launches = launches;
+    return FGF_OK;
 }
 
 int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, int r,

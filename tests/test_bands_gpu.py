@@ -56,3 +56,80 @@ def test_upsample_rows_rejects_missing_maps():
     # rows [0, 64) of a 256-row image need low-res rows 0..16, the buffer holds only 0..3
     rc = fgf.fgf_upsample_output_rows(I, m, q, 1, 64, 64, 1, 1, 256, 64, 16, 0, 0, 4, check=False)
     assert rc == fgf.FGF_ERR_PARAM
+
+
+# ---------------------------------------------------------------- the C-ABI band path
+
+def _loopback(I, p, r, eps, s, sub, nranks):
+    _, C_I, H, W = I.shape
+    C_p = p.shape[1]
+    q = torch.empty((1, C_p, H, W), device="cuda")
+    nb = fgf.fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks)
+    assert nb > 0
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    fgf.fgf_filter_bands_loopback(I, p, q, H, W, C_I, C_p, r, eps, s, sub, nranks, ws, nb,
+                                  torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    return q
+
+
+@pytest.mark.parametrize("C_I,C_p,s,sub,nranks", [(1, 1, 4, 0, 1), (1, 1, 4, 0, 2), (1, 1, 4, 0, 8),
+                                                  (3, 1, 2, 1, 3), (1, 2, 1, 0, 4), (3, 3, 4, 0, 5)])
+def test_c_band_loopback_matches_whole_image(C_I, C_p, s, sub, nranks):
+    """fgf_filter_bands_loopback: the C band path (same plan, subsample, halo geometry and
+    finish as fgf_filter_band; halos copied between the bands' buffers) against the
+    whole-image filter and the oracle."""
+    g = torch.Generator(device="cuda").manual_seed(23 + nranks)
+    H, W, r, eps = 1200, 1032, 32, 0.01
+    I = torch.rand((1, C_I, H, W), device="cuda", generator=g)
+    p = torch.rand((1, C_p, H, W), device="cuda", generator=g)
+    q = _loopback(I, p, r, eps, s, sub, nranks)
+    q_whole = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    assert float((q - q_whole).abs().max()) < 1e-5
+    ref = oracle.fast_guided_filter(I.cpu().numpy(), p.cpu().numpy(), r, eps, s, sub)
+    assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 1e-4
+
+
+def test_c_band_loopback_self_guided_config4b_shape():
+    I, _ = synth.make_batch(0, "cuda", H=2048, W=512)
+    q = _loopback(I, I, 32, 0.01, 4, 0, 8)
+    ref = oracle.fast_guided_filter(I.cpu().numpy(), I.cpu().numpy(), 32, 0.01, 4, 0)
+    assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 1e-4
+
+
+def test_c_band_single_rank_with_nccl_communicator():
+    """fgf_filter_band through a real (one-rank) NCCL communicator: NCCL loads, the
+    communicator initialises, and the band equals the whole-image filter."""
+    uid = fgf.fgf_nccl_unique_id()
+    comm = fgf.fgf_nccl_comm_init(uid, 0, 1)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(5)
+        H, W = 640, 480
+        I = torch.rand((1, 1, H, W), device="cuda", generator=g)
+        p = torch.rand((1, 1, H, W), device="cuda", generator=g)
+        q = torch.empty_like(p)
+        nb = fgf.fgf_band_workspace_bytes(H, W, 0, H, 1, 1, 16, 4, 1)
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        fgf.fgf_filter_band(I, p, q, H, W, 0, H, 1, 1, 16, 0.01, 4, 0, comm, 0, 1, ws, nb,
+                            torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert float((q - fgf.filter(I, p, 16, 0.01, 4, 0)).abs().max()) < 1e-5
+    finally:
+        fgf.fgf_nccl_comm_destroy(comm)
+
+
+def test_c_band_errors():
+    I = torch.rand((1, 1, 64, 64), device="cuda")
+    q = torch.empty_like(I)
+    ws = torch.empty(1 << 22, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    # a band thinner than the 2r'+1-row halo, with several ranks
+    assert fgf.fgf_filter_band(I, I, q, 256, 64, 0, 64, 1, 1, 32, 0.01, 4, 0, None, 0, 4, ws,
+                               ws.numel(), st, check=False) == fgf.FGF_ERR_PARAM
+    # several ranks and no communicator
+    assert fgf.fgf_filter_band(I, I, q, 1024, 64, 0, 64, 1, 1, 4, 0.01, 4, 0, None, 0, 4, ws,
+                               ws.numel(), st, check=False) == fgf.FGF_ERR_NULL
+    # row0 not on the subsample grid
+    assert fgf.fgf_filter_band(I, I, q, 1024, 64, 2, 64, 1, 1, 4, 0.01, 4, 0, None, 0, 1, ws,
+                               ws.numel(), st, check=False) == fgf.FGF_ERR_PARAM
