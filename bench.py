@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dtype", choices=["f32", "f16", "bf16"], default="f32",
+                    help="element type of I, p, q (f16 / bf16: the reduced-precision I/O variant)")
     ap.add_argument("--band-impl", choices=["c", "torch"], default="c",
                     help="config 5 (4b): C-ABI band call with NCCL inside, or the Python stages")
     return ap.parse_args()
@@ -233,13 +235,26 @@ def main():
 
     # Inputs resident in HBM before timing; rank k owns global images [k*B, (k+1)*B).
     I, p = synth.make_batch(args.config, dev, batch=B, first=rank * B)
-    q = torch.empty((B, CP, H, W), dtype=torch.float32, device=dev)
-    ws_bytes = fgf.fgf_workspace_bytes(B, H, W, CI, CP, r, s)
+    # --dtype f16 / bf16: the reduced-precision I/O variant (fgf_filter_ex_ws; not the
+    # BASELINE.json configuration, which is fp32)
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[args.dtype]
+    code = {"f32": fgf.FGF_F32, "f16": fgf.FGF_F16, "bf16": fgf.FGF_BF16}[args.dtype]
+    esize = 4 if args.dtype == "f32" else 2
+    if args.dtype != "f32":
+        same = p is I
+        I = I.to(tdt).contiguous()
+        p = I if same else p.to(tdt).contiguous()
+    q = torch.empty((B, CP, H, W), dtype=tdt, device=dev)
+    ws_bytes = fgf.fgf_workspace_bytes_ex(B, H, W, CI, CP, r, s, code)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, ws_bytes, stream)
+        if args.dtype == "f32":
+            fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, ws_bytes, stream)
+        else:
+            fgf.fgf_filter_ex_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, code, ws, ws_bytes,
+                                 stream)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -294,7 +309,7 @@ def main():
     # x (read I: 4 C_I N + write q: 4 C_p N + read mean maps: 4 NC n)   (DESIGN.md Roofline).
     k4_ms, k4_n = prof["upsample_output"]
     imgs_per_launch = B / max(1, k4_n / args.steps)
-    k4_bytes = imgs_per_launch * (4 * CI * N + 4 * CP * N + 4 * NC * n)
+    k4_bytes = imgs_per_launch * (esize * CI * N + esize * CP * N + 4 * NC * n)
     k4_gbs = k4_bytes / (k4_ms / k4_n / 1e3) / 1e9 if k4_n else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "k4_traffic.json")
@@ -302,7 +317,7 @@ def main():
         try:
             tj = json.load(open(tpath))
             key = f"{c['name']}_s{s}"
-            if key in tj:
+            if key in tj and args.dtype == "f32":
                 traffic = tj[key]["dram_bytes_per_image"] * imgs_per_launch
         except Exception:
             traffic = None
@@ -311,9 +326,9 @@ def main():
                 "frac": k4_gbs / peak, "traffic": traffic,
                 "alg_bytes_per_launch": k4_bytes}
     # Whole filter against BASELINE's byte model (read I and p, write q, + low-res traffic).
-    B_model = B * (4 * N * (CI + 2 * CP) + 8 * n * NC)
+    B_model = B * (esize * N * (CI + 2 * CP) + 8 * n * NC)
     rho = 1.0 if (s == 1 or sub == 1) else 1.0 / min(s, 8)
-    B_alg = B * 4 * N * (CI + rho * CP + CP)
+    B_alg = B * esize * N * (CI + rho * CP + CP)
     whole = {"B_model_per_step": B_model, "B_alg_per_step": B_alg,
              "model_GBs": B_model / (ms_per_step / 1e3) / 1e9,
              "alg_GBs": B_alg / (ms_per_step / 1e3) / 1e9}
@@ -323,7 +338,7 @@ def main():
 
     # ---------------- e2e: host buffers through fgf_filter_host (H2D + filter + D2H inside).
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.dtype == "f32":   # fgf_filter_host takes fp32 buffers
         e2e = run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B)
 
     cpu = None
@@ -335,7 +350,7 @@ def main():
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": config_json(c, prm, B, world),
+                "config": dict(config_json(c, prm, B, world), io_dtype=args.dtype),
                 "gpu_launches": launches_per_step * args.steps,
                 "roofline": roofline, "hbm_whole_filter": whole, "kernels": kern,
                 "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

@@ -69,6 +69,13 @@ enum {
                                 not host memory (fgf_filter_host)                           */
 };
 
+/* Element type of I, p and q (fgf_filter_ex_ws); every operation is fp32 / fp64. */
+enum {
+    FGF_F32 = 0,          /* float                                                          */
+    FGF_F16 = 1,          /* IEEE binary16 (__half)                                          */
+    FGF_BF16 = 2          /* bfloat16 (__nv_bfloat16)                                        */
+};
+
 enum {
     FGF_SUB_NEAREST = 0,  /* R3: top-left sample of each s x s block          */
     FGF_SUB_BILINEAR = 1  /* R4: mean of the clipped s x s block              */
@@ -178,6 +185,17 @@ size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r,
 int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, int W, int C_I,
                               int C_p, int r, double eps, int s, int sub_mode, int nranks,
                               void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/* Reduced-precision I/O: fgf_filter_ws with I, p and q of element type
+ * dtype (FGF_F32 / FGF_F16 / FGF_BF16; all three buffers the same type, 2-byte alignment for
+ * the 16-bit types).  Only the storage changes: samples are widened to fp32 / fp64 on load
+ * exactly as in the fp32 path, and q is rounded to the element type once, on store.  16-bit
+ * types support C_I / C_p = 1 / 1, 3 / 1 and 3 / 3 (else FGF_ERR_UNSUPPORTED).  Workspace:
+ * fgf_workspace_bytes_ex().  Other errors as fgf_filter_ws; a bad dtype is FGF_ERR_PARAM. */
+size_t fgf_workspace_bytes_ex(int batch, int H, int W, int C_I, int C_p, int r, int s, int dtype);
+int fgf_filter_ex_ws(const void* I, const void* p, void* q, int batch, int H, int W, int C_I,
+                     int C_p, int r, double eps, int s, int sub_mode, int dtype, void* workspace,
+                     size_t ws_bytes, void* cuda_stream);
 
 /* Detail enhancement, the application of PAPER.md Fig. 2 ("enhanced images with x5
  * detail"; SPEC S:303-311 enhance): out = (I - q) * gain + q, with q the SELF-guided fast

@@ -32,6 +32,9 @@ FGF_ERR_NOMEM = 7
 FGF_ERR_NCCL = 8
 FGF_ERR_UNSUPPORTED = 9
 FGF_ERR_DEVICE = 10
+FGF_F32 = 0
+FGF_F16 = 1
+FGF_BF16 = 2
 FGF_SUB_NEAREST = 0
 FGF_SUB_BILINEAR = 1
 
@@ -42,7 +45,7 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows",
            "fgf_enhance_ws", "fgf_band_workspace_bytes", "fgf_filter_band", "fgf_nccl_unique_id",
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
-           "fgf_filter_bands_loopback")
+           "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -92,6 +95,10 @@ _lib.fgf_bands_loopback_workspace_bytes.argtypes = [_i] * 7
 _lib.fgf_bands_loopback_workspace_bytes.restype = _sz
 _lib.fgf_filter_bands_loopback.argtypes = [_P, _P, _P] + [_i] * 5 + [_d, _i, _i, _i, _P, _sz, _P]
 _lib.fgf_filter_bands_loopback.restype = _i
+_lib.fgf_workspace_bytes_ex.argtypes = [_i] * 8
+_lib.fgf_workspace_bytes_ex.restype = _sz
+_lib.fgf_filter_ex_ws.argtypes = [_P, _P, _P] + _GEOM + [_i, _P, _sz, _P]
+_lib.fgf_filter_ex_ws.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -240,6 +247,20 @@ def fgf_enhance_ws(I, out, batch, H, W, C, r, eps, s, sub_mode, gain, workspace,
     return rc
 
 
+def fgf_workspace_bytes_ex(batch, H, W, C_I, C_p, r, s, dtype) -> int:
+    return _lib.fgf_workspace_bytes_ex(batch, H, W, C_I, C_p, r, s, dtype)
+
+
+def fgf_filter_ex_ws(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, dtype, workspace,
+                     ws_bytes, stream=None, check=True):
+    rc = _lib.fgf_filter_ex_ws(_addr(I), _addr(p), _addr(q), batch, H, W, C_I, C_p, r,
+                               float(eps), s, sub_mode, dtype, _addr(workspace), ws_bytes,
+                               _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_ex_ws")
+    return rc
+
+
 def fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks) -> int:
     return _lib.fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks)
 
@@ -315,18 +336,25 @@ def filter(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None, w
     Enqueued on `stream` (default: torch's current stream); returns q."""
     import torch
     B, H, W, C_I, C_p = _geom(I, p)
+    codes = {torch.float32: FGF_F32, torch.float16: FGF_F16, torch.bfloat16: FGF_BF16}
     for t in (I, p):
-        if not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
-            raise ValueError("I and p must be contiguous float32 CUDA tensors")
+        if not t.is_cuda or t.dtype not in codes or not t.is_contiguous() or t.dtype != I.dtype:
+            raise ValueError("I and p must be contiguous CUDA tensors of one dtype "
+                             "(float32, float16 or bfloat16)")
+    dt = codes[I.dtype]
     if out is None:
-        out = torch.empty((B, C_p, H, W), dtype=torch.float32, device=I.device)
+        out = torch.empty((B, C_p, H, W), dtype=I.dtype, device=I.device)
     ws = workspace or Workspace()
-    nbytes = fgf_workspace_bytes(B, H, W, C_I, C_p, r, s)
+    nbytes = fgf_workspace_bytes_ex(B, H, W, C_I, C_p, r, s, dt)
     if nbytes == 0:
-        _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
+        _check(FGF_ERR_PARAM, "fgf_workspace_bytes_ex")
     buf = ws.get(nbytes, I.device)
     st = stream if stream is not None else torch.cuda.current_stream(I.device)
-    fgf_filter_ws(I, p, out, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, buf.numel(), st)
+    if dt == FGF_F32:
+        fgf_filter_ws(I, p, out, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, buf.numel(), st)
+    else:
+        fgf_filter_ex_ws(I, p, out, B, H, W, C_I, C_p, r, eps, s, sub_mode, dt, buf, buf.numel(),
+                         st)
     return out
 
 

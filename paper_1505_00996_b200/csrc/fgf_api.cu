@@ -81,6 +81,8 @@ struct Plan {
     int batch, H, W, CI, CP, r, s, sub;
     double eps;
     float k1 = 1.0f, k0 = 0.0f;   // mean-map fold (detail enhancement), identity by default
+    int dtype = FGF_F32;          // element type of I, p, q (FGF_F32 / FGF_F16 / FGF_BF16)
+    int esize = 4;                // its bytes
     int h, w, R, NC;
     size_t N, n;
     int chunk;
@@ -156,6 +158,26 @@ size_t plan_ws(const Plan& P, bool need_mean) {
     return P.ws_slot * P.nslots;
 }
 
+// Reduced-precision I/O: the strip engine reads fp32 planes, so at s = 1 a non-fp32 image is
+// first converted into the planes region (K0 with s = 1), which then always exists.
+int set_dtype(Plan& P, int dtype) {
+    if (dtype != FGF_F32 && dtype != FGF_F16 && dtype != FGF_BF16) return FGF_ERR_PARAM;
+    P.dtype = dtype;
+    P.esize = dtype == FGF_F32 ? 4 : 2;
+    if (dtype != FGF_F32 && P.ws_planes == 0) {
+        P.ws_planes = align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float));
+        P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
+    }
+    return FGF_OK;
+}
+
+const void* elem_off(const void* base, size_t elems, const Plan& P) {
+    return static_cast<const char*>(base) + elems * P.esize;
+}
+void* elem_off(void* base, size_t elems, const Plan& P) {
+    return static_cast<char*>(base) + elems * P.esize;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
     auto x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
     return x < y + nb && y < x + na;
@@ -170,12 +192,13 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-int check_pointers(const float* I, const float* p, const float* q, const Plan& P, bool device) {
+int check_pointers(const void* I, const void* p, const void* q, const Plan& P, bool device) {
     if (!I || !p || !q) return FGF_ERR_NULL;
     if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(p) |
-         reinterpret_cast<uintptr_t>(q)) & 3u)
+         reinterpret_cast<uintptr_t>(q)) & (uintptr_t)(P.esize - 1))
         return FGF_ERR_ALIGN;
-    const size_t bI = (size_t)P.batch * P.CI * P.N * 4, bp = (size_t)P.batch * P.CP * P.N * 4;
+    const size_t bI = (size_t)P.batch * P.CI * P.N * P.esize;
+    const size_t bp = (size_t)P.batch * P.CP * P.N * P.esize;
     if (overlaps(q, bp, I, bI) || overlaps(q, bp, p, bp)) return FGF_ERR_ALIAS;
     if (device) {
         if (!is_device_ptr(I) || !is_device_ptr(p) || !is_device_ptr(q)) return FGF_ERR_DEVICE;
@@ -195,20 +218,30 @@ void set_smem(K kernel, size_t bytes) {
 
 int last_error() { return cudaGetLastError() == cudaSuccess ? FGF_OK : FGF_ERR_CUDA; }
 
-// K0: step 1 into compact low-res planes.
-int launch_subsample(const float* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
+// K0: step 1 into compact fp32 low-res planes (s = 1 nearest: a conversion to fp32).
+template <typename E>
+int launch_subsample_e(const void* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
     SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s, 8};
     dim3 grid((P.w + 255) / 256, (P.h + sp.rows_per_cta - 1) / sp.rows_per_cta, planes);
     ProfScope ps(KIND_SUB, st);
-    const bool vec4 = P.s == 4 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (P.W % 4) == 0;
+    const bool vec4 = P.s == 4 && (reinterpret_cast<uintptr_t>(src) & (4 * sizeof(E) - 1)) == 0 &&
+                      (P.W % 4) == 0;
     if (P.sub == FGF_SUB_NEAREST)
-        subsample_nearest_kernel<8><<<grid, 256, 0, st>>>(sp);
+        subsample_nearest_kernel<8, E><<<grid, 256, 0, st>>>(sp);
     else if (vec4)
-        subsample_block_kernel<true><<<grid, 256, 0, st>>>(sp);
+        subsample_block_kernel<true, E><<<grid, 256, 0, st>>>(sp);
     else
-        subsample_block_kernel<false><<<grid, 256, 0, st>>>(sp);
+        subsample_block_kernel<false, E><<<grid, 256, 0, st>>>(sp);
     ++g_last_launches;
     return last_error();
+}
+
+int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
+    switch (P.dtype) {
+        case FGF_F16: return launch_subsample_e<__half>(src, dst, planes, P, st);
+        case FGF_BF16: return launch_subsample_e<__nv_bfloat16>(src, dst, planes, P, st);
+    }
+    return launch_subsample_e<float>(src, dst, planes, P, st);
 }
 
 template <int MODE, int CI, int CP, int NT>
@@ -274,9 +307,8 @@ int lowres_span(int T, int n_dst, int n_src) {
 }
 
 constexpr size_t kOutSmemBudget = 44 * 1024;
-int g_num_sms = 0;
 
-template <int CI, int CP, int PX>
+template <int CI, int CP, int PX, typename E = float>
 int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream_t st) {
     constexpr int NC = (CI + 1) * CP;
     OutParams op = op0;
@@ -297,57 +329,26 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         // can be co-resident (experiment knob)
         if (const char* e = getenv("FGF_K4_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
     }
-    if (!s1 && getenv("FGF_PERSIST") != nullptr) {
-        // persistent walker: ~2 CTAs per SM, bands of 64 rows, double-buffered staging
-        using PC = PersistCfg<CI, CP, PX>;
-        PersistParams pp{op, images, (P.W + 256 * PX - 1) / (256 * PX), 1, 0, 0};
-        pp.o.TR = 64;
-        pp.ncl = lowres_span(256 * PX, P.W, P.w);
-        pp.nrl = lowres_span(pp.o.TR, op.Hg, op.hg);
-        size_t psm = 2 * (size_t)pp.nrl * NC * pp.ncl * sizeof(float);
-        while (psm > 150 * 1024 && pp.o.TR > 8) {
-            pp.o.TR /= 2;
-            pp.nrl = lowres_span(pp.o.TR, op.Hg, op.hg);
-            psm = 2 * (size_t)pp.nrl * NC * pp.ncl * sizeof(float);
-        }
-        if (psm <= 200 * 1024) {
-            if (g_num_sms == 0) {
-                int dev = 0;
-                cudaGetDevice(&dev);
-                cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-                if (g_num_sms <= 0) g_num_sms = 148;
-            }
-            auto kern = output_persist_kernel<CI, CP, PX>;
-            set_smem(kern, psm);
-            int occ = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, psm);
-            occ = std::max(1, occ);
-            const long long items = (long long)images * ((P.H + pp.o.TR - 1) / pp.o.TR);
-            pp.cpb = (int)std::max<long long>(1, std::min<long long>(items, (long long)g_num_sms * occ / pp.ncb));
-            ProfScope ps(KIND_OUT, st);
-            kern<<<pp.ncb * pp.cpb, 256, psm, st>>>(pp);
-            ++g_last_launches;
-            return last_error();
-        }
-    }
     dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
-    if (!s1 && getenv("FGF_NO_ASYNC") == nullptr) {
-        // cp.async ring variant: prefetch held in shared memory, not registers
-        const size_t asm_ = smem + AsyncCfg<CI, CP, PX>::RING_BYTES;
-        if (asm_ <= 200 * 1024) {
-            auto kern = output_async_kernel<CI, CP, PX>;
-            set_smem(kern, asm_);
-            ProfScope ps(KIND_OUT, st);
-            kern<<<grid, 256, asm_, st>>>(op);
-            ++g_last_launches;
-            return last_error();
+    if constexpr (PX * sizeof(E) >= 4) {   // cp.async moves 4, 8 or 16 bytes
+        if (!s1 && getenv("FGF_NO_ASYNC") == nullptr) {
+            // cp.async ring variant: prefetch held in shared memory, not registers
+            const size_t asm_ = smem + AsyncCfg<CI, CP, PX, E>::RING_BYTES;
+            if (asm_ <= 200 * 1024) {
+                auto kern = output_async_kernel<CI, CP, PX, E>;
+                set_smem(kern, asm_);
+                ProfScope ps(KIND_OUT, st);
+                kern<<<grid, 256, asm_, st>>>(op);
+                ++g_last_launches;
+                return last_error();
+            }
         }
     }
     ProfScope ps(KIND_OUT, st);
     if (s1) {
-        output_kernel<CI, CP, PX, true><<<grid, 256, 0, st>>>(op);
+        output_kernel<CI, CP, PX, true, 0, 0, 0, E><<<grid, 256, 0, st>>>(op);
     } else {
-        auto kern = output_kernel<CI, CP, PX, false>;
+        auto kern = output_kernel<CI, CP, PX, false, 0, 0, 0, E>;
         set_smem(kern, smem);
         kern<<<grid, 256, smem, st>>>(op);
     }
@@ -356,16 +357,17 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
 }
 
 // Pixels per thread: as wide as alignment allows while the coefficient registers fit.
-template <int CI, int CP>
+template <int CI, int CP, typename E = float>
 int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
     constexpr int NC = (CI + 1) * CP;
-    const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q) |
-                         reinterpret_cast<uintptr_t>(op.M);
-    if (NC <= 2 && P.W % 4 == 0 && (al & 15u) == 0)
-        return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1)>(op, images, P, st);
-    if (NC <= 4 && P.W % 2 == 0 && (al & 7u) == 0)
-        return launch_output_px<CI, CP, (NC <= 4 ? 2 : 1)>(op, images, P, st);
-    return launch_output_px<CI, CP, 1>(op, images, P, st);
+    constexpr uintptr_t ES = sizeof(E);
+    const uintptr_t ai = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
+    const uintptr_t am = reinterpret_cast<uintptr_t>(op.M);
+    if (NC <= 2 && P.W % 4 == 0 && (ai & (4 * ES - 1)) == 0 && (am & 15u) == 0)
+        return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1), E>(op, images, P, st);
+    if (NC <= 4 && P.W % 2 == 0 && (ai & (2 * ES - 1)) == 0 && (am & 7u) == 0)
+        return launch_output_px<CI, CP, (NC <= 4 ? 2 : 1), E>(op, images, P, st);
+    return launch_output_px<CI, CP, 1, E>(op, images, P, st);
 }
 
 // Row band of a taller image: I/q hold rows [Yoff, Yoff + P.H) of an image of height Hg;
@@ -374,10 +376,24 @@ struct Band {
     int Hg, hg, Yoff, yoff, hm;
 };
 
-int launch_output(const float* I, const float* M, float* q, int images, const Plan& P,
+int launch_output(const void* I, const float* M, void* q, int images, const Plan& P,
                   cudaStream_t st, const Band* band = nullptr) {
     const Band b = band ? *band : Band{P.H, P.h, 0, 0, P.h};
     OutParams op{I, M, q, P.H, P.W, b.hm, P.w, b.Hg, b.hg, b.Yoff, b.yoff, P.TR};
+    if (P.dtype != FGF_F32) {
+        // reduced-precision I/O: gray -> gray, colour -> colour, colour guide -> one channel
+        const int key = P.CI * 10 + P.CP;
+        if (P.dtype == FGF_F16) {
+            if (key == 11) return launch_output_t<1, 1, __half>(op, images, P, st);
+            if (key == 31) return launch_output_t<3, 1, __half>(op, images, P, st);
+            if (key == 33) return launch_output_t<3, 3, __half>(op, images, P, st);
+        } else {
+            if (key == 11) return launch_output_t<1, 1, __nv_bfloat16>(op, images, P, st);
+            if (key == 31) return launch_output_t<3, 1, __nv_bfloat16>(op, images, P, st);
+            if (key == 33) return launch_output_t<3, 3, __nv_bfloat16>(op, images, P, st);
+        }
+        return FGF_ERR_UNSUPPORTED;
+    }
     switch (P.CI * 10 + P.CP) {
         case 11: return launch_output_t<1, 1>(op, images, P, st);
         case 12: return launch_output_t<1, 2>(op, images, P, st);
@@ -466,10 +482,11 @@ bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     return false;
 }
 
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1>
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
+          typename E = float>
 int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
                          cudaStream_t st) {
-    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB>;
+    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, E>;
     size_t smem = g.smem;
     // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
     // previous chunk can be co-resident (overlap experiment knob)
@@ -492,6 +509,16 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
     lp.TW = g.TW;
     lp.TH = g.TH;
     if (CP > 1) return launch_lowres_gray_g<CP, 4, 9, 9>(lp, g, images, P, st);
+    if (P.dtype != FGF_F32) {   // reduced-precision inputs: the default variant and the wide one
+        const bool h = P.dtype == FGF_F16;
+        if (g.V == 3)
+            return h ? launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, __half>(lp, g, images, P, st)
+                     : launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, __nv_bfloat16>(lp, g, images, P, st);
+        if (g.V == 0)
+            return h ? launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __half>(lp, g, images, P, st)
+                     : launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __nv_bfloat16>(lp, g, images, P, st);
+        return FGF_ERR_UNSUPPORTED;
+    }
     switch (g.V) {
         case 0: return launch_lowres_gray_g<1, 4, 9, 9>(lp, g, images, P, st);
         case 1: return launch_lowres_gray_g<1, 8, 9, 9>(lp, g, images, P, st);
@@ -514,21 +541,33 @@ int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaSt
     if (const char* e = getenv("FGF_LOWRES")) {
         if (strcmp(e, "strip") == 0) return FGF_ERR_UNSUPPORTED;
     }
+    if (P.dtype != FGF_F32 && P.CP != 1) return FGF_ERR_UNSUPPORTED;
     switch (P.CP) {
-        case 1: return launch_lowres_gray_t<1>(lp, images, P, st, dry);
+        case 1: {
+            if (P.dtype != FGF_F32 && dry) {
+                // only variants 3 and 0 exist for reduced-precision inputs
+                LrGeom g;
+                if (!lowres_geom<1>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
+                return (g.V == 3 || g.V == 0) ? FGF_OK : FGF_ERR_UNSUPPORTED;
+            }
+            return launch_lowres_gray_t<1>(lp, images, P, st, dry);
+        }
         case 2: return launch_lowres_gray_t<2>(lp, images, P, st, dry);
     }
     return FGF_ERR_UNSUPPORTED;
 }
 
 // Steps 1-5 for images [b0, b0+nb): writes the mean maps into `mean`.
-int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, const Plan& P,
+int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const Plan& P,
                char* slot, cudaStream_t st) {
     const bool p_is_I = (I == p) && P.CI == 1 && P.CP == 1;
-    const float* Ib = I + (size_t)b0 * P.CI * P.N;
-    const float* pb = p + (size_t)b0 * P.CP * P.N;
+    const void* Ib = elem_off(I, (size_t)b0 * P.CI * P.N, P);
+    const void* pb = elem_off(p, (size_t)b0 * P.CP * P.N, P);
     float* planes = reinterpret_cast<float*>(slot);
     float* coef = reinterpret_cast<float*>(slot + P.ws_planes);
+    Plan Pf = P;                   // the compact planes K0 writes are fp32
+    Pf.dtype = FGF_F32;
+    Pf.esize = 4;
     int rc;
 
     // Gray guidance: the fused K13 (steps 1-5 in one kernel; nearest samples read in place).
@@ -546,18 +585,19 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
             lp.srcI = Is; lp.imgI = (long long)P.n;
             lp.srcP = ps; lp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; lp.planeP = (int)P.n;
             lp.row = P.w; lp.col = 1;
-        } else {
-            // nearest (R3): sample (y, x) = I[y s][x s]; s = 1: the image itself
-            lp.srcI = Ib; lp.imgI = (long long)P.N;
-            lp.srcP = pb; lp.imgP = (long long)P.CP * P.N; lp.planeP = (int)P.N;
-            lp.row = P.s * P.W; lp.col = P.s;
+            return launch_lowres_gray(lp, nb, Pf, st);
         }
+        // nearest (R3): sample (y, x) = I[y s][x s]; s = 1: the image itself
+        lp.srcI = Ib; lp.imgI = (long long)P.N;
+        lp.srcP = pb; lp.imgP = (long long)P.CP * P.N; lp.planeP = (int)P.N;
+        lp.row = P.s * P.W; lp.col = P.s;
         return launch_lowres_gray(lp, nb, P, st);
     }
 
     StripParams sp{};
-    if (P.s > 1) {
-        // Step 1 as its own pass (R3 nearest / R4 block mean) into compact low-res planes.
+    if (P.s > 1 || P.dtype != FGF_F32) {
+        // Step 1 as its own pass (R3 nearest / R4 block mean) into compact fp32 low-res planes
+        // (s = 1 with reduced-precision inputs: the conversion to fp32).
         float* Is = planes;
         float* ps = planes + (size_t)nb * P.CI * P.n;
         if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
@@ -568,8 +608,8 @@ int run_lowres(const float* I, const float* p, float* mean, int b0, int nb, cons
         sp.row = P.w; sp.col = 1;
     } else {
         // s = 1: I' = I, p' = p; K1 reads the images directly.
-        sp.srcI = Ib; sp.imgI = (long long)P.CI * P.N; sp.planeI = (int)P.N;
-        sp.srcP = pb; sp.imgP = (long long)P.CP * P.N; sp.planeP = (int)P.N;
+        sp.srcI = static_cast<const float*>(Ib); sp.imgI = (long long)P.CI * P.N; sp.planeI = (int)P.N;
+        sp.srcP = static_cast<const float*>(pb); sp.imgP = (long long)P.CP * P.N; sp.planeP = (int)P.N;
         sp.row = P.W; sp.col = 1;
     }
     sp.h = P.h; sp.w = P.w; sp.R = P.R; sp.eps = P.eps;
@@ -627,7 +667,7 @@ int get_pipe(Pipe*& out) {
 // stream while the output pass K4 of chunk j-1 streams the full-resolution images on the
 // caller's stream; the two workspace slots alternate.  The caller's stream is joined
 // before return (it waits on the last low-res event, and all K4s are on it).
-int run_all(const float* I, const float* p, float* q, const Plan& P, void* ws, size_t ws_bytes,
+int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size_t ws_bytes,
             cudaStream_t st) {
     if (!ws) return FGF_ERR_NULL;
     if (ws_bytes < plan_ws(P, true)) return FGF_ERR_NOMEM;
@@ -656,8 +696,8 @@ int run_all(const float* I, const float* p, float* q, const Plan& P, void* ws, s
         if ((rc = run_lowres(I, p, mean, b0, nb, P, slot, pp->low))) return rc;
         if (cudaEventRecord(pp->done_low[k], pp->low) || cudaStreamWaitEvent(st, pp->done_low[k], 0))
             return FGF_ERR_CUDA;
-        if ((rc = launch_output(I + (size_t)b0 * P.CI * P.N, mean, q + (size_t)b0 * P.CP * P.N,
-                                nb, P, st)))
+        if ((rc = launch_output(elem_off(I, (size_t)b0 * P.CI * P.N, P), mean,
+                                elem_off(q, (size_t)b0 * P.CP * P.N, P), nb, P, st)))
             return rc;
         if (cudaEventRecord(pp->done_out[k], st)) return FGF_ERR_CUDA;
     }
@@ -665,7 +705,7 @@ int run_all(const float* I, const float* p, float* q, const Plan& P, void* ws, s
 }
 
 // Steps 1-5 into a caller buffer (fgf_coefficients), on the caller's stream.
-int run_coefficients(const float* I, const float* p, float* mean_out, const Plan& P, void* ws,
+int run_coefficients(const void* I, const void* p, float* mean_out, const Plan& P, void* ws,
                      size_t ws_bytes, cudaStream_t st) {
     if (!ws) return FGF_ERR_NULL;
     if (ws_bytes < plan_ws(P, false)) return FGF_ERR_NOMEM;
@@ -760,6 +800,28 @@ size_t fgf_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int
     if (make_plan(P0, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
     if (make_plan(P1, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_BILINEAR)) return 0;
     return std::max(plan_ws(P0, true), plan_ws(P1, true));
+}
+
+size_t fgf_workspace_bytes_ex(int batch, int H, int W, int C_I, int C_p, int r, int s, int dtype) {
+    Plan P0, P1;
+    if (make_plan(P0, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
+    if (make_plan(P1, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_BILINEAR)) return 0;
+    if (set_dtype(P0, dtype) || set_dtype(P1, dtype)) return 0;
+    return std::max(plan_ws(P0, true), plan_ws(P1, true));
+}
+
+int fgf_filter_ex_ws(const void* I, const void* p, void* q, int batch, int H, int W, int C_I,
+                     int C_p, int r, double eps, int s, int sub_mode, int dtype, void* workspace,
+                     size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    Plan P;
+    int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if ((rc = set_dtype(P, dtype))) return rc;
+    if (dtype != FGF_F32 && !(C_I * 10 + C_p == 11 || C_I * 10 + C_p == 31 || C_I * 10 + C_p == 33))
+        return FGF_ERR_UNSUPPORTED;
+    if ((rc = check_pointers(I, p, q, P, true))) return rc;
+    return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,

@@ -37,8 +37,8 @@ namespace fgf {
 struct LowresParams {
     // Sample (y, x) of image b: srcI[b*imgI + y*row + x*col]; p channel c at
     // srcP[b*imgP + c*planeP + y*row + x*col].  In-image offsets fit in 32 bits (validated).
-    const float* srcI;
-    const float* srcP;
+    const void* srcI;      // element type E of the kernel (float, __half, __nv_bfloat16)
+    const void* srcP;
     long long imgI, imgP;
     int planeP;
     int row, col;
@@ -106,7 +106,8 @@ __device__ __forceinline__ double inv_count(int i, int n, int R) {
 //   Y (run threads):     stage-A horizontal phase + epilogue of those a, b rows on threads
 //                        [0, TA), and concurrently the stage-B horizontal phase of the outputs
 //                        on threads [TA, TA + TB); then the staged outputs are stored.
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1>
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
+          typename E = float>
 __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P) {
     using C = LowresCfg<CP, G, KA, KB, RING>;
     constexpr int NIN = C::NIN, NMAP = C::NMAP, NAB = C::NAB;
@@ -147,15 +148,16 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     const bool colS = tid < L.NCS;                // owns a statistics column (maybe outside)
     const bool colA = colS && cs >= 0 && cs < w;  // ... inside the image
     const int offc = (colA ? cs : 0) * P.col;
-    const float* bI = P.srcI + img * P.imgI + offc;
-    const float* bP = P.srcP + img * P.imgP + offc;
+    const E* bI = static_cast<const E*>(P.srcI) + img * P.imgI + offc;
+    const E* bP = static_cast<const E*>(P.srcP) + img * P.imgP + offc;
     const int row = P.row, planeP = P.planeP;
     const long long dP = bP - bI;
+    auto ld = [](const E* q) { return ElemT<E>::load(q); };
     auto load = [&](int y, float* v) {
-        const float* pi = bI + (long long)y * row;
-        v[0] = __ldg(pi);
+        const E* pi = bI + (long long)y * row;
+        v[0] = ld(pi);
 #pragma unroll
-        for (int c = 0; c < CP; ++c) v[1 + c] = __ldg(pi + dP + c * planeP);
+        for (int c = 0; c < CP; ++c) v[1 + c] = ld(pi + dP + c * planeP);
     };
     // add (sub = false) or remove one sample row: [I, II, p_c, Ip_c], exact products in fp64
     auto accum = [&](double* acc, const float* v, bool sub) {
@@ -200,22 +202,22 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     auto load_batch = [&](int ya) {
         if (!colA) return;
         const int ng = min(yA1 - ya, h - (ya + R));   // add rows that exist
-        const float* pi = bI + (long long)(ya + R) * row;
+        const E* pi = bI + (long long)(ya + R) * row;
         if (ng >= G) {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-                nv[g][0] = __ldg(pi);
+                nv[g][0] = ld(pi);
 #pragma unroll
-                for (int c = 0; c < CP; ++c) nv[g][1 + c] = __ldg(pi + dP + c * planeP);
+                for (int c = 0; c < CP; ++c) nv[g][1 + c] = ld(pi + dP + c * planeP);
                 pi += row;
             }
         } else {
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 if (g < ng) {
-                    nv[g][0] = __ldg(pi);
+                    nv[g][0] = ld(pi);
 #pragma unroll
-                    for (int c = 0; c < CP; ++c) nv[g][1 + c] = __ldg(pi + dP + c * planeP);
+                    for (int c = 0; c < CP; ++c) nv[g][1 + c] = ld(pi + dP + c * planeP);
                 }
                 pi += row;
             }
@@ -223,22 +225,22 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         if (!RING) {
             const int g0 = max(0, R + 1 - ya);             // subtract rows ya + g - R - 1 >= 0
             const int g1 = min(G, yA1 - ya);
-            const float* ps = bI + (long long)(ya - R - 1) * row;
+            const E* ps = bI + (long long)(ya - R - 1) * row;
             if (g0 == 0 && g1 == G) {
 #pragma unroll
                 for (int g = 0; g < (RING ? 1 : G); ++g) {
-                    sv[g][0] = __ldg(ps);
+                    sv[g][0] = ld(ps);
 #pragma unroll
-                    for (int c = 0; c < CP; ++c) sv[g][1 + c] = __ldg(ps + dP + c * planeP);
+                    for (int c = 0; c < CP; ++c) sv[g][1 + c] = ld(ps + dP + c * planeP);
                     ps += row;
                 }
             } else {
 #pragma unroll
                 for (int g = 0; g < (RING ? 1 : G); ++g) {
                     if (g >= g0 && g < g1) {
-                        sv[g][0] = __ldg(ps);
+                        sv[g][0] = ld(ps);
 #pragma unroll
-                        for (int c = 0; c < CP; ++c) sv[g][1 + c] = __ldg(ps + dP + c * planeP);
+                        for (int c = 0; c < CP; ++c) sv[g][1 + c] = ld(ps + dP + c * planeP);
                     }
                     ps += row;
                 }

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include "../paper_1505_00996_b200/csrc/fgf_kernels.cuh"
+#include "k4_variants.cuh"
 using namespace fgf;
 
 template <int UNROLL, bool CS>
