@@ -416,6 +416,7 @@ constexpr size_t kLrSmemMax = 227 * 1024;
 //   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
 // (measured on config 4, profiles/round1/k13_variants.txt: G 8 / K 17 and G 6 / K 13 without
 // the ring, and a lane-pair split of the runs, were slower)
+// (also slower: K 5/17 and K 7/17, rebalancing the two concurrent horizontal phases)
 constexpr int kLrNumVariants = 4;
 
 // Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.

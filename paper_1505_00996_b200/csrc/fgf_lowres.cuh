@@ -263,9 +263,23 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     // outside the image keep the zeros written at the start.
     auto column_A = [&](int ya0, int nA) {
         if (!colA) return;
-        int s = sAdd;
         double* vcol = VsA + tid;
-        const bool full = nA == G && ya0 - R - 1 >= 0 && ya0 + G - 1 + R < h;
+        if (!RING && nA == G && ya0 - R - 1 >= 0 && ya0 + G - 1 + R < h) {
+            // interior batch: every add and subtract row exists -- straight-line code
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                step(nv[g], sv[RING ? 0 : g], true, true);
+                double* v = vcol + g * NMAP * VPA;
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m) {
+                    *v = accA[m];
+                    v += VPA;
+                }
+            }
+            return;
+        }
+        int s = sAdd;
+        const bool full = false;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             if (full || g < nA) {
@@ -428,11 +442,29 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                 const float* ps = slotp(max(yb - R - 1, 0));
                 float* vcol = VsB + tid;
                 const bool full = nB == G && yb - R - 1 >= 0 && yb + G - 1 + R < h;
+                if (full) {
+                    // interior batch: straight-line code, ring wrap tested once per row
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) accB[m] += pa[m * PA] - ps[m * PA];
+                        float* v = vcol + g * NAB * VPB;
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) {
+                            *v = accB[m];
+                            v += VPB;
+                        }
+                        pa += rstep;
+                        pa = pa >= ring_end ? pa - rlen : pa;
+                        ps += rstep;
+                        ps = ps >= ring_end ? ps - rlen : ps;
+                    }
+                }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    if (full || g < nB) {
+                    if (!full && g < nB) {
                         const int y = yb + g;
-                        const bool hasA = full || y + R < h, hasS = full || y - R - 1 >= 0;
+                        const bool hasA = y + R < h, hasS = y - R - 1 >= 0;
 #pragma unroll
                         for (int m = 0; m < NAB; ++m)
                             accB[m] += (hasA ? pa[m * PA] : 0.0f) - (hasS ? ps[m * PA] : 0.0f);
