@@ -467,10 +467,11 @@ bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
         if (NT < 64) break;
     }
     if (best.NT == 0) return false;
-    // Segment height: long segments amortise the r' warm-up rows; keep >= ~8 waves.
+    // Segment height: long segments amortise the 2r'+1 warm-up rows (up to 256 rows); small
+    // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
     const long long cols = (long long)best.strips * images;
-    long long th = ((long long)h * cols + 8 * 3 * 148 - 1) / (8 * 3 * 148);
-    th = std::max<long long>(th, 256);
+    long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
+    th = std::min<long long>(256, std::max<long long>(th, std::max(16, 2 * R + 2)));
     if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
     if (const char* e = getenv("FGF_LR_V")) {
