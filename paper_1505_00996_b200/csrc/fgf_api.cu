@@ -114,6 +114,8 @@ int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double ep
     return FGF_OK;
 }
 
+void trim_ws(Plan& P);   // after the K13 dispatch (below)
+
 int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
               int sub) {
     int rc = check_shape_params(batch, H, W, CI, CP, r, eps, s, sub);
@@ -149,13 +151,14 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
     P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
     P.nslots = batch > P.chunk ? 2 : 1;
+    trim_ws(P);
     return FGF_OK;
 }
 
 // need_mean: false when the caller provides the mean maps buffer (fgf_coefficients).
 size_t plan_ws(const Plan& P, bool need_mean) {
-    if (!need_mean) return P.ws_planes + P.ws_coef;
-    return P.ws_slot * P.nslots;
+    if (!need_mean) return std::max<size_t>(kAlign, P.ws_planes + P.ws_coef);
+    return std::max<size_t>(kAlign, P.ws_slot * P.nslots);
 }
 
 // Reduced-precision I/O: the strip engine reads fp32 planes, so at s = 1 a non-fp32 image is
@@ -168,6 +171,7 @@ int set_dtype(Plan& P, int dtype) {
         P.ws_planes = align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float));
         P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
     }
+    trim_ws(P);
     return FGF_OK;
 }
 
@@ -557,6 +561,22 @@ int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaSt
         case 2: return launch_lowres_gray_t<2>(lp, images, P, st, dry);
     }
     return FGF_ERR_UNSUPPORTED;
+}
+
+// When K13 serves a plan it needs no a, b maps, and no compact planes unless it subsamples by
+// block means: shrink the workspace (and so let a chunk hold more images).
+void trim_ws(Plan& P) {
+    if (P.s < 1 || launch_lowres_gray(LowresParams{}, P.chunk, P, nullptr, true) != FGF_OK) return;
+    const bool planes = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
+    const size_t per_img = (size_t)((planes ? P.CI + P.CP : 0) + P.NC) * P.n * sizeof(float);
+    size_t target = kChunkTargetBytes;
+    if (const char* e = getenv("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
+    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(P.batch, target / std::max<size_t>(per_img, 1)));
+    P.ws_planes = planes ? align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float)) : 0;
+    P.ws_coef = 0;
+    P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
+    P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
+    P.nslots = P.batch > P.chunk ? 2 : 1;
 }
 
 // Steps 1-5 for images [b0, b0+nb): writes the mean maps into `mean`.
@@ -1106,9 +1126,12 @@ int fgf_subsample(const float* src, float* dst, int planes, int H, int W, int s,
 }
 
 size_t fgf_lowres_workspace_bytes(int batch, int h, int w, int C_I, int C_p) {
+    // radius-independent: enough for either low-res engine (K13 or the strip engine)
     Plan P;
     if (make_plan(P, batch, h, w, C_I, C_p, 1, 1.0, 1, FGF_SUB_NEAREST)) return 0;
-    return plan_ws(P, false);
+    const size_t chunk = (size_t)std::max(1, std::min(batch, (int)std::max<size_t>(
+        1, kChunkTargetBytes / std::max<size_t>(1, (size_t)2 * P.NC * P.n * sizeof(float)))));
+    return std::max<size_t>(kAlign, align_up(chunk * P.NC * P.n * sizeof(float)));
 }
 
 int fgf_lowres_mean(const float* Is, const float* ps, float* mean_ab, int batch, int h, int w,
