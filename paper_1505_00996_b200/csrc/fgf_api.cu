@@ -327,6 +327,9 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
             const size_t b = (size_t)lowres_span(tr, op.Hg, op.hg) * NC * ncl * sizeof(float);
             if (b <= kOutSmemBudget) { op.TR = tr; break; }
         }
+        // small launches (single images): shorter bands until ~2 waves of 4 CTAs per SM exist
+        const long long ncb = (P.W + 256 * PX - 1) / (256 * PX);
+        while (op.TR > 8 && ncb * ((P.H + op.TR - 1) / op.TR) * images < 2LL * 4 * 148) op.TR /= 2;
         smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
         // optional floor on the dynamic smem: caps K4 CTAs/SM so the low-res stream's CTAs
@@ -475,7 +478,7 @@ bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
     const long long cols = (long long)best.strips * images;
     long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
-    th = std::min<long long>(256, std::max<long long>(th, std::max(16, 2 * R + 2)));
+    th = std::min<long long>(256, std::max<long long>(th, std::max(8, 2 * R + 2)));
     if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
     if (const char* e = getenv("FGF_LR_V")) {
