@@ -1,0 +1,140 @@
+"""SURVEY §8(d) per-configuration report: every BASELINE.json configuration (and the s sweep
+of configs 1 and 4) in its own launch configuration, timed with CUDA events (3 warm-up calls,
+median / min / max of 10), checked against the fp64 oracle on a deterministic sample of images
+(max |dq| against the north-star tolerance), with BASELINE's byte model, the oracle's own
+throughput on one image (host cores), and the PSNR of q at s against the s = 1 filter.
+
+It is a parity test first (every record must pass); with FGF_REPORT=<path> it also appends one
+JSON line per record to <path> (profiles/round1/report_configs.jsonl is produced this way).
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+import statistics
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+import paper_1505_00996_b200 as fgf  # no fallback: a missing libfgf.so fails here
+
+# (cfg, s override, oracle sample images)
+RECORDS = [
+    (0, None, [0]),
+    (1, None, [0]), (1, 1, [0]),
+    (2, None, [0]),
+    (3, None, [0, 63]),
+    (4, None, [0, 255]), (4, 1, [0]), (4, 2, [0]), (4, 8, [0]),
+]
+
+PEAK_GBS = 6530.0
+
+
+def _peak():
+    try:
+        with open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return PEAK_GBS
+
+
+def _sm_clock():
+    try:
+        import subprocess
+        out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm", "--format=csv,noheader,nounits",
+                              "-i", "0"], capture_output=True, text=True, timeout=10).stdout
+        return float(out.strip().splitlines()[0])
+    except Exception:
+        return None
+
+
+def _psnr(a, b):
+    mse = float(((a.double() - b.double()) ** 2).mean())
+    return float("inf") if mse == 0 else 10.0 * math.log10(1.0 / mse)
+
+
+@pytest.mark.parametrize("cfg,s_over,sample", RECORDS)
+def test_config_report(cfg, s_over, sample):
+    c = synth.CONFIGS[cfg]
+    prm = synth.params(cfg, **({} if s_over is None else {"s": s_over}))
+    r, eps, s, sub = prm["r"], prm["eps"], prm["s"], prm["sub_mode"]
+    B, H, W, CI, CP = c["batch"], c["H"], c["W"], c["C_I"], c["C_p"]
+    if cfg == 4 and s == 1:
+        B = 32                                   # the full-resolution maps of 256 images: 32 per call
+    I, p = synth.make_batch(cfg, "cuda", batch=B)
+    q = torch.empty((B, CP, H, W), device="cuda")
+    nb = fgf.fgf_workspace_bytes(B, H, W, CI, CP, r, s)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def call():
+        fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, nb, st)
+
+    for _ in range(3):
+        call()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(10):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        call()
+        b.record(st)
+        b.synchronize()
+        times.append(a.elapsed_time(b))
+    t_med = statistics.median(times)
+    launches = fgf.fgf_last_launch_count()
+
+    # parity on the sampled images
+    tol = 1e-4 if eps >= 1e-3 else 1e-3
+    worst = 0.0
+    oracle_s = 0.0
+    for i in sample:
+        Ih = I[i:i + 1].cpu().numpy()
+        ph = p[i:i + 1].cpu().numpy()
+        t0 = time.perf_counter()
+        ref = oracle.fast_guided_filter(Ih, ph, r, eps, s, sub)
+        if i == sample[0]:
+            oracle_s = time.perf_counter() - t0
+        worst = max(worst, float(np.abs(q[i:i + 1].double().cpu().numpy() - ref).max()))
+    assert worst <= tol, (cfg, s, worst)
+
+    # quality against the full-resolution filter (s = 1) on the first image
+    psnr = None
+    if s > 1:
+        q1 = fgf.filter(I[:1].contiguous(), p[:1].contiguous(), r, eps, 1, sub)
+        torch.cuda.synchronize()
+        psnr = _psnr(q[:1], q1)
+
+    N = H * W
+    h, w = -(-H // s), -(-W // s)
+    n = h * w
+    NC = (CI + 1) * CP
+    B_model = B * (4 * N * (CI + 2 * CP) + 8 * n * NC)
+    rho = 1.0 if (s == 1 or sub == 1) else 1.0 / min(s, 8)
+    B_alg = B * 4 * N * (CI + rho * CP + CP)
+    peak = _peak()
+    rec = {
+        "cfg": cfg, "name": c["name"], "s": s, "G": 1, "sub_mode": "block_mean" if sub else "nearest",
+        "batch": B, "H": H, "W": W, "C_I": CI, "C_p": CP, "r": r, "eps": eps,
+        "t_med_ms": t_med, "t_min_ms": min(times), "t_max_ms": max(times),
+        "mpx_s": B * N / (t_med / 1e3) / 1e6,
+        "B_model": B_model, "B_alg": B_alg,
+        "frac_model_8T": B_model / (t_med / 1e3) / 8e12,
+        "frac_model_meas": B_model / (t_med / 1e3) / (peak * 1e9),
+        "max_abs_dq": worst, "tol": tol, "pass": worst <= tol, "oracle_images": sample,
+        "oracle_mpx_s": N / oracle_s / 1e6, "host_cores": os.cpu_count(),
+        "sm_clock_mhz": _sm_clock(), "psnr_vs_s1_db": psnr,
+        "kernel_launches": launches,
+    }
+    out = os.environ.get("FGF_REPORT")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps(rec) + "\n")
