@@ -248,6 +248,10 @@ int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cud
     return launch_subsample_e<float>(src, dst, planes, P, st);
 }
 
+// measured (config 4): prefix sums win at r' = 32 (s = 1: 22.8 -> 15.6 ms per 32 images), lose at
+// r' = 15, 16 (configs 2, 1 s=1, 4 s=2)
+constexpr int kHpreR = 24;
+
 template <int MODE, int CI, int CP, int NT>
 int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
     using C = StripConfig<MODE, CI, CP, NT>;
@@ -265,7 +269,11 @@ int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream
     sp.TH = TH;
     sp.TW = P.TW;
     dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
-    auto kern = box_strip_kernel<MODE, CI, CP, NT>;
+    // wide windows: prefix-sum horizontal phase (restart-free); measured threshold below
+    int hpre_r = kHpreR;
+    if (const char* e = getenv("FGF_HPRE_R")) hpre_r = atoi(e);
+    auto kern = P.R >= hpre_r ? box_strip_kernel<MODE, CI, CP, NT, 0, 0, true>
+                              : box_strip_kernel<MODE, CI, CP, NT, 0, 0, false>;
     set_smem(kern, smem);
     ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
     kern<<<grid, NT, smem, st>>>(sp);

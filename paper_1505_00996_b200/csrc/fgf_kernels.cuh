@@ -361,7 +361,11 @@ __device__ __forceinline__ void load_row(const float* bI, const float* bP, int o
 }
 
 // grid (strips, segments, images); block NT.
-template <int MODE, int CI, int CP, int NT, int G_ = 0, int MINB_ = 0>
+// HPRE: wide windows (large r') -- the horizontal window sums come from an in-place prefix
+// sum of each snapshotted row (one warp per row; cost independent of r') instead of sliding
+// runs whose restart costs 2r'+1 reads per run.  Sums of fp64 column sums over <= 1024
+// columns: the difference of two prefixes loses nothing at the 1e-4 level.
+template <int MODE, int CI, int CP, int NT, int G_ = 0, int MINB_ = 0, bool HPRE = false>
 __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>::MINB)) box_strip_kernel(StripParams P) {
     using T = StripTraits<MODE, CI, CP>;
     using C = StripConfig<MODE, CI, CP, NT, G_, MINB_>;
@@ -491,9 +495,49 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
         // ---- prefetch the next batch (in flight during the horizontal phase).
         if (colthr && yb + G < ye) load_batch(yb + G);
 
+        if (HPRE) {
+            // ---- horizontal phase by prefix sums: rows (g, m), one warp each, in place over
+            // Vs indices [0, L); the window of output oc is P[cbase+oc+2R] - P[cbase+oc-1].
+            const int L = R + ncol;
+            const int CH = (L + 31) >> 5;
+            const int nrows_b = min(G, ye - yb);
+            for (int rr = warp; rr < nrows_b * NMAP; rr += C::NW) {
+                double* vrow = Vs + (size_t)rr * VP;
+                const int a = lane * CH, e = min(L, a + CH);
+                double tot = 0.0;
+                for (int i = a; i < e; ++i) tot += vrow[i];
+                // exclusive warp scan of the chunk totals
+                double x = tot;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, x, d);
+                    if (lane >= d) x += y;
+                }
+                double run = x - tot;
+                for (int i = a; i < e; ++i) {
+                    run += vrow[i];
+                    vrow[i] = run;
+                }
+            }
+            __syncthreads();
+            for (int qq = tid; qq < nrows_b * ocn; qq += NT) {
+                const int g = qq / ocn, oc = qq - g * ocn;
+                const int yo2 = yb + g;
+                const double invy = 1.0 / (double)(min(h - 1, yo2 + R) - max(0, yo2 - R) + 1);
+                // past the scanned range the columns are zero pads: the prefix stays P[L-1]
+                const int hi = min(cbase + oc + 2 * R, L - 1), lo = cbase + oc - 1;
+                const double* pr = Vs + (size_t)g * NMAP * VP;
+                double S[NMAP];
+#pragma unroll
+                for (int m = 0; m < NMAP; ++m)
+                    S[m] = pr[m * VP + hi] - (lo >= 0 ? pr[m * VP + lo] : 0.0);
+                StripEpilogue<MODE, CI, CP>::emit(S, invx[oc] * invy, P,
+                                                  Os + (size_t)g * NOUT * NT + oc, NT);
+            }
+        }
         // ---- horizontal phase: branch-free sliding window along each snapshotted row.
         const int yo = yb + hg;
-        if (yo < ye && oc0 < ocn) {
+        if (!HPRE && yo < ye && oc0 < ocn) {
             const double* vr = Vs + (size_t)hg * NMAP * VP + R + cbase + oc0;  // local col of oc0
             const double invy = 1.0 / (double)(min(h - 1, yo + R) - max(0, yo - R) + 1);
             double S[NMAP];
