@@ -252,9 +252,9 @@ int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cud
 // r' = 15, 16 (configs 2, 1 s=1, 4 s=2)
 constexpr int kHpreR = 24;
 
-template <int MODE, int CI, int CP, int NT>
-int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
-    using C = StripConfig<MODE, CI, CP, NT>;
+template <int MODE, int CI, int CP, int NT, int G_ = 0>
+int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
+    using C = StripConfig<MODE, CI, CP, NT, G_>;
     StripParams sp = sp0;
     sp.VP = NT + 2 * P.R + C::K + 1;
     const size_t smem = C::smem(sp.VP);
@@ -272,13 +272,26 @@ int launch_strip_t(const StripParams& sp0, int images, const Plan& P, cudaStream
     // wide windows: prefix-sum horizontal phase (restart-free); measured threshold below
     int hpre_r = kHpreR;
     if (const char* e = getenv("FGF_HPRE_R")) hpre_r = atoi(e);
-    auto kern = P.R >= hpre_r ? box_strip_kernel<MODE, CI, CP, NT, 0, 0, true>
-                              : box_strip_kernel<MODE, CI, CP, NT, 0, 0, false>;
+    auto kern = P.R >= hpre_r ? box_strip_kernel<MODE, CI, CP, NT, G_, 0, true>
+                              : box_strip_kernel<MODE, CI, CP, NT, G_, 0, false>;
     set_smem(kern, smem);
     ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
     kern<<<grid, NT, smem, st>>>(sp);
     ++g_last_launches;
     return last_error();
+}
+
+// The default G assumes the worst-case padded row (r' up to the strip limit); colour
+// statistics (13 / 21 fp64 maps) then get G = 1 or 2.  With r' <= 16 the real rows are short
+// enough for more rows per batch (fewer barriers, longer runs).
+template <int MODE, int CI, int CP, int NT>
+int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
+    if (CI == 3 && NT == 256 && P.R <= 16 && getenv("FGF_STRIP_WORSTG") == nullptr) {
+        constexpr int GC = (MODE == MODE_MEAN || CP == 1) ? 4 : 2;
+        const int rc = launch_strip_g<MODE, CI, CP, NT, GC>(sp, images, P, st);
+        if (rc != FGF_ERR_UNSUPPORTED) return rc;
+    }
+    return launch_strip_g<MODE, CI, CP, NT>(sp, images, P, st);
 }
 
 template <int MODE, int CI, int CP>
