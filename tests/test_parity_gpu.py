@@ -240,3 +240,18 @@ def test_device_errors():
     Ih = torch.rand((1, 1, 64, 64))
     assert fgf.fgf_filter_host(I, I, Ih, 1, 64, 64, 1, 1, 8, 0.01, 4, 0, 0,
                                check=False) == fgf.FGF_ERR_DEVICE
+
+
+def test_multi_chunk_pipeline_equals_single_chunk(monkeypatch):
+    """A batch larger than one pipeline slot runs as several chunks (low-res chain of chunk j
+    on the library's second stream while K4 of chunk j-1 streams): same result, bit for bit,
+    as one chunk; covers K13 (gray) and the strip engine (colour)."""
+    for cfg, H, W in [(1, 1080, 1920), (3, 135, 240)]:   # 6 and 2 chunks at 1 MB per slot
+        I, p = synth.make_batch(cfg, "cuda", batch=6, H=H, W=W)
+        prm = synth.params(cfg)
+        monkeypatch.delenv("FGF_CHUNK_MB", raising=False)
+        q1 = gpu_filter(I, p, **prm)
+        monkeypatch.setenv("FGF_CHUNK_MB", "1")        # ~1 MB of low-res workspace per slot
+        q2 = gpu_filter(I, p, **prm)
+        torch.cuda.synchronize()
+        assert torch.equal(q1, q2), cfg
