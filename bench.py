@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dtype", choices=["f32", "f16", "bf16"], default="f32",
                     help="element type of I, p, q (f16 / bf16: the reduced-precision I/O variant)")
+    ap.add_argument("--band-mode", choices=["single", "two-step"], default="single",
+                    help="config 5: one 2r'+1-row exchange of I', p', or r' rows then r'+1 rows of a, b")
     ap.add_argument("--band-impl", choices=["c", "torch"], default="c",
                     help="config 5 (4b): C-ABI band call with NCCL inside, or the Python stages")
     return ap.parse_args()
@@ -388,9 +390,11 @@ def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
         nb = fgf.fgf_band_workspace_bytes(H, W, pl.Y0, rows, 1, 1, r, s, world)
         ws = torch.empty(nb, dtype=torch.uint8, device=dev)
 
+        mode = fgf.FGF_BAND_TWO_STEP if args.band_mode == "two-step" else fgf.FGF_BAND_SINGLE
+
         def step():
-            fgf.fgf_filter_band(I_own, p_own, q_own, H, W, pl.Y0, rows, 1, 1, r, eps, s, sub,
-                                comm, rank, world, ws, nb, stream)
+            fgf.fgf_filter_band_ex(I_own, p_own, q_own, H, W, pl.Y0, rows, 1, 1, r, eps, s, sub,
+                                   mode, comm, rank, world, ws, nb, stream)
             return q_own
     else:
         ex = bands.DistExchange(rank, world)
@@ -423,7 +427,7 @@ def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": c["name"], "H": H, "W": W, "r": r, "eps": eps, "s": s,
                            "parallelism": f"row bands x{world}, halo {pl.halo} low-res rows "
-                                          + ("fgf_filter_band (NCCL P2P inside libfgf.so)"
+                                          + (f"fgf_filter_band_ex {args.band_mode} (NCCL P2P inside libfgf.so)"
                                              if args.band_impl == "c" else
                                              "over torch.distributed P2P"),
                            "l2": "inputs larger than L2 (no flush needed)"}}

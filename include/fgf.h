@@ -165,6 +165,18 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
  * FGF_ERR_CUDA.  The NCCL library is loaded at run time (dlopen "libnccl.so.2"). */
 size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
                                 int s, int nranks);
+/* Halo exchange modes of the band path. */
+enum {
+    FGF_BAND_SINGLE = 0,   /* one exchange: 2r'+1 rows of I', p' (the default of fgf_filter_band) */
+    FGF_BAND_TWO_STEP = 1  /* r' rows of I', p', then ceil(r/s)+1 = r'+1 rows of a, b (BASELINE.json's
+                              halo); the statistics of the halo rows are not recomputed */
+};
+/* fgf_filter_band with an explicit exchange mode (FGF_ERR_PARAM for an unknown mode).  Every
+ * rank must use the same mode; the workspace query covers both. */
+int fgf_filter_band_ex(const float* I_band, const float* p_band, float* q_band, int H_total,
+                       int W, int row0, int rows, int C_I, int C_p, int r, double eps, int s,
+                       int sub_mode, int mode, void* nccl_comm, int rank, int nranks,
+                       void* workspace, size_t ws_bytes, void* cuda_stream);
 int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int H_total, int W,
                     int row0, int rows, int C_I, int C_p, int r, double eps, int s, int sub_mode,
                     void* nccl_comm, int rank, int nranks, void* workspace, size_t ws_bytes,
@@ -179,12 +191,12 @@ int fgf_nccl_comm_destroy(void* comm);
  * (batch 1) are filtered one after another with the halo rows copied between the bands'
  * buffers (the same halo geometry fgf_filter_band sends over NCCL), and stitched into q.
  * Band k owns low-res rows [k h / nranks, (k+1) h / nranks).  Workspace:
- * fgf_bands_loopback_workspace_bytes(). */
+ * fgf_bands_loopback_workspace_bytes(); mode as fgf_filter_band_ex. */
 size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r, int s,
                                           int nranks);
 int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, int W, int C_I,
-                              int C_p, int r, double eps, int s, int sub_mode, int nranks,
-                              void* workspace, size_t ws_bytes, void* cuda_stream);
+                              int C_p, int r, double eps, int s, int sub_mode, int mode,
+                              int nranks, void* workspace, size_t ws_bytes, void* cuda_stream);
 
 /* Reduced-precision I/O: fgf_filter_ws with I, p and q of element type
  * dtype (FGF_F32 / FGF_F16 / FGF_BF16; all three buffers the same type, 2-byte alignment for

@@ -35,6 +35,8 @@ FGF_ERR_DEVICE = 10
 FGF_F32 = 0
 FGF_F16 = 1
 FGF_BF16 = 2
+FGF_BAND_SINGLE = 0
+FGF_BAND_TWO_STEP = 1
 FGF_SUB_NEAREST = 0
 FGF_SUB_BILINEAR = 1
 
@@ -45,7 +47,8 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_lowres_workspace_bytes", "fgf_lowres_mean", "fgf_upsample_output_rows",
            "fgf_enhance_ws", "fgf_band_workspace_bytes", "fgf_filter_band", "fgf_nccl_unique_id",
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
-           "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws")
+           "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
+           "fgf_filter_band_ex")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -93,7 +96,9 @@ _lib.fgf_nccl_comm_destroy.argtypes = [_P]
 _lib.fgf_nccl_comm_destroy.restype = _i
 _lib.fgf_bands_loopback_workspace_bytes.argtypes = [_i] * 7
 _lib.fgf_bands_loopback_workspace_bytes.restype = _sz
-_lib.fgf_filter_bands_loopback.argtypes = [_P, _P, _P] + [_i] * 5 + [_d, _i, _i, _i, _P, _sz, _P]
+_lib.fgf_filter_bands_loopback.argtypes = [_P, _P, _P] + [_i] * 5 + [_d, _i, _i, _i, _i, _P, _sz, _P]
+_lib.fgf_filter_band_ex.argtypes = [_P, _P, _P] + [_i] * 7 + [_d, _i, _i, _i, _P, _i, _i, _P, _sz, _P]
+_lib.fgf_filter_band_ex.restype = _i
 _lib.fgf_filter_bands_loopback.restype = _i
 _lib.fgf_workspace_bytes_ex.argtypes = [_i] * 8
 _lib.fgf_workspace_bytes_ex.restype = _sz
@@ -276,6 +281,17 @@ def fgf_filter_band(I_band, p_band, q_band, H_total, W, row0, rows, C_I, C_p, r,
     return rc
 
 
+def fgf_filter_band_ex(I_band, p_band, q_band, H_total, W, row0, rows, C_I, C_p, r, eps, s,
+                       sub_mode, mode, nccl_comm, rank, nranks, workspace, ws_bytes, stream=None,
+                       check=True):
+    rc = _lib.fgf_filter_band_ex(_addr(I_band), _addr(p_band), _addr(q_band), H_total, W, row0,
+                                 rows, C_I, C_p, r, float(eps), s, sub_mode, mode, nccl_comm, rank,
+                                 nranks, _addr(workspace), ws_bytes, _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_band_ex")
+    return rc
+
+
 def fgf_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.fgf_nccl_unique_id(buf), "fgf_nccl_unique_id")
@@ -298,9 +314,9 @@ def fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks) -> int:
 
 
 def fgf_filter_bands_loopback(I, p, q, H, W, C_I, C_p, r, eps, s, sub_mode, nranks, workspace,
-                              ws_bytes, stream=None, check=True):
+                              ws_bytes, stream=None, check=True, mode=FGF_BAND_SINGLE):
     rc = _lib.fgf_filter_bands_loopback(_addr(I), _addr(p), _addr(q), H, W, C_I, C_p, r,
-                                        float(eps), s, sub_mode, nranks, _addr(workspace),
+                                        float(eps), s, sub_mode, mode, nranks, _addr(workspace),
                                         ws_bytes, _stream(stream))
     if check:
         _check(rc, "fgf_filter_bands_loopback")

@@ -910,21 +910,34 @@ int fgf_nccl_comm_destroy(void* comm) {
 
 size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
                                 int s, int nranks) {
-    BandPlan B;
-    if (band_plan(B, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false))
+    BandPlan B1, B2;
+    if (band_plan(B1, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
+                  FGF_BAND_SINGLE) ||
+        band_plan(B2, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
+                  FGF_BAND_TWO_STEP))
         return 0;
-    return B.ws_total;
+    return std::max(B1.ws_total, B2.ws_total);
 }
 
 int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int H_total, int W,
                     int row0, int rows, int C_I, int C_p, int r, double eps, int s, int sub_mode,
                     void* nccl_comm, int rank, int nranks, void* workspace, size_t ws_bytes,
                     void* cuda_stream) {
+    return fgf_filter_band_ex(I_band, p_band, q_band, H_total, W, row0, rows, C_I, C_p, r, eps, s,
+                              sub_mode, FGF_BAND_SINGLE, nccl_comm, rank, nranks, workspace,
+                              ws_bytes, cuda_stream);
+}
+
+int fgf_filter_band_ex(const float* I_band, const float* p_band, float* q_band, int H_total,
+                       int W, int row0, int rows, int C_I, int C_p, int r, double eps, int s,
+                       int sub_mode, int mode, void* nccl_comm, int rank, int nranks,
+                       void* workspace, size_t ws_bytes, void* cuda_stream) {
     g_last_launches = 0;
     if (nranks < 1 || rank < 0 || rank >= nranks) return FGF_ERR_PARAM;
     const bool self = I_band == p_band && C_I == 1 && C_p == 1;
     BandPlan B;
-    int rc = band_plan(B, H_total, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self);
+    int rc = band_plan(B, H_total, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self,
+                       mode);
     if (rc) return rc;
     if (!I_band || !p_band || !q_band || !workspace) return FGF_ERR_NULL;
     if (nranks > 1 && !nccl_comm) return FGF_ERR_NULL;
@@ -941,14 +954,16 @@ int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     char* ws = static_cast<char*>(workspace);
     if ((rc = band_prepare(B, I_band, p_band, ws, st))) return rc;
-    if (nranks > 1) {
+    // one NCCL group: every plane's halo rows to / from rank-1 and rank+1
+    auto exchange = [&](int planes, bool ab) -> int {
+        if (nranks == 1) return FGF_OK;
         const Nccl* n = nccl();
         if (!n) return FGF_ERR_NCCL;
         ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
         if (n->groupStart() != ncclSuccess) return FGF_ERR_NCCL;
         ncclResult_t e = ncclSuccess;
-        for (int j = 0; j < B.NPL && e == ncclSuccess; ++j) {
-            const Halo hl = band_halo(B, ws, j, rank, nranks);
+        for (int j = 0; j < planes && e == ncclSuccess; ++j) {
+            const Halo hl = ab ? band_halo_ab(B, ws, j, rank, nranks) : band_halo(B, ws, j, rank, nranks);
             if (hl.n_up) {
                 e = n->send(hl.send_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
                 if (e == ncclSuccess) e = n->recv(hl.recv_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
@@ -959,29 +974,39 @@ int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int
             }
         }
         if (n->groupEnd() != ncclSuccess || e != ncclSuccess) return FGF_ERR_NCCL;
+        return FGF_OK;
+    };
+    if ((rc = exchange(B.NPL, false))) return rc;                      // I', p' (exchange A)
+    if (B.mode == FGF_BAND_TWO_STEP) {
+        if ((rc = band_stats_ab(B, ws, st, self))) return rc;
+        if ((rc = exchange(B.lp.NC, true))) return rc;                 // a, b (exchange B)
     }
     return band_finish(B, I_band, q_band, ws, st, self);
 }
 
 size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r, int s,
                                           int nranks) {
+    // (the larger of the two exchange modes)
     if (nranks < 1 || s < 1 || H < 1 || W < 1) return 0;
     const int h = lowres_dim(H, s);
     size_t tot = 0;
     for (int k = 0; k < nranks; ++k) {
         const int y0 = (int)((long long)k * h / nranks), y1 = (int)((long long)(k + 1) * h / nranks);
         const int row0 = y0 * s, rows = std::min(H, y1 * s) - row0;
-        BandPlan B;
-        if (band_plan(B, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false))
+        BandPlan B1, B2;
+        if (band_plan(B1, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
+                      FGF_BAND_SINGLE) ||
+            band_plan(B2, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
+                      FGF_BAND_TWO_STEP))
             return 0;
-        tot += B.ws_total + 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
+        tot += std::max(B1.ws_total, B2.ws_total) + 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
     }
     return tot;
 }
 
 int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, int W, int C_I,
-                              int C_p, int r, double eps, int s, int sub_mode, int nranks,
-                              void* workspace, size_t ws_bytes, void* cuda_stream) {
+                              int C_p, int r, double eps, int s, int sub_mode, int mode,
+                              int nranks, void* workspace, size_t ws_bytes, void* cuda_stream) {
     g_last_launches = 0;
     if (nranks < 1) return FGF_ERR_PARAM;
     Plan P0;
@@ -1002,10 +1027,14 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
     for (int k = 0; k < nranks; ++k) {
         const int y0 = (int)((long long)k * h / nranks), y1 = (int)((long long)(k + 1) * h / nranks);
         const int row0 = y0 * s, rows = std::min(H, y1 * s) - row0;
-        if ((rc = band_plan(Bs[k], H, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self)))
+        if ((rc = band_plan(Bs[k], H, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self,
+                            mode)))
             return rc;
         wss[k] = cur;
-        cur += Bs[k].ws_total;
+        BandPlan Bx;   // the workspace layout reserves the larger mode (as the size query)
+        band_plan(Bx, H, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self,
+                  mode == FGF_BAND_SINGLE ? FGF_BAND_TWO_STEP : FGF_BAND_SINGLE);
+        cur += std::max(Bs[k].ws_total, Bx.ws_total);
         // the band's own rows, contiguous per plane, as a rank would hold them
         Ib[k] = reinterpret_cast<float*>(cur);
         pb[k] = self ? Ib[k] : Ib[k] + (size_t)C_I * rows * W;
@@ -1024,16 +1053,32 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
         launches += g_last_launches;
         g_last_launches = 0;
     }
-    // the exchange, rank k <-> k+1, with the same halo geometry the NCCL path sends
-    for (int k = 0; k + 1 < nranks; ++k)
-        for (int j = 0; j < Bs[k].NPL; ++j) {
-            const Halo a = band_halo(Bs[k], wss[k], j, k, nranks);
-            const Halo b = band_halo(Bs[k + 1], wss[k + 1], j, k + 1, nranks);
-            if (a.n_down != b.n_up) return FGF_ERR_PARAM;   // both sides agree on the depth
-            if (cudaMemcpyAsync(a.recv_down, b.send_up, b.n_up * 4, cudaMemcpyDeviceToDevice, st) ||
-                cudaMemcpyAsync(b.recv_up, a.send_down, a.n_down * 4, cudaMemcpyDeviceToDevice, st))
-                return FGF_ERR_CUDA;
+    // the exchanges, rank k <-> k+1, with the same halo geometry the NCCL path sends
+    auto exchange = [&](bool ab) -> int {
+        for (int k = 0; k + 1 < nranks; ++k) {
+            const int planes = ab ? Bs[k].lp.NC : Bs[k].NPL;
+            for (int j = 0; j < planes; ++j) {
+                const Halo a = ab ? band_halo_ab(Bs[k], wss[k], j, k, nranks)
+                                  : band_halo(Bs[k], wss[k], j, k, nranks);
+                const Halo b = ab ? band_halo_ab(Bs[k + 1], wss[k + 1], j, k + 1, nranks)
+                                  : band_halo(Bs[k + 1], wss[k + 1], j, k + 1, nranks);
+                if (a.n_down != b.n_up) return FGF_ERR_PARAM;   // both sides agree on the depth
+                if (cudaMemcpyAsync(a.recv_down, b.send_up, b.n_up * 4, cudaMemcpyDeviceToDevice, st) ||
+                    cudaMemcpyAsync(b.recv_up, a.send_down, a.n_down * 4, cudaMemcpyDeviceToDevice, st))
+                    return FGF_ERR_CUDA;
+            }
         }
+        return FGF_OK;
+    };
+    if ((rc = exchange(false))) return rc;
+    if (mode == FGF_BAND_TWO_STEP) {
+        for (int k = 0; k < nranks; ++k) {
+            if ((rc = band_stats_ab(Bs[k], wss[k], st, self))) return rc;
+            launches += g_last_launches;
+            g_last_launches = 0;
+        }
+        if ((rc = exchange(true))) return rc;
+    }
     for (int k = 0; k < nranks; ++k) {
         if ((rc = band_finish(Bs[k], Ib[k], qb[k], wss[k], st, self))) return rc;
         launches += g_last_launches;

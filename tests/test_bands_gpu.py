@@ -60,7 +60,7 @@ def test_upsample_rows_rejects_missing_maps():
 
 # ---------------------------------------------------------------- the C-ABI band path
 
-def _loopback(I, p, r, eps, s, sub, nranks):
+def _loopback(I, p, r, eps, s, sub, nranks, mode=fgf.FGF_BAND_SINGLE):
     _, C_I, H, W = I.shape
     C_p = p.shape[1]
     q = torch.empty((1, C_p, H, W), device="cuda")
@@ -68,14 +68,15 @@ def _loopback(I, p, r, eps, s, sub, nranks):
     assert nb > 0
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
     fgf.fgf_filter_bands_loopback(I, p, q, H, W, C_I, C_p, r, eps, s, sub, nranks, ws, nb,
-                                  torch.cuda.current_stream())
+                                  torch.cuda.current_stream(), mode=mode)
     torch.cuda.synchronize()
     return q
 
 
+@pytest.mark.parametrize("mode", [0, 1])   # FGF_BAND_SINGLE, FGF_BAND_TWO_STEP
 @pytest.mark.parametrize("C_I,C_p,s,sub,nranks", [(1, 1, 4, 0, 1), (1, 1, 4, 0, 2), (1, 1, 4, 0, 8),
                                                   (3, 1, 2, 1, 3), (1, 2, 1, 0, 4), (3, 3, 4, 0, 5)])
-def test_c_band_loopback_matches_whole_image(C_I, C_p, s, sub, nranks):
+def test_c_band_loopback_matches_whole_image(C_I, C_p, s, sub, nranks, mode):
     """fgf_filter_bands_loopback: the C band path (same plan, subsample, halo geometry and
     finish as fgf_filter_band; halos copied between the bands' buffers) against the
     whole-image filter and the oracle."""
@@ -83,7 +84,7 @@ def test_c_band_loopback_matches_whole_image(C_I, C_p, s, sub, nranks):
     H, W, r, eps = 1200, 1032, 32, 0.01
     I = torch.rand((1, C_I, H, W), device="cuda", generator=g)
     p = torch.rand((1, C_p, H, W), device="cuda", generator=g)
-    q = _loopback(I, p, r, eps, s, sub, nranks)
+    q = _loopback(I, p, r, eps, s, sub, nranks, mode)
     q_whole = fgf.filter(I, p, r, eps, s, sub)
     torch.cuda.synchronize()
     assert float((q - q_whole).abs().max()) < 1e-5
@@ -91,9 +92,10 @@ def test_c_band_loopback_matches_whole_image(C_I, C_p, s, sub, nranks):
     assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 1e-4
 
 
-def test_c_band_loopback_self_guided_config4b_shape():
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c_band_loopback_self_guided_config4b_shape(mode):
     I, _ = synth.make_batch(0, "cuda", H=2048, W=512)
-    q = _loopback(I, I, 32, 0.01, 4, 0, 8)
+    q = _loopback(I, I, 32, 0.01, 4, 0, 8, mode)
     ref = oracle.fast_guided_filter(I.cpu().numpy(), I.cpu().numpy(), 32, 0.01, 4, 0)
     assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 1e-4
 
@@ -115,6 +117,12 @@ def test_c_band_single_rank_with_nccl_communicator():
                             torch.cuda.current_stream())
         torch.cuda.synchronize()
         assert float((q - fgf.filter(I, p, 16, 0.01, 4, 0)).abs().max()) < 1e-5
+        q2 = torch.empty_like(p)
+        fgf.fgf_filter_band_ex(I, p, q2, H, W, 0, H, 1, 1, 16, 0.01, 4, 0,
+                               fgf.FGF_BAND_TWO_STEP, comm, 0, 1, ws, nb,
+                               torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        assert float((q2 - q).abs().max()) < 1e-5
     finally:
         fgf.fgf_nccl_comm_destroy(comm)
 
