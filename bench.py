@@ -305,6 +305,18 @@ def main():
     tot = sum(v[0] for v in prof.values()) or 1.0
     for k, v in prof.items():
         kern[k]["share_of_kernel_time"] = v[0] / tot
+    # K13 (fused low-res chain): algorithmic DRAM bytes per step = the nearest sample rows of I
+    # and p (every s-th row, all of its sectors for s <= 8) + the mean maps written; it is
+    # issue/latency-bound, not HBM-bound, so this is context, not a roofline.
+    if "lowres_fused" in kern and prof["lowres_fused"][1]:
+        planes_in = CI + (0 if args.config == 0 else CP)
+        if sub == 0:      # samples read in place from the full-resolution rows
+            k13_bytes = B * (esize * N * planes_in / s + 4 * NC * n)
+        else:             # K0's compact fp32 planes
+            k13_bytes = B * (4 * n * planes_in + 4 * NC * n)
+        k13_ms = prof["lowres_fused"][0] / args.steps
+        kern["lowres_fused"]["alg_bytes_per_step"] = k13_bytes
+        kern["lowres_fused"]["alg_GBs"] = k13_bytes / (k13_ms / 1e3) / 1e9
 
     peak, peak_src = peaks()
     # Dominant kernel K4 (upsample + output): algorithmic bytes per launch = images per launch
