@@ -291,6 +291,13 @@ int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_
         const int rc = launch_strip_g<MODE, CI, CP, NT, GC>(sp, images, P, st);
         if (rc != FGF_ERR_UNSUPPORTED) return rc;
     }
+    // gray box of a, b at 12 <= r' < 24: 8 rows per batch (measured: config 4 s=2 K3 2.44 -> 2.27 ms
+    // per 64 images; the statistics kernel was slower with 8)
+    if (MODE == MODE_MEAN && CI == 1 && CP == 1 && NT == 256 && P.R >= 12 && P.R < kHpreR &&
+        getenv("FGF_STRIP_WORSTG") == nullptr) {
+        const int rc = launch_strip_g<MODE, CI, CP, NT, 8>(sp, images, P, st);
+        if (rc != FGF_ERR_UNSUPPORTED) return rc;
+    }
     return launch_strip_g<MODE, CI, CP, NT>(sp, images, P, st);
 }
 
