@@ -59,12 +59,39 @@ BAD = 0x1000  # a fake, 16-byte aligned address; validation must fail before it 
     ((1, 64, 64, 2, 1, 8, 0.01, 4, 0), fgf.FGF_ERR_SHAPE),     # C_I not in {1,3}
     ((1, 64, 64, 1, 5, 8, 0.01, 4, 0), fgf.FGF_ERR_SHAPE),     # C_p > 4
     ((1, 64, 64, 1, 0, 8, 0.01, 4, 0), fgf.FGF_ERR_SHAPE),
+    ((1, 65536, 32768, 1, 1, 8, 0.01, 4, 0), fgf.FGF_ERR_UNSUPPORTED),  # 2^31 in-image elements
 ])
 def test_validation_before_launch(args, code):
     a = 0x100000
     assert fgf.fgf_filter(a, a + 0x10000000, a + 0x20000000, *args, check=False) == code
     assert fgf.fgf_filter_ws(a, a + 0x10000000, a + 0x20000000, *args, BAD, 1 << 30, None,
                              check=False) == code
+    assert fgf.fgf_filter_ex_ws(a, a + 0x10000000, a + 0x20000000, *args, fgf.FGF_F16, BAD,
+                                1 << 30, None, check=False) == code
+
+
+def test_extended_entry_point_validation():
+    a = 0x100000
+    geo = (1, 64, 64, 1, 1, 8, 0.01, 4, 0)
+    # unknown element type; 16-bit types are not offered for C_I / C_p = 1 / 2
+    assert fgf.fgf_filter_ex_ws(a, a + 0x100000, a + 0x200000, *geo, 7, BAD, 1 << 30, None,
+                                check=False) == fgf.FGF_ERR_PARAM
+    assert fgf.fgf_filter_ex_ws(a, a + 0x100000, a + 0x200000, 1, 64, 64, 1, 2, 8, 0.01, 4, 0,
+                                fgf.FGF_F16, BAD, 1 << 30, None,
+                                check=False) == fgf.FGF_ERR_UNSUPPORTED
+    assert fgf.fgf_workspace_bytes_ex(1, 64, 64, 1, 1, 8, 4, 9) == 0
+    assert fgf.fgf_workspace_bytes_ex(1, 64, 64, 1, 1, 8, 4, fgf.FGF_F16) > 0
+    # enhancement: negative gain; band path: bad exchange mode, thin band, bad rank
+    assert fgf.fgf_enhance_ws(a, a + 0x100000, 1, 64, 64, 1, 8, 0.01, 4, 0, -1.0, BAD, 1 << 30,
+                              None, check=False) == fgf.FGF_ERR_PARAM
+    assert fgf.fgf_filter_band_ex(a, a, a + 0x100000, 1024, 64, 0, 64, 1, 1, 8, 0.01, 4, 0, 5,
+                                  None, 0, 1, BAD, 1 << 30, None,
+                                  check=False) == fgf.FGF_ERR_PARAM
+    assert fgf.fgf_filter_band(a, a, a + 0x100000, 1024, 64, 0, 64, 1, 1, 32, 0.01, 4, 0,
+                               None, 0, 4, BAD, 1 << 30, None, check=False) == fgf.FGF_ERR_PARAM
+    assert fgf.fgf_filter_band(a, a, a + 0x100000, 1024, 64, 0, 64, 1, 1, 8, 0.01, 4, 0,
+                               None, 4, 4, BAD, 1 << 30, None, check=False) == fgf.FGF_ERR_PARAM
+    assert fgf.fgf_band_workspace_bytes(1024, 64, 0, 256, 1, 1, 8, 4, 4) > 0
 
 
 def test_pointer_errors():
