@@ -524,6 +524,8 @@ template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int M
 int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
                          cudaStream_t st) {
     auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, E>;
+    LowresParams lpl = lp;
+    lpl.L = LowresCfg<CP, G, KA, KB, RING>::layout(g.NT, lp.TW, lp.TH, P.R);
     size_t smem = g.smem;
     // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
     // previous chunk can be co-resident (overlap experiment knob)
@@ -531,7 +533,7 @@ int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, co
     set_smem(kern, smem);
     dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
     ProfScope ps(KIND_LOWRES, st);
-    kern<<<grid, g.NT, smem, st>>>(lp);
+    kern<<<grid, g.NT, smem, st>>>(lpl);
     ++g_last_launches;
     return last_error();
 }

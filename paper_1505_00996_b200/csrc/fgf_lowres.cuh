@@ -34,6 +34,13 @@
 
 namespace fgf {
 
+// Shared-memory carve-up of K13 (bytes), computed on the host by LowresCfg::layout and passed
+// in the parameters.
+struct LowresLayout {
+    int NT, NCA, NCS, nrA, nrB, PA, PB, VPA, VPB, RBA, RBI, THA, THB;
+    size_t oVsA, oVsB, oInvxA, oInvxB, oInvyA, oInvyB, oABr, oINr, oOs, total;
+};
+
 struct LowresParams {
     // Sample (y, x) of image b: srcI[b*imgI + y*row + x*col]; p channel c at
     // srcP[b*imgP + c*planeP + y*row + x*col].  In-image offsets fit in 32 bits (validated).
@@ -47,6 +54,7 @@ struct LowresParams {
     int TW, TH;            // output columns per strip, output rows per segment
     double eps;
     float k1, k0;          // written maps: k1 mean_a + k0 (map 0), k1 mean (others); 1, 0 = plain
+    LowresLayout L;        // LowresCfg<...>::layout(blockDim.x, TW, TH, R), set by the host
 };
 
 template <int CP, int G, int KA, int KB, bool RING = true>
@@ -57,10 +65,7 @@ struct LowresCfg {
     // Shared-memory carve-up (bytes); identical on host and device.  Every horizontal run
     // may read / write past the last valid column: the pitches are padded so those accesses
     // stay inside zero-initialised (read) or scratch (write) padding.
-    struct Layout {
-        int NT, NCA, NCS, nrA, nrB, PA, PB, VPA, VPB, RBA, RBI;
-        size_t oVsA, oVsB, oInvxA, oInvxB, oABr, oINr, oOs, total;
-    };
+    using Layout = LowresLayout;
     __host__ __device__ static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
     __host__ __device__ static Layout layout(int NT, int TW, int TH, int R) {
         Layout L;
@@ -77,11 +82,15 @@ struct LowresCfg {
         if (L.VPB < L.PA) L.VPB = L.PA;
         L.RBA = 2 * R + G + 1;                   // a, b rows [yb - R - 1, yA) live at once
         L.RBI = 2 * R + 2;                       // sample rows [ya - R - 1, ya + R]
+        L.THA = TH + 2 * R + 2;                  // a, b rows of a segment (1 / count table)
+        L.THB = TH;
         size_t o = 0;
         L.oVsA = o; o = al16(o + (size_t)G * NMAP * L.VPA * 8);
         L.oVsB = o; o = al16(o + (size_t)G * NAB * L.VPB * 4);
         L.oInvxA = o; o = al16(o + (size_t)L.PA * 8);
         L.oInvxB = o; o = al16(o + (size_t)L.PB * 4);
+        L.oInvyA = o; o = al16(o + (size_t)L.THA * 8);
+        L.oInvyB = o; o = al16(o + (size_t)L.THB * 4);
         L.oABr = o; o = al16(o + (size_t)L.RBA * NAB * L.PA * 4);
         L.oINr = o; o = al16(o + (RING ? (size_t)L.RBI * NIN * NT * 4 : 0));
         L.oOs = o; o = al16(o + (size_t)G * NAB * L.PB * 4);
@@ -114,11 +123,13 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     extern __shared__ __align__(16) unsigned char smem[];
     const int NT = blockDim.x, tid = threadIdx.x;
     const int h = P.h, w = P.w, R = P.R, TW = P.TW;
-    const auto L = C::layout(NT, TW, P.TH, R);
+    const LowresLayout& L = P.L;
     double* VsA = reinterpret_cast<double*>(smem + L.oVsA);     // [G][NMAP][VPA]
     float* VsB = reinterpret_cast<float*>(smem + L.oVsB);       // [G][NAB][VPB]
     double* invxA = reinterpret_cast<double*>(smem + L.oInvxA); // [PA], 0 = outside the image
     float* invxB = reinterpret_cast<float*>(smem + L.oInvxB);   // [PB]
+    double* invyA = reinterpret_cast<double*>(smem + L.oInvyA); // [THA] per a, b row - yA0
+    float* invyB = reinterpret_cast<float*>(smem + L.oInvyB);   // [THB] per output row - y0
     float* ABr = reinterpret_cast<float*>(smem + L.oABr);       // [RBA][NAB][PA]
     float* INr = reinterpret_cast<float*>(smem + L.oINr);       // [RBI][NIN][NT]
     float* Os = reinterpret_cast<float*>(smem + L.oOs);         // [G][NAB][PB]
@@ -142,6 +153,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         invxA[j] = (j < L.NCA && ca >= 0 && ca < w) ? inv_count(ca, w, R) : 0.0;
     }
     for (int k = tid; k < PB; k += NT) invxB[k] = (float)inv_count(min(x0 + k, w - 1), w, R);
+    for (int t = tid; t < yA1 - yA0; t += NT) invyA[t] = inv_count(yA0 + t, h, R);
+    for (int t = tid; t < yB1 - y0; t += NT) invyB[t] = (float)inv_count(y0 + t, h, R);
 
     // ---- this thread's sample column (stage A column phase)
     const int cs = x0 - 2 * R + tid;
@@ -341,7 +354,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         // ================= Y: horizontal phases
         if (runA && gA < nA) {
             const int ya = yA + gA;
-            const double invy = inv_count(ya, h, R);
+            const double invy = invyA[ya - yA0];
             int sl = sA + gA;
             if (sl >= RBA) sl -= RBA;
             float* ab = ABr + (size_t)sl * NAB * PA + jA0;
@@ -360,7 +373,8 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                 const double mI = S[0] * inv;
                 double var = fma(-mI, mI, S[1] * inv);     // var_I
                 var = var < 0.0 ? 0.0 : var;               // R8
-                const float rden = __fdividef(1.0f, (float)(var + P.eps));
+                float rden;                                // 1 / (var + eps), ~1 ulp
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"((float)(var + P.eps)));
                 const float mIf = (float)mI;
 #pragma unroll
                 for (int c = 0; c < CP; ++c) {
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             }
         }
         if (runB && gB < hbN) {
-            const float invy = (float)inv_count(hbY + gB, h, R);
+            const float invy = invyB[hbY + gB - y0];
             const float* ix = invxB + kB0;
             const float* vw = hvB + 2 * R + 1;
             float S[NAB];
@@ -402,12 +416,16 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         __syncthreads();
         // coalesced store of the outputs staged in Os
         if (hbN > 0 && tid < TW && x0 + tid < w) {
-            float* d = dstimg + (size_t)hbY * w + x0 + tid;
+            float* d[NAB];
+#pragma unroll
+            for (int m = 0; m < NAB; ++m) d[m] = dstimg + (size_t)m * n + (size_t)hbY * w + x0 + tid;
             const float* os = Os + tid;
             for (int g = 0; g < hbN; ++g) {
 #pragma unroll
-                for (int m = 0; m < NAB; ++m) d[(size_t)m * n] = os[m * PB];
-                d += w;
+                for (int m = 0; m < NAB; ++m) {
+                    *d[m] = os[m * PB];
+                    d[m] += w;
+                }
                 os += NAB * PB;
             }
         }
@@ -423,23 +441,23 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         const int nB = min(G, allowed - yb);
         if (nB > 0) {
             if (colBv) {
-                // row y of the a, b ring (y >= yA - RBA) for this column
-                auto slotp = [&](int y) {
+                // row y of the a, b ring (y >= yA - RBA): float offset of its slot
+                const int rstep = NAB * PA, rlen = RBA * NAB * PA;
+                auto slot_off = [&](int y) {
                     int s = sA - (yA - y);
                     s = s < 0 ? s + RBA : s;
-                    return ABr + (size_t)s * NAB * PA + tid;
+                    return s * rstep;
                 };
-                const float* ring_end = ABr + (size_t)RBA * NAB * PA + tid;
-                const int rstep = NAB * PA, rlen = RBA * NAB * PA;
+                const float* abc = ABr + tid;
                 if (yb == y0) {                   // warm-up: window of y0 - 1
                     for (int y = max(0, y0 - R - 1); y < min(h, y0 + R); ++y) {
-                        const float* r = slotp(y);
+                        const float* r = abc + slot_off(y);
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) accB[m] += r[m * PA];
                     }
                 }
-                const float* pa = slotp(min(yb + R, h - 1));
-                const float* ps = slotp(max(yb - R - 1, 0));
+                int oa = slot_off(min(yb + R, h - 1));
+                int os_ = slot_off(max(yb - R - 1, 0));
                 float* vcol = VsB + tid;
                 const bool full = nB == G && yb - R - 1 >= 0 && yb + G - 1 + R < h;
                 if (full) {
@@ -447,17 +465,17 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
 #pragma unroll
-                        for (int m = 0; m < NAB; ++m) accB[m] += pa[m * PA] - ps[m * PA];
+                        for (int m = 0; m < NAB; ++m) accB[m] += abc[oa + m * PA] - abc[os_ + m * PA];
                         float* v = vcol + g * NAB * VPB;
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) {
                             *v = accB[m];
                             v += VPB;
                         }
-                        pa += rstep;
-                        pa = pa >= ring_end ? pa - rlen : pa;
-                        ps += rstep;
-                        ps = ps >= ring_end ? ps - rlen : ps;
+                        oa += rstep;
+                        oa = oa >= rlen ? oa - rlen : oa;
+                        os_ += rstep;
+                        os_ = os_ >= rlen ? os_ - rlen : os_;
                     }
                 }
 #pragma unroll
@@ -467,11 +485,11 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                         const bool hasA = y + R < h, hasS = y - R - 1 >= 0;
 #pragma unroll
                         for (int m = 0; m < NAB; ++m)
-                            accB[m] += (hasA ? pa[m * PA] : 0.0f) - (hasS ? ps[m * PA] : 0.0f);
+                            accB[m] += (hasA ? abc[oa + m * PA] : 0.0f) - (hasS ? abc[os_ + m * PA] : 0.0f);
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) vcol[(g * NAB + m) * VPB] = accB[m];
-                        if (hasA) { pa += rstep; if (pa >= ring_end) pa -= rlen; }
-                        if (hasS) { ps += rstep; if (ps >= ring_end) ps -= rlen; }
+                        if (hasA) { oa += rstep; if (oa >= rlen) oa -= rlen; }
+                        if (hasS) { os_ += rstep; if (os_ >= rlen) os_ -= rlen; }
                     }
                 }
             }
