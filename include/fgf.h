@@ -209,6 +209,17 @@ int fgf_filter_ex_ws(const void* I, const void* p, void* q, int batch, int H, in
                      int C_p, int r, double eps, int s, int sub_mode, int dtype, void* workspace,
                      size_t ws_bytes, void* cuda_stream);
 
+/* Joint upsampling (the setting P:18 names as the origin of the speed-up,
+ * procedure not given in the paper -- DESIGN.md R18): the filtering input is given ONLY at
+ * low resolution, p_low: DEVICE [batch][C_p][h][w] with h = ceil(H/s), w = ceil(W/s), and is
+ * taken as the p' of Alg. 2; I' = f_sub(I, s) (sub_mode), steps 2-5 on (I', p'), steps 6-7
+ * with the full-resolution I: q [batch][C_p][H][W].  Workspace: fgf_joint_workspace_bytes().
+ * Errors as fgf_filter_ws. */
+size_t fgf_joint_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s);
+int fgf_filter_joint_ws(const float* I, const float* p_low, float* q, int batch, int H, int W,
+                        int C_I, int C_p, int r, double eps, int s, int sub_mode,
+                        void* workspace, size_t ws_bytes, void* cuda_stream);
+
 /* Detail enhancement, the application of PAPER.md Fig. 2 ("enhanced images with x5
  * detail"; SPEC S:303-311 enhance): out = (I - q) * gain + q, with q the SELF-guided fast
  * guided filter of I (p = I, C_p = C_I = C in {1, 3}) with these r, eps, s, sub_mode.  Since

@@ -194,3 +194,23 @@ def enhance(I, gain: float, r: int, eps: float, s: int, sub_mode: int = NEAREST)
         I = I[None, None]
     base = fast_guided_filter(I, I, r, eps, s, sub_mode)
     return (I.astype(np.float64) - base) * gain + base
+
+
+def joint_upsample(I, p_low, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
+    """Joint upsampling (R18; the setting P:18 names, no procedure in the paper):
+    p is given only at low resolution and IS the p' of Alg. 2; I' = f_sub(I, s), the
+    low-res steps run at s = 1 with r' = radius_lowres(r, s), and the output
+    uses the full-resolution I.  I: [B,C_I,H,W]; p_low: [B,C_p,h,w]."""
+    I = _f32(I)
+    if I.ndim == 2:
+        I = I[None, None]
+    p_low = _f32(p_low)
+    if p_low.ndim == 2:
+        p_low = p_low[None, None]
+    B, C_I, H, W = I.shape
+    Is = np.stack([np.stack([subsample(I[b, c], s, sub_mode) for c in range(C_I)])
+                   for b in range(B)]).astype(np.float32)
+    if p_low.shape[2:] != Is.shape[2:]:
+        raise ValueError("p_low must be [B, C_p, ceil(H/s), ceil(W/s)]")
+    mean_ab = coefficients(Is, p_low, radius_lowres(r, s), eps, 1, NEAREST)
+    return upsample_output(I, mean_ab, s)

@@ -48,7 +48,7 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_enhance_ws", "fgf_band_workspace_bytes", "fgf_filter_band", "fgf_nccl_unique_id",
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
-           "fgf_filter_band_ex")
+           "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -104,6 +104,10 @@ _lib.fgf_workspace_bytes_ex.argtypes = [_i] * 8
 _lib.fgf_workspace_bytes_ex.restype = _sz
 _lib.fgf_filter_ex_ws.argtypes = [_P, _P, _P] + _GEOM + [_i, _P, _sz, _P]
 _lib.fgf_filter_ex_ws.restype = _i
+_lib.fgf_joint_workspace_bytes.argtypes = [_i] * 7
+_lib.fgf_joint_workspace_bytes.restype = _sz
+_lib.fgf_filter_joint_ws.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
+_lib.fgf_filter_joint_ws.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -266,6 +270,20 @@ def fgf_filter_ex_ws(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, dtype,
     return rc
 
 
+def fgf_joint_workspace_bytes(batch, H, W, C_I, C_p, r, s) -> int:
+    return _lib.fgf_joint_workspace_bytes(batch, H, W, C_I, C_p, r, s)
+
+
+def fgf_filter_joint_ws(I, p_low, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, workspace,
+                        ws_bytes, stream=None, check=True):
+    rc = _lib.fgf_filter_joint_ws(_addr(I), _addr(p_low), _addr(q), batch, H, W, C_I, C_p, r,
+                                  float(eps), s, sub_mode, _addr(workspace), ws_bytes,
+                                  _stream(stream))
+    if check:
+        _check(rc, "fgf_filter_joint_ws")
+    return rc
+
+
 def fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks) -> int:
     return _lib.fgf_band_workspace_bytes(H_total, W, row0, rows, C_I, C_p, r, s, nranks)
 
@@ -418,3 +436,19 @@ def enhance(I, gain=5.0, r=16, eps=0.01, s=4, sub_mode=FGF_SUB_NEAREST, out=None
     st = stream if stream is not None else torch.cuda.current_stream(I.device)
     fgf_enhance_ws(I, out, B, H, W, C, r, eps, s, sub_mode, gain, buf, buf.numel(), st)
     return out
+
+
+def filter_joint(I, p_low, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, stream=None):
+    """Joint upsampling: q at I's resolution from the low-resolution input p_low
+    [B, C_p, ceil(H/s), ceil(W/s)] (fgf_filter_joint_ws)."""
+    import torch
+    B, C_I, H, W = I.shape
+    C_p = p_low.shape[1]
+    q = torch.empty((B, C_p, H, W), dtype=torch.float32, device=I.device)
+    nb = fgf_joint_workspace_bytes(B, H, W, C_I, C_p, r, s)
+    if nb == 0:
+        _check(FGF_ERR_PARAM, "fgf_joint_workspace_bytes")
+    ws = torch.empty(nb, dtype=torch.uint8, device=I.device)
+    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    fgf_filter_joint_ws(I, p_low.contiguous(), q, B, H, W, C_I, C_p, r, eps, s, sub_mode, ws, nb, st)
+    return q

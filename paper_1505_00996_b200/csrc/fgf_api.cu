@@ -1101,6 +1101,69 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
     return FGF_OK;
 }
 
+// ---- joint upsampling (R18): p given at low resolution
+struct JointPlan {
+    Plan P;                  // the full-resolution plan (I, q)
+    Plan L;                  // the s = 1 plan on the low-res planes, radius r'
+    size_t o_planes, o_lowres, o_mean, total;
+};
+
+int joint_plan(JointPlan& J, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
+               int sub) {
+    int rc = make_plan(J.P, batch, H, W, CI, CP, r, eps, s, sub);
+    if (rc) return rc;
+    if ((rc = make_plan(J.L, batch, J.P.h, J.P.w, CI, CP, J.P.R, eps, 1, FGF_SUB_NEAREST)))
+        return rc;
+    J.o_planes = 0;
+    J.o_lowres = align_up((size_t)batch * CI * J.P.n * sizeof(float));
+    J.o_mean = J.o_lowres + align_up(plan_ws(J.L, false));     // reused chunk by chunk
+    J.total = J.o_mean + align_up((size_t)batch * J.P.NC * J.P.n * sizeof(float));
+    return FGF_OK;
+}
+
+size_t fgf_joint_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s) {
+    JointPlan J;
+    if (joint_plan(J, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST)) return 0;
+    JointPlan J2;
+    if (joint_plan(J2, batch, H, W, C_I, C_p, r, 1.0, s, FGF_SUB_BILINEAR)) return 0;
+    return std::max(J.total, J2.total);
+}
+
+int fgf_filter_joint_ws(const float* I, const float* p_low, float* q, int batch, int H, int W,
+                        int C_I, int C_p, int r, double eps, int s, int sub_mode,
+                        void* workspace, size_t ws_bytes, void* cuda_stream) {
+    g_last_launches = 0;
+    JointPlan J;
+    int rc = joint_plan(J, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    const Plan& P = J.P;
+    if (!I || !p_low || !q || !workspace) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(p_low) |
+         reinterpret_cast<uintptr_t>(q)) & 3u)
+        return FGF_ERR_ALIGN;
+    const size_t bq = (size_t)batch * C_p * P.N * 4;
+    if (overlaps(q, bq, I, (size_t)batch * C_I * P.N * 4) ||
+        overlaps(q, bq, p_low, (size_t)batch * C_p * P.n * 4))
+        return FGF_ERR_ALIAS;
+    if (!is_device_ptr(I) || !is_device_ptr(p_low) || !is_device_ptr(q) || !is_device_ptr(workspace))
+        return FGF_ERR_DEVICE;
+    if (ws_bytes < J.total) return FGF_ERR_NOMEM;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    char* ws = static_cast<char*>(workspace);
+    float* Is = reinterpret_cast<float*>(ws + J.o_planes);
+    float* mean = reinterpret_cast<float*>(ws + J.o_mean);
+    // step 1 for I only (p' is given), steps 2-5 on (I', p'), steps 6-7 with the full-res I
+    if ((rc = launch_subsample(I, Is, batch * C_I, P, st))) return rc;
+    int launches = g_last_launches;
+    if ((rc = run_coefficients(Is, p_low, mean, J.L, ws + J.o_lowres, J.o_mean - J.o_lowres, st)))
+        return rc;
+    launches += g_last_launches;
+    g_last_launches = 0;
+    rc = launch_output(I, mean, q, batch, P, st);
+    g_last_launches += launches;
+    return rc;
+}
+
 int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, int r,
                    double eps, int s, int sub_mode, double gain, void* workspace,
                    size_t ws_bytes, void* cuda_stream) {

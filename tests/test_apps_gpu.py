@@ -67,3 +67,34 @@ def test_enhance_errors():
                               check=False) == fgf.FGF_ERR_ALIAS
     assert fgf.fgf_enhance_ws(I, out, 1, 64, 64, 2, 8, 0.01, 4, 0, 5.0, ws, ws.numel(), st,
                               check=False) == fgf.FGF_ERR_SHAPE
+
+
+# ---------------------------------------------------------------- joint upsampling (NEXT-4)
+
+@pytest.mark.parametrize("C_I,C_p,H,W,r,eps,s,sub", [
+    (1, 1, 540, 960, 16, 0.01, 4, 0),     # gray (K13 on the low-res planes)
+    (3, 1, 300, 400, 60, 1e-6, 4, 0),     # colour guide, one channel (feathering-like)
+    (3, 3, 270, 480, 8, 0.01, 4, 1),      # colour, block mean
+    (1, 2, 203, 301, 9, 0.02, 3, 1),      # ragged, s = 3
+])
+def test_joint_upsampling_vs_oracle(C_I, C_p, H, W, r, eps, s, sub):
+    g = torch.Generator(device="cuda").manual_seed(C_I * 10 + C_p + H)
+    I = torch.rand((2, C_I, H, W), device="cuda", generator=g)
+    h, w = -(-H // s), -(-W // s)
+    p_low = torch.rand((2, C_p, h, w), device="cuda", generator=g)
+    q = fgf.filter_joint(I, p_low, r, eps, s, sub)
+    torch.cuda.synchronize()
+    ref = oracle.joint_upsample(I.cpu().numpy(), p_low.cpu().numpy(), r, eps, s, sub)
+    err = float(np.abs(q.double().cpu().numpy() - ref).max())
+    assert err <= (1e-4 if eps >= 1e-3 else 1e-3), err
+
+
+def test_joint_with_subsampled_p_equals_filter():
+    """p_low = f_sub(p) (nearest) makes the joint path the filter itself, bit for bit up to
+    the low-res engine's segmentation (same kernels, same samples)."""
+    I, p = synth.make_batch(1, "cuda", batch=1, H=540, W=960)
+    p_low = p[:, :, ::4, ::4].contiguous()
+    q1 = fgf.filter_joint(I, p_low, 16, 0.01, 4, 0)
+    q2 = fgf.filter(I, p, 16, 0.01, 4, 0)
+    torch.cuda.synchronize()
+    assert float((q1 - q2).abs().max()) < 1e-5

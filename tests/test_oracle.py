@@ -358,3 +358,27 @@ def test_enhance_identities():
     assert np.allclose(e5 - base, 5.0 * (I - base), atol=1e-12)
     I3 = rng.random((1, 3, 20, 24)).astype(np.float32)
     assert np.allclose(oracle.enhance(I3, 1.0, 4, 0.01, 2), I3.astype(np.float64), rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------- joint upsampling (R18)
+
+@pytest.mark.parametrize("sub", [0, 1])
+def test_joint_upsample_reduces_to_fgf(sub):
+    """With p_low = f_sub(p, s) the joint path is Alg. 2 itself."""
+    rng = np.random.default_rng(41 + sub)
+    I = rng.random((1, 3, 37, 45)).astype(np.float32)
+    p = rng.random((1, 2, 37, 45)).astype(np.float32)
+    s, r, eps = 3, 7, 0.01
+    p_low = np.stack([oracle.subsample(p[0, c], s, sub) for c in range(2)])[None].astype(np.float32)
+    q_joint = oracle.joint_upsample(I, p_low, r, eps, s, sub)
+    q_fgf = oracle.fast_guided_filter(I, p, r, eps, s, sub)
+    # nearest: identical samples; block mean: I', p' rounded to fp32 on the joint side
+    assert np.abs(q_joint - q_fgf).max() <= (1e-12 if sub == 0 else 1e-5)
+
+
+def test_joint_upsample_constant_input():
+    rng = np.random.default_rng(5)
+    I = rng.random((1, 1, 40, 52)).astype(np.float32)
+    p_low = np.full((1, 1, 10, 13), 0.625, np.float32)
+    q = oracle.joint_upsample(I, p_low, 8, 1e-4, 4, 0)
+    assert np.abs(q - 0.625).max() < 1e-9
