@@ -317,6 +317,21 @@ def main():
         k13_ms = prof["lowres_fused"][0] / args.steps
         kern["lowres_fused"]["alg_bytes_per_step"] = k13_bytes
         kern["lowres_fused"]["alg_GBs"] = k13_bytes / (k13_ms / 1e3) / 1e9
+        # its real bound: instruction issue (warp-instructions per image from the committed
+        # ncu capture) against 148 SMs x 4 schedulers x the SM clock seen during the run
+        try:
+            ij = json.load(open(os.path.join(ROOT, "profiles", "k13_instructions.json")))
+            key = f"{c['name']}_s{s}"
+            if key in ij and args.dtype == "f32":
+                mhz = (clocks or {}).get("sm_mhz") or 1965.0
+                rate = ij[key]["warp_instructions_per_image"] * B / (k13_ms / 1e3)
+                peak_issue = 148 * 4 * mhz * 1e6
+                kern["lowres_fused"]["issue"] = {
+                    "bound": "issue", "achieved": rate, "peak": peak_issue,
+                    "unit": "warp-instr/s", "frac": rate / peak_issue,
+                    "source": "profiles/k13_instructions.json"}
+        except Exception:
+            pass
 
     peak, peak_src = peaks()
     # Dominant kernel K4 (upsample + output): algorithmic bytes per launch = images per launch
