@@ -197,16 +197,25 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     if (colA) {
         // warm-up: the window of row yA0 - 1, rows [yA0 - R - 1, yA0 + R - 1] clipped
         const int wa = max(0, yA0 - R - 1), wb = min(h, yA0 + R);
-        for (int y = wa; y < wb; ++y) {
-            float v[NIN];
-            load(y, v);
-            if (RING) {
-                int sl = sAdd + (y - yA0 - R);
-                if (sl < 0) sl += RBI;
+        constexpr int WB = 8;                     // rows whose loads are in flight together
+        for (int y0w = wa; y0w < wb; y0w += WB) {
+            float v[WB][NIN];
 #pragma unroll
-                for (int k = 0; k < NIN; ++k) inr[sl * ringStride + k * NT] = v[k];
+            for (int k = 0; k < WB; ++k)
+                if (y0w + k < wb) load(y0w + k, v[k]);
+#pragma unroll
+            for (int k = 0; k < WB; ++k) {
+                const int y = y0w + k;
+                if (y < wb) {
+                    if (RING) {
+                        int sl = sAdd + (y - yA0 - R);
+                        if (sl < 0) sl += RBI;
+#pragma unroll
+                        for (int c = 0; c < NIN; ++c) inr[sl * ringStride + c * NT] = v[k][c];
+                    }
+                    accum(accA, v[k], false);
+                }
             }
-            accum(accA, v, false);
         }
     }
     // prefetch of the add rows (and without the ring, the subtract rows) of a batch
