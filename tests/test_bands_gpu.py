@@ -141,3 +141,18 @@ def test_c_band_errors():
     # row0 not on the subsample grid
     assert fgf.fgf_filter_band(I, I, q, 1024, 64, 2, 64, 1, 1, 4, 0.01, 4, 0, None, 0, 1, ws,
                                ws.numel(), st, check=False) == fgf.FGF_ERR_PARAM
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("H,W,s,r,nranks", [(1003, 517, 4, 16, 3), (641, 300, 3, 9, 5),
+                                            (400, 128, 1, 6, 4), (1024, 200, 8, 40, 2)])
+def test_c_band_uneven_splits(H, W, s, r, nranks, mode):
+    """Bands of unequal heights, a last band ending off the subsample grid, s = 1 and s = 8,
+    r' from 2 to 6: the loop-back band path equals the whole-image filter."""
+    g = torch.Generator(device="cuda").manual_seed(H + W + nranks)
+    I = torch.rand((1, 1, H, W), device="cuda", generator=g)
+    p = torch.rand((1, 1, H, W), device="cuda", generator=g)
+    q = _loopback(I, p, r, 0.01, s, 0, nranks, mode)
+    q_whole = fgf.filter(I, p, r, 0.01, s, 0)
+    torch.cuda.synchronize()
+    assert float((q - q_whole).abs().max()) < 1e-5
