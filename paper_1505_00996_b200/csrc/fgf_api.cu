@@ -272,8 +272,12 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
     // wide windows: prefix-sum horizontal phase (restart-free); measured threshold below
     int hpre_r = kHpreR;
     if (const char* e = getenv("FGF_HPRE_R")) hpre_r = atoi(e);
-    auto kern = P.R >= hpre_r ? box_strip_kernel<MODE, CI, CP, NT, G_, 0, true>
-                              : box_strip_kernel<MODE, CI, CP, NT, G_, 0, false>;
+    // (instantiated for gray 1/1 and colour 3/1, 3/3 -- the channel layouts BASELINE.json uses)
+    constexpr bool HP_OK = (CI == 1 && CP == 1) || (CI == 3 && (CP == 1 || CP == 3));
+    auto kern = box_strip_kernel<MODE, CI, CP, NT, G_, 0, false>;
+    if constexpr (HP_OK) {
+        if (P.R >= hpre_r) kern = box_strip_kernel<MODE, CI, CP, NT, G_, 0, true>;
+    }
     set_smem(kern, smem);
     ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
     kern<<<grid, NT, smem, st>>>(sp);
@@ -286,14 +290,15 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
 // enough for more rows per batch (fewer barriers, longer runs).
 template <int MODE, int CI, int CP, int NT>
 int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
+    constexpr bool MEANLIKE = MODE == MODE_MEAN;
     if (CI == 3 && NT == 256 && P.R <= 16 && getenv("FGF_STRIP_WORSTG") == nullptr) {
-        constexpr int GC = (MODE == MODE_MEAN || CP == 1) ? 4 : 2;
+        constexpr int GC = (MEANLIKE || CP == 1) ? 4 : 2;
         const int rc = launch_strip_g<MODE, CI, CP, NT, GC>(sp, images, P, st);
         if (rc != FGF_ERR_UNSUPPORTED) return rc;
     }
     // gray box of a, b at 12 <= r' < 24: 8 rows per batch (measured: config 4 s=2 K3 2.44 -> 2.27 ms
     // per 64 images; the statistics kernel was slower with 8)
-    if (MODE == MODE_MEAN && CI == 1 && CP == 1 && NT == 256 && P.R >= 12 && P.R < kHpreR &&
+    if (MEANLIKE && CI == 1 && CP == 1 && NT == 256 && P.R >= 12 && P.R < kHpreR &&
         getenv("FGF_STRIP_WORSTG") == nullptr) {
         const int rc = launch_strip_g<MODE, CI, CP, NT, 8>(sp, images, P, st);
         if (rc != FGF_ERR_UNSUPPORTED) return rc;
@@ -684,6 +689,7 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     mp.k1 = P.k1; mp.k0 = P.k0;
     return launch_strip<MODE_MEAN>(mp, nb, P, st);
 }
+
 
 // Per-device pipeline objects: a high-priority stream for the low-res chain and the
 // fork / hand-off events.  Guarded by g_pipe_mu for the duration of an enqueue.
