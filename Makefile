@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # NCCL headers only (the library is dlopen-ed at run time by the band path)
 NCCL_INC ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include) /usr/include)
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -I$(NCCL_INC)
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -I$(NCCL_INC) --split-compile=0
 PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 SRCS := $(PKG)/csrc/fgf_api.cu
