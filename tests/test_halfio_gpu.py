@@ -84,3 +84,14 @@ def test_half_io_unsupported_and_errors():
                                 ws.numel(), st, check=False) == fgf.FGF_ERR_UNSUPPORTED
     assert fgf.fgf_filter_ex_ws(I, I, q[:, :1], 1, 64, 64, 1, 1, 8, 0.01, 4, 0, 7, ws,
                                 ws.numel(), st, check=False) == fgf.FGF_ERR_PARAM
+
+
+def test_half_io_multi_chunk_equals_single_chunk(monkeypatch):
+    """16-bit buffers through the chunked pipeline (element offsets of 2 bytes)."""
+    I, p = _inputs("gray", 6, 1, 1, 1080, 1920, torch.float16, 3)
+    monkeypatch.delenv("FGF_CHUNK_MB", raising=False)
+    q1 = fgf.filter(I, p, 16, 0.01, 4, 0)
+    monkeypatch.setenv("FGF_CHUNK_MB", "1")
+    q2 = fgf.filter(I, p, 16, 0.01, 4, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(q1, q2)
