@@ -32,7 +32,9 @@
  * SYNCHRONISATION.  Device-pointer entry points validate synchronously on the host, before
  * any launch, then enqueue kernels on the given stream and return without synchronising.
  * Launch failures return FGF_ERR_CUDA; asynchronous faults surface at the caller's next
- * synchronisation.  After any non-OK status q is unspecified.  fgf_filter_host() is
+ * synchronisation (with FGF_DEBUG_SYNC=1 in the environment every launch is followed by a
+ * device synchronisation and the faulting call returns FGF_ERR_CUDA).  Every launch is wrapped
+ * in an NVTX range named after its kernel.  After any non-OK status q is unspecified.  fgf_filter_host() is
  * synchronous: it returns when q is in host memory.
  *
  * REENTRANCY.  Calls with distinct workspaces and streams are thread-safe.  Results are
@@ -187,6 +189,10 @@ int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int
 int fgf_nccl_unique_id(void* id_out);
 int fgf_nccl_comm_init(void** comm_out, const void* id, int rank, int nranks);
 int fgf_nccl_comm_destroy(void* comm);
+/* Failure detection for the band path: polls ncclCommGetAsyncError on a communicator (the
+ * exchange is asynchronous, so a failed peer shows up here, not in fgf_filter_band's status).
+ * FGF_OK while healthy or in progress, FGF_ERR_NCCL on an asynchronous NCCL error. */
+int fgf_nccl_check(void* comm);
 /* Test driver of the band path on ONE device: the nranks bands of a whole image [C][H][W]
  * (batch 1) are filtered one after another with the halo rows copied between the bands'
  * buffers (the same halo geometry fgf_filter_band sends over NCCL), and stitched into q.

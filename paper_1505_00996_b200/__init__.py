@@ -48,7 +48,8 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_enhance_ws", "fgf_band_workspace_bytes", "fgf_filter_band", "fgf_nccl_unique_id",
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
-           "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws")
+           "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
+           "fgf_nccl_check")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
 
 _P = ctypes.c_void_p
@@ -92,6 +93,8 @@ _lib.fgf_nccl_unique_id.argtypes = [_P]
 _lib.fgf_nccl_unique_id.restype = _i
 _lib.fgf_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), _P, _i, _i]
 _lib.fgf_nccl_comm_init.restype = _i
+_lib.fgf_nccl_check.argtypes = [_P]
+_lib.fgf_nccl_check.restype = _i
 _lib.fgf_nccl_comm_destroy.argtypes = [_P]
 _lib.fgf_nccl_comm_destroy.restype = _i
 _lib.fgf_bands_loopback_workspace_bytes.argtypes = [_i] * 7
@@ -321,6 +324,10 @@ def fgf_nccl_comm_init(uid: bytes, rank: int, nranks: int) -> int:
     buf = ctypes.create_string_buffer(bytes(uid), 128)
     _check(_lib.fgf_nccl_comm_init(ctypes.byref(comm), buf, rank, nranks), "fgf_nccl_comm_init")
     return comm.value
+
+
+def fgf_nccl_check(comm) -> int:
+    return _lib.fgf_nccl_check(comm)
 
 
 def fgf_nccl_comm_destroy(comm) -> None:

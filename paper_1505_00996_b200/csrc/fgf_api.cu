@@ -14,6 +14,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost ~nothing without a tool
+
 #include "../../include/fgf.h"
 #include "fgf_kernels.cuh"
 #include "fgf_lowres.cuh"
@@ -56,11 +58,18 @@ struct Profiler {
 };
 Profiler g_prof;
 
+const char* const kKindName[NKIND] = {"fgf K0 subsample", "fgf K1 statistics+coefficients",
+                                      "fgf K3 box of a,b", "fgf K4 upsample+output",
+                                      "fgf K13 fused low-res chain"};
+
+// Around every launch: an NVTX range named after the kernel (timeline tools: nsys, ncu
+// --nvtx) and, when fgf_profile_enable(1) is on, a CUDA-event pair on the launching stream.
 struct ProfScope {
     cudaStream_t st;
     int kind;
     cudaEvent_t a = nullptr;
     ProfScope(int k, cudaStream_t s) : st(s), kind(k) {
+        nvtxRangePushA(kKindName[k]);
         if (g_prof.on) {
             a = g_prof.get();
             cudaEventRecord(a, st);
@@ -72,6 +81,7 @@ struct ProfScope {
             cudaEventRecord(b, st);
             g_prof.recs.push_back({kind, a, b});
         }
+        nvtxRangePop();
     }
 };
 
@@ -220,7 +230,18 @@ void set_smem(K kernel, size_t bytes) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-int last_error() { return cudaGetLastError() == cudaSuccess ? FGF_OK : FGF_ERR_CUDA; }
+// FGF_DEBUG_SYNC=1: synchronise after every launch so that an asynchronous fault is reported
+// by the call (and the kernel) that caused it, not at the caller's next synchronisation.
+bool debug_sync() {
+    const char* e = getenv("FGF_DEBUG_SYNC");   // read per launch: a few per call
+    return e && atoi(e) != 0;
+}
+
+int last_error() {
+    if (cudaGetLastError() != cudaSuccess) return FGF_ERR_CUDA;
+    if (debug_sync() && cudaDeviceSynchronize() != cudaSuccess) return FGF_ERR_CUDA;
+    return FGF_OK;
+}
 
 // K0: step 1 into compact fp32 low-res planes (s = 1 nearest: a conversion to fp32).
 template <typename E>
@@ -914,6 +935,15 @@ int fgf_nccl_comm_init(void** comm_out, const void* id, int rank, int nranks) {
     if (n->commInitRank(&c, nranks, uid, rank) != ncclSuccess) return FGF_ERR_NCCL;
     *comm_out = c;
     return FGF_OK;
+}
+
+int fgf_nccl_check(void* comm) {
+    if (!comm) return FGF_ERR_NULL;
+    const Nccl* n = nccl();
+    if (!n || !n->commGetAsyncError) return FGF_ERR_NCCL;
+    ncclResult_t async = ncclSuccess;
+    if (n->commGetAsyncError(static_cast<ncclComm_t>(comm), &async) != ncclSuccess) return FGF_ERR_NCCL;
+    return async == ncclSuccess || async == ncclInProgress ? FGF_OK : FGF_ERR_NCCL;
 }
 
 int fgf_nccl_comm_destroy(void* comm) {

@@ -40,6 +40,7 @@ struct Nccl {
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclGroupStart) groupStart = nullptr;
     decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclCommGetAsyncError) commGetAsyncError = nullptr;   // optional
 };
 std::mutex g_nccl_mu;
 Nccl g_nccl;
@@ -57,6 +58,8 @@ const Nccl* nccl() {
             g_nccl.recv = (decltype(g_nccl.recv))dlsym(h, "ncclRecv");
             g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
             g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
+            g_nccl.commGetAsyncError =
+                (decltype(g_nccl.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
             g_nccl.ok = g_nccl.getUniqueId && g_nccl.commInitRank && g_nccl.commDestroy &&
                         g_nccl.send && g_nccl.recv && g_nccl.groupStart && g_nccl.groupEnd;
         }

@@ -123,6 +123,7 @@ def test_c_band_single_rank_with_nccl_communicator():
                                torch.cuda.current_stream())
         torch.cuda.synchronize()
         assert float((q2 - q).abs().max()) < 1e-5
+        assert fgf.fgf_nccl_check(comm) == fgf.FGF_OK
     finally:
         fgf.fgf_nccl_comm_destroy(comm)
 

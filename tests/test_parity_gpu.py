@@ -255,3 +255,13 @@ def test_multi_chunk_pipeline_equals_single_chunk(monkeypatch):
         q2 = gpu_filter(I, p, **prm)
         torch.cuda.synchronize()
         assert torch.equal(q1, q2), cfg
+
+
+def test_debug_sync_mode(monkeypatch):
+    """FGF_DEBUG_SYNC=1 (synchronise after every launch) changes nothing in the results."""
+    I, p = synth.make_batch(1, "cuda", batch=2, H=270, W=480)
+    prm = synth.params(1)
+    q1 = gpu_filter(I, p, **prm)
+    monkeypatch.setenv("FGF_DEBUG_SYNC", "1")
+    q2 = gpu_filter(I, p, **prm)
+    assert torch.equal(q1, q2)
