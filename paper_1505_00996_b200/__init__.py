@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfgf.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("FGF_LIB_NAME", "libfgf.so"))   # (A/B builds)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
