@@ -3,18 +3,25 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # NCCL headers only (the library is dlopen-ed at run time by the band path)
 NCCL_INC ?= $(firstword $(wildcard /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include) /usr/include)
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -I$(NCCL_INC) --split-compile=0
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v -I$(NCCL_INC)
 PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
-SRCS := $(PKG)/csrc/fgf_api.cu
+# one translation unit per kernel family, compiled in parallel (make -j), each in a single
+# ptxas pass: nvcc --split-compile made register allocation depend on the split count
+TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_lowres
+OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
 ORACLE := oracle/libfgf_oracle.so
 
 all: $(LIB) $(ORACLE)
 
-$(LIB): $(SRCS) $(HDRS)
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -ldl 2> build/ptxas.log || (cat build/ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
+	@cat $(patsubst %,build/%.ptxas.log,$(TUS)) > build/ptxas.log
 
 $(ORACLE): oracle/fgf_oracle.c
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC -o $@ $< -lm

@@ -4,106 +4,16 @@
 // (low-res dims, r', strip and tile geometry, chunking of the batch so that each chunk's
 // low-res workspace and the sample rows of I stay resident in the 126 MB L2), and the
 // kernel launches of Alg. 2 on the caller's stream.
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdint>
-#include <cstdlib>
-#include <cstring>
 #include <mutex>
-#include <vector>
 
-#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost ~nothing without a tool
-
-#include "../../include/fgf.h"
-#include "fgf_kernels.cuh"
-#include "fgf_lowres.cuh"
+#include "fgf_host.cuh"
 
 namespace fgf {
-namespace {
 
 thread_local int g_last_launches = 0;
-
-constexpr size_t kAlign = 256;
-constexpr size_t kChunkTargetBytes = 8ull << 30;  // low-res workspace bytes per pipeline slot
-
-// ---- optional per-launch event timing (fgf_profile_*)
-enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, KIND_LOWRES = 4, NKIND = 5 };
-struct ProfRec {
-    int kind;
-    cudaEvent_t a, b;
-};
-struct Profiler {
-    bool on = false;
-    std::vector<ProfRec> recs;
-    std::vector<cudaEvent_t> pool;
-    cudaEvent_t get() {
-        if (!pool.empty()) {
-            cudaEvent_t e = pool.back();
-            pool.pop_back();
-            return e;
-        }
-        cudaEvent_t e = nullptr;
-        cudaEventCreate(&e);
-        return e;
-    }
-    void clear() {
-        for (auto& r : recs) {
-            pool.push_back(r.a);
-            pool.push_back(r.b);
-        }
-        recs.clear();
-    }
-};
 Profiler g_prof;
 
-const char* const kKindName[NKIND] = {"fgf K0 subsample", "fgf K1 statistics+coefficients",
-                                      "fgf K3 box of a,b", "fgf K4 upsample+output",
-                                      "fgf K13 fused low-res chain"};
-
-// Around every launch: an NVTX range named after the kernel (timeline tools: nsys, ncu
-// --nvtx) and, when fgf_profile_enable(1) is on, a CUDA-event pair on the launching stream.
-struct ProfScope {
-    cudaStream_t st;
-    int kind;
-    cudaEvent_t a = nullptr;
-    ProfScope(int k, cudaStream_t s) : st(s), kind(k) {
-        nvtxRangePushA(kKindName[k]);
-        if (g_prof.on) {
-            a = g_prof.get();
-            cudaEventRecord(a, st);
-        }
-    }
-    ~ProfScope() {
-        if (a) {
-            cudaEvent_t b = g_prof.get();
-            cudaEventRecord(b, st);
-            g_prof.recs.push_back({kind, a, b});
-        }
-        nvtxRangePop();
-    }
-};
-
-size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-
-struct Plan {
-    int batch, H, W, CI, CP, r, s, sub;
-    double eps;
-    float k1 = 1.0f, k0 = 0.0f;   // mean-map fold (detail enhancement), identity by default
-    int dtype = FGF_F32;          // element type of I, p, q (FGF_F32 / FGF_F16 / FGF_BF16)
-    int esize = 4;                // its bytes
-    int h, w, R, NC;
-    size_t N, n;
-    int chunk;
-    // strip box engine
-    int nt, TW, strips;
-    // output kernel
-    int TR;
-    // workspace carve-up per pipeline slot (bytes)
-    size_t ws_planes, ws_coef, ws_mean, ws_slot;
-    int nslots;
-};
+namespace {
 
 int lowres_dim(int D, int s) { return (D + s - 1) / s; }
 
@@ -220,406 +130,6 @@ int check_pointers(const void* I, const void* p, const void* q, const Plan& P, b
         if (is_device_ptr(I) || is_device_ptr(p) || is_device_ptr(q)) return FGF_ERR_DEVICE;
     }
     return FGF_OK;
-}
-
-// --------------------------------------------------------------------- launch helpers
-
-template <typename K>
-void set_smem(K kernel, size_t bytes) {
-    if (bytes > 48 * 1024)
-        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
-
-// FGF_DEBUG_SYNC=1: synchronise after every launch so that an asynchronous fault is reported
-// by the call (and the kernel) that caused it, not at the caller's next synchronisation.
-bool debug_sync() {
-    const char* e = getenv("FGF_DEBUG_SYNC");   // read per launch: a few per call
-    return e && atoi(e) != 0;
-}
-
-int last_error() {
-    if (cudaGetLastError() != cudaSuccess) return FGF_ERR_CUDA;
-    if (debug_sync() && cudaDeviceSynchronize() != cudaSuccess) return FGF_ERR_CUDA;
-    return FGF_OK;
-}
-
-// K0: step 1 into compact fp32 low-res planes (s = 1 nearest: a conversion to fp32).
-template <typename E>
-int launch_subsample_e(const void* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
-    SubParams sp{src, dst, P.H, P.W, P.h, P.w, P.s, 8};
-    dim3 grid((P.w + 255) / 256, (P.h + sp.rows_per_cta - 1) / sp.rows_per_cta, planes);
-    ProfScope ps(KIND_SUB, st);
-    const bool vec4 = P.s == 4 && (reinterpret_cast<uintptr_t>(src) & (4 * sizeof(E) - 1)) == 0 &&
-                      (P.W % 4) == 0;
-    if (P.sub == FGF_SUB_NEAREST)
-        subsample_nearest_kernel<8, E><<<grid, 256, 0, st>>>(sp);
-    else if (vec4)
-        subsample_block_kernel<true, E><<<grid, 256, 0, st>>>(sp);
-    else
-        subsample_block_kernel<false, E><<<grid, 256, 0, st>>>(sp);
-    ++g_last_launches;
-    return last_error();
-}
-
-int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cudaStream_t st) {
-    switch (P.dtype) {
-        case FGF_F16: return launch_subsample_e<__half>(src, dst, planes, P, st);
-        case FGF_BF16: return launch_subsample_e<__nv_bfloat16>(src, dst, planes, P, st);
-    }
-    return launch_subsample_e<float>(src, dst, planes, P, st);
-}
-
-// measured (config 4): prefix sums win at r' = 32 (s = 1: 22.8 -> 15.6 ms per 32 images), lose at
-// r' = 15, 16 (configs 2, 1 s=1, 4 s=2)
-constexpr int kHpreR = 24;
-
-template <int MODE, int CI, int CP, int NT, int G_ = 0>
-int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream_t st) {
-    using C = StripConfig<MODE, CI, CP, NT, G_>;
-    StripParams sp = sp0;
-    sp.VP = NT + 2 * P.R + C::K + 1;
-    const size_t smem = C::smem(sp.VP);
-    if (smem > 227 * 1024) return FGF_ERR_UNSUPPORTED;
-    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 4G (and 2R) and 64.
-    const long long want = 4LL * 148;
-    const long long strips_imgs = (long long)P.strips * images;
-    long long th = (P.h * strips_imgs + want - 1) / want;
-    th = std::max<long long>(th, std::max(4 * C::G, 2 * P.R));
-    int TH = (int)std::min<long long>(64, th);
-    TH = (TH + C::G - 1) / C::G * C::G;
-    sp.TH = TH;
-    sp.TW = P.TW;
-    dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
-    // wide windows: prefix-sum horizontal phase (restart-free); measured threshold below
-    int hpre_r = kHpreR;
-    if (const char* e = getenv("FGF_HPRE_R")) hpre_r = atoi(e);
-    // (instantiated for gray 1/1 and colour 3/1, 3/3 -- the channel layouts BASELINE.json uses)
-    constexpr bool HP_OK = (CI == 1 && CP == 1) || (CI == 3 && (CP == 1 || CP == 3));
-    auto kern = box_strip_kernel<MODE, CI, CP, NT, G_, 0, false>;
-    if constexpr (HP_OK) {
-        if (P.R >= hpre_r) kern = box_strip_kernel<MODE, CI, CP, NT, G_, 0, true>;
-    }
-    set_smem(kern, smem);
-    ProfScope ps(MODE == MODE_STATS ? KIND_STATS : KIND_MEAN, st);
-    kern<<<grid, NT, smem, st>>>(sp);
-    ++g_last_launches;
-    return last_error();
-}
-
-// The default G assumes the worst-case padded row (r' up to the strip limit); colour
-// statistics (13 / 21 fp64 maps) then get G = 1 or 2.  With r' <= 16 the real rows are short
-// enough for more rows per batch (fewer barriers, longer runs).
-template <int MODE, int CI, int CP, int NT>
-int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
-    constexpr bool MEANLIKE = MODE == MODE_MEAN;
-    if (CI == 3 && NT == 256 && P.R <= 16 && getenv("FGF_STRIP_WORSTG") == nullptr) {
-        constexpr int GC = (MEANLIKE || CP == 1) ? 4 : 2;
-        const int rc = launch_strip_g<MODE, CI, CP, NT, GC>(sp, images, P, st);
-        if (rc != FGF_ERR_UNSUPPORTED) return rc;
-    }
-    // gray box of a, b at 12 <= r' < 24: 8 rows per batch (measured: config 4 s=2 K3 2.44 -> 2.27 ms
-    // per 64 images; the statistics kernel was slower with 8)
-    if (MEANLIKE && CI == 1 && CP == 1 && NT == 256 && P.R >= 12 && P.R < kHpreR &&
-        getenv("FGF_STRIP_WORSTG") == nullptr) {
-        const int rc = launch_strip_g<MODE, CI, CP, NT, 8>(sp, images, P, st);
-        if (rc != FGF_ERR_UNSUPPORTED) return rc;
-    }
-    return launch_strip_g<MODE, CI, CP, NT>(sp, images, P, st);
-}
-
-template <int MODE, int CI, int CP>
-int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
-    if (P.nt == 256) return launch_strip_t<MODE, CI, CP, 256>(sp, images, P, st);
-    return launch_strip_t<MODE, CI, CP, 512>(sp, images, P, st);
-}
-
-template <int MODE>
-int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
-    switch (P.CI * 10 + P.CP) {
-        case 11: return launch_strip_nt<MODE, 1, 1>(sp, images, P, st);
-        case 12: return launch_strip_nt<MODE, 1, 2>(sp, images, P, st);
-        case 13: return launch_strip_nt<MODE, 1, 3>(sp, images, P, st);
-        case 14: return launch_strip_nt<MODE, 1, 4>(sp, images, P, st);
-        case 31: return launch_strip_nt<MODE, 3, 1>(sp, images, P, st);
-        case 32: return launch_strip_nt<MODE, 3, 2>(sp, images, P, st);
-        case 33: return launch_strip_nt<MODE, 3, 3>(sp, images, P, st);
-        case 34: return launch_strip_nt<MODE, 3, 4>(sp, images, P, st);
-    }
-    return FGF_ERR_SHAPE;
-}
-
-// Largest low-res rectangle (rows x cols) a CTA of TR rows and `cols` pixels touches (R5).
-int lowres_span(int T, int n_dst, int n_src) {
-    auto lo = [&](int d) {
-        long long num = (long long)(2 * d + 1) * n_src - n_dst;
-        if (num <= 0) return 0;
-        long long q = num / (2LL * n_dst);
-        return (int)std::min<long long>(q, n_src - 1);
-    };
-    int best = 1;
-    for (int d0 = 0; d0 < n_dst; d0 += T) {
-        int dl = std::min(n_dst, d0 + T) - 1;
-        best = std::max(best, std::min(lo(dl) + 1, n_src - 1) - lo(d0) + 1);
-    }
-    return best;
-}
-
-constexpr size_t kOutSmemBudget = 44 * 1024;
-
-template <int CI, int CP, int PX, typename E = float>
-int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream_t st) {
-    constexpr int NC = (CI + 1) * CP;
-    OutParams op = op0;
-    const bool s1 = op.hg == op.Hg && P.w == P.W;
-    size_t smem = 0;
-    if (s1) {
-        op.TR = 64;
-    } else {
-        const int ncl = lowres_span(256 * PX, P.W, P.w);
-        op.TR = 8;
-        for (int tr = kMaxTR; tr >= 8; tr /= 2) {
-            const size_t b = (size_t)lowres_span(tr, op.Hg, op.hg) * NC * ncl * sizeof(float);
-            if (b <= kOutSmemBudget) { op.TR = tr; break; }
-        }
-        // small launches (single images): shorter bands until ~2 waves of 4 CTAs per SM exist
-        const long long ncb = (P.W + 256 * PX - 1) / (256 * PX);
-        while (op.TR > 8 && ncb * ((P.H + op.TR - 1) / op.TR) * images < 2LL * 4 * 148) op.TR /= 2;
-        smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
-        if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
-        // optional floor on the dynamic smem: caps K4 CTAs/SM so the low-res stream's CTAs
-        // can be co-resident (experiment knob)
-        if (const char* e = getenv("FGF_K4_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
-    }
-    dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
-    if constexpr (PX * sizeof(E) >= 4) {   // cp.async moves 4, 8 or 16 bytes
-        if (!s1 && getenv("FGF_NO_ASYNC") == nullptr) {
-            // cp.async ring variant: prefetch held in shared memory, not registers
-            const size_t asm_ = smem + AsyncCfg<CI, CP, PX, E>::RING_BYTES;
-            if (asm_ <= 200 * 1024) {
-                auto kern = output_async_kernel<CI, CP, PX, E>;
-                set_smem(kern, asm_);
-                ProfScope ps(KIND_OUT, st);
-                kern<<<grid, 256, asm_, st>>>(op);
-                ++g_last_launches;
-                return last_error();
-            }
-        }
-    }
-    ProfScope ps(KIND_OUT, st);
-    if (s1) {
-        output_kernel<CI, CP, PX, true, 0, 0, 0, E><<<grid, 256, 0, st>>>(op);
-    } else {
-        auto kern = output_kernel<CI, CP, PX, false, 0, 0, 0, E>;
-        set_smem(kern, smem);
-        kern<<<grid, 256, smem, st>>>(op);
-    }
-    ++g_last_launches;
-    return last_error();
-}
-
-// Pixels per thread: as wide as alignment allows while the coefficient registers fit.
-template <int CI, int CP, typename E = float>
-int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t st) {
-    constexpr int NC = (CI + 1) * CP;
-    constexpr uintptr_t ES = sizeof(E);
-    const uintptr_t ai = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
-    const uintptr_t am = reinterpret_cast<uintptr_t>(op.M);
-    if (NC <= 2 && P.W % 4 == 0 && (ai & (4 * ES - 1)) == 0 && (am & 15u) == 0)
-        return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1), E>(op, images, P, st);
-    if (NC <= 4 && P.W % 2 == 0 && (ai & (2 * ES - 1)) == 0 && (am & 7u) == 0)
-        return launch_output_px<CI, CP, (NC <= 4 ? 2 : 1), E>(op, images, P, st);
-    return launch_output_px<CI, CP, 1, E>(op, images, P, st);
-}
-
-// Row band of a taller image: I/q hold rows [Yoff, Yoff + P.H) of an image of height Hg;
-// the maps buffer holds low-res rows [yoff, yoff + hm) of a low-res image of height hg.
-struct Band {
-    int Hg, hg, Yoff, yoff, hm;
-};
-
-int launch_output(const void* I, const float* M, void* q, int images, const Plan& P,
-                  cudaStream_t st, const Band* band = nullptr) {
-    const Band b = band ? *band : Band{P.H, P.h, 0, 0, P.h};
-    OutParams op{I, M, q, P.H, P.W, b.hm, P.w, b.Hg, b.hg, b.Yoff, b.yoff, P.TR};
-    if (P.dtype != FGF_F32) {
-        // reduced-precision I/O: gray -> gray, colour -> colour, colour guide -> one channel
-        const int key = P.CI * 10 + P.CP;
-        if (P.dtype == FGF_F16) {
-            if (key == 11) return launch_output_t<1, 1, __half>(op, images, P, st);
-            if (key == 31) return launch_output_t<3, 1, __half>(op, images, P, st);
-            if (key == 33) return launch_output_t<3, 3, __half>(op, images, P, st);
-        } else {
-            if (key == 11) return launch_output_t<1, 1, __nv_bfloat16>(op, images, P, st);
-            if (key == 31) return launch_output_t<3, 1, __nv_bfloat16>(op, images, P, st);
-            if (key == 33) return launch_output_t<3, 3, __nv_bfloat16>(op, images, P, st);
-        }
-        return FGF_ERR_UNSUPPORTED;
-    }
-    switch (P.CI * 10 + P.CP) {
-        case 11: return launch_output_t<1, 1>(op, images, P, st);
-        case 12: return launch_output_t<1, 2>(op, images, P, st);
-        case 13: return launch_output_t<1, 3>(op, images, P, st);
-        case 14: return launch_output_t<1, 4>(op, images, P, st);
-        case 31: return launch_output_t<3, 1>(op, images, P, st);
-        case 32: return launch_output_t<3, 2>(op, images, P, st);
-        case 33: return launch_output_t<3, 3>(op, images, P, st);
-        case 34: return launch_output_t<3, 4>(op, images, P, st);
-    }
-    return FGF_ERR_SHAPE;
-}
-
-// ---- K13: fused low-res chain (gray guidance), fgf_lowres.cuh
-constexpr size_t kLrSmemMax = 227 * 1024;
-
-// Kernel variants (rows per batch G, horizontal run lengths KA / KB); the first that fits
-// is used unless FGF_LR_V selects one (development sweep).
-//   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
-//   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
-// (measured on config 4, profiles/round1/k13_variants.txt: G 8 / K 17 and G 6 / K 13 without
-// the ring, and a lane-pair split of the runs, were slower)
-// (also slower: K 5/17 and K 7/17, rebalancing the two concurrent horizontal phases)
-constexpr int kLrNumVariants = 4;
-
-// Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
-struct LrGeom {
-    int NT = 0, TW = 0, strips = 0, TH = 0, V = -1;
-    size_t smem = 0;
-};
-
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512>
-bool lowres_fits(LrGeom& g, int R, int v) {
-    using C = LowresCfg<CP, G, KA, KB, RING>;
-    const auto L = C::layout(g.NT, g.TW, g.TH, R);
-    // both horizontal phases run concurrently on disjoint threads
-    if (L.total > kLrSmemMax || G * (L.nrA + L.nrB) > g.NT || g.NT > MAXT) return false;
-    g.smem = L.total;
-    g.V = v;
-    return true;
-}
-
-template <int CP>
-bool lowres_fits_v(LrGeom& g, int R, int v) {
-    if (CP > 1 && v != 0) return false;          // one variant for several p channels
-    switch (v) {
-        case 0: return lowres_fits<CP, 4, 9, 9>(g, R, v);
-        case 1: return lowres_fits<CP, 8, 9, 9>(g, R, v);
-        case 2: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
-        case 3: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
-    }
-    return false;
-}
-
-template <int CP>
-bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
-    // Target ~160 threads (5 warps) per CTA: three CTAs per SM, halo overhead (TW + 4R) / TW.
-    int want_nt = 160;
-    if (const char* e = getenv("FGF_LR_NT")) want_nt = atoi(e);
-    LrGeom best;
-    for (int ns = 1; ns <= w; ++ns) {
-        const int TW = (w + ns - 1) / ns;
-        if ((ns - 1) * TW >= w) continue;
-        const int NT = (TW + 4 * R + 31) / 32 * 32;
-        if (NT > 512) continue;
-        const long long tot = (long long)ns * NT, btot = (long long)best.strips * best.NT;
-        // closest to the target size; on ties the fewer total threads
-        const bool better = best.NT == 0 || std::abs(NT - want_nt) < std::abs(best.NT - want_nt) ||
-                            (std::abs(NT - want_nt) == std::abs(best.NT - want_nt) && tot < btot);
-        if (better) { best.NT = NT; best.TW = TW; best.strips = ns; }
-        if (NT < 64) break;
-    }
-    if (best.NT == 0) return false;
-    // Segment height: long segments amortise the 2r'+1 warm-up rows (up to 256 rows); small
-    // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
-    const long long cols = (long long)best.strips * images;
-    long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
-    th = std::min<long long>(256, std::max<long long>(th, std::max(8, 2 * R + 2)));
-    if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
-    best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
-    if (const char* e = getenv("FGF_LR_V")) {
-        if (lowres_fits_v<CP>(best, R, atoi(e))) { g = best; return true; }
-        return false;
-    }
-    static const int order[kLrNumVariants] = {3, 0, 1, 2};   // measured: 3 fastest (config 4)
-    for (int v : order)
-        if (lowres_fits_v<CP>(best, R, v)) { g = best; return true; }
-    return false;
-}
-
-template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
-          typename E = float>
-int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
-                         cudaStream_t st) {
-    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, E>;
-    LowresParams lpl = lp;
-    lpl.L = LowresCfg<CP, G, KA, KB, RING>::layout(g.NT, lp.TW, lp.TH, P.R);
-    size_t smem = g.smem;
-    // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
-    // previous chunk can be co-resident (overlap experiment knob)
-    if (const char* e = getenv("FGF_LR_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
-    set_smem(kern, smem);
-    dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
-    ProfScope ps(KIND_LOWRES, st);
-    kern<<<grid, g.NT, smem, st>>>(lpl);
-    ++g_last_launches;
-    return last_error();
-}
-
-template <int CP>
-int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cudaStream_t st,
-                         bool dry) {
-    LrGeom g;
-    if (!lowres_geom<CP>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
-    if (dry) return FGF_OK;
-    LowresParams lp = lp0;
-    lp.TW = g.TW;
-    lp.TH = g.TH;
-    if (CP > 1) return launch_lowres_gray_g<CP, 4, 9, 9>(lp, g, images, P, st);
-    if (P.dtype != FGF_F32) {   // reduced-precision inputs: the default variant and the wide one
-        const bool h = P.dtype == FGF_F16;
-        if (g.V == 3)
-            return h ? launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, __half>(lp, g, images, P, st)
-                     : launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3, __nv_bfloat16>(lp, g, images, P, st);
-        if (g.V == 0)
-            return h ? launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __half>(lp, g, images, P, st)
-                     : launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __nv_bfloat16>(lp, g, images, P, st);
-        return FGF_ERR_UNSUPPORTED;
-    }
-    switch (g.V) {
-        case 0: return launch_lowres_gray_g<1, 4, 9, 9>(lp, g, images, P, st);
-        case 1: return launch_lowres_gray_g<1, 8, 9, 9>(lp, g, images, P, st);
-        case 2: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 4>(lp, g, images, P, st);
-        case 3: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 3>(lp, g, images, P, st);
-    }
-    return FGF_ERR_UNSUPPORTED;
-}
-
-// dry = true: only report whether K13 serves this plan (FGF_OK) or not.
-int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaStream_t st,
-                       bool dry = false) {
-    if (P.CI != 1) return FGF_ERR_UNSUPPORTED;
-    // K13's horizontal restarts cost (2r' + 1) / K per output and its a, b ring 2r' + G + 1
-    // rows: measured faster than the strip engine at r' = 4 and 8, slower at r' = 16 and 32
-    // (config 4 at s = 8, 4, 2, 1), so wide windows take the strip engine.
-    int rmax = 12;
-    if (const char* e = getenv("FGF_LR_RMAX")) rmax = atoi(e);
-    if (P.R > rmax) return FGF_ERR_UNSUPPORTED;
-    if (const char* e = getenv("FGF_LOWRES")) {
-        if (strcmp(e, "strip") == 0) return FGF_ERR_UNSUPPORTED;
-    }
-    if (P.dtype != FGF_F32 && P.CP != 1) return FGF_ERR_UNSUPPORTED;
-    switch (P.CP) {
-        case 1: {
-            if (P.dtype != FGF_F32 && dry) {
-                // only variants 3 and 0 exist for reduced-precision inputs
-                LrGeom g;
-                if (!lowres_geom<1>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
-                return (g.V == 3 || g.V == 0) ? FGF_OK : FGF_ERR_UNSUPPORTED;
-            }
-            return launch_lowres_gray_t<1>(lp, images, P, st, dry);
-        }
-        case 2: return launch_lowres_gray_t<2>(lp, images, P, st, dry);
-    }
-    return FGF_ERR_UNSUPPORTED;
 }
 
 // When K13 serves a plan it needs no a, b maps, and no compact planes unless it subsamples by

@@ -573,6 +573,59 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
     }
 }
 
+// cp.async helpers (K4 staging and rings)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_px(void* dst, const void* src) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    if (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else if (BYTES == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+
+// Stage the low-res rectangle rows [ylo, ylo + nrl) x columns [x4, x4 + ncs) of the NC maps
+// into Ms[(row * NC + map) * ncs + col] with cp.async (all copies in flight at once, no
+// register round trip; the caller commits and waits).  x4 is 4-aligned and ncs a multiple of
+// 4: with w % 4 == 0 and a 16-byte aligned maps pointer every line moves in 16-byte copies,
+// otherwise in 4-byte copies clipped at the image edge.  One warp per line.
+template <int NC, int NT>
+__device__ __forceinline__ void stage_rect(float* Ms, const float* Mb, size_t n, int w, int ylo,
+                                           int nrl, int x4, int ncs, int tid) {
+    const int lane = tid & 31;
+    if ((w & 3) == 0 && (reinterpret_cast<uintptr_t>(Mb) & 15u) == 0) {
+        const int nq = ncs >> 2;
+        for (int rm = tid >> 5; rm < nrl * NC; rm += NT / 32) {
+            const int rr = rm / NC, m = rm - rr * NC;
+            const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + x4;
+            float* d = Ms + (size_t)rm * ncs;
+            for (int c = lane; c < nq; c += 32) cp_async_px<16>(d + 4 * c, src + 4 * c);
+        }
+    } else {
+        const int cols = min(ncs, w - x4);
+        for (int rm = tid >> 5; rm < nrl * NC; rm += NT / 32) {
+            const int rr = rm / NC, m = rm - rr * NC;
+            const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + x4;
+            float* d = Ms + (size_t)rm * ncs;
+            for (int c = lane; c < cols; c += 32) cp_async_px<4>(d + c, src + c);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ K4: upsample + output
 
 struct OutParams {
@@ -719,20 +772,17 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
         src_coord(X0, w, W, xlo, xd, fd);
         src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
         const int nrl = yhi - ylo + 1;
-        ncl = xhi - xlo + 1;
-        // one warp per (row, map) line of the rectangle, lanes along the columns
-        for (int rm = threadIdx.x >> 5; rm < nrl * NC; rm += 8) {
-            const int rr = rm / NC, m = rm - rr * NC;
-            const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo;
-            float* d = Ms + (size_t)rm * ncl;
-            for (int xx = threadIdx.x & 31; xx < ncl; xx += 32) d[xx] = __ldg(src + xx);
-        }
+        xlo &= ~3;
+        ncl = (xhi + 1 - xlo + 3) & ~3;   // row stride of the staged rectangle
+        stage_rect<NC, 256>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, threadIdx.x);
+        cp_async_commit();
 #pragma unroll
         for (int i = 0; i < PX; ++i) {
             src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
             oa[i] -= xlo;      // local columns in the staged rectangle
             ob[i] -= xlo;
         }
+        cp_async_wait<0>();
         __syncthreads();
     }
 
@@ -833,29 +883,6 @@ __global__ void __launch_bounds__(256, (MINB_ ? MINB_ : OutCfg<CI, CP, PX>::MINB
 // waits with cp.async.wait_group(U-1) before consuming row t.  With ~60 registers the SM
 // keeps 4 CTAs resident and U = 8 rows x 16 B x 1024 threads = 128 KB of I in flight.
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <int BYTES>
-__device__ __forceinline__ void cp_async_px(void* dst, const void* src) {
-    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
-    if (BYTES == 16)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
-    else if (BYTES == 8)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 template <int CI, int CP, int PX, typename E = float>
 struct AsyncCfg {
     static constexpr int NC = (CI + 1) * CP;
@@ -891,16 +918,6 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
     E* qp = static_cast<E*>(P.q) + (size_t)img * CP * N + (size_t)Y0 * W + X;
     const float* Mb = P.M + (size_t)img * NC * n;
 
-    // Issue the first U rows (one commit group per row, empty groups keep the count uniform).
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        if (act && u < nrows)
-#pragma unroll
-            for (int j = 0; j < CI; ++j)
-                cp_async_px<V::BYTES>(&ring[(u * CI + j) * 256 + tid], Ip + j * N + (size_t)u * W);
-        cp_async_commit();
-    }
-
     // Row table and staged low-res rectangle (as in output_kernel).
     for (int t = tid; t < nrows; t += 256) {
         int ya, yb;
@@ -918,12 +935,18 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
     yhi -= P.yoff;
     src_coord(X0, w, W, xlo, xd, fd);
     src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
-    const int nrl = yhi - ylo + 1, ncl = xhi - xlo + 1;
-    for (int rm = tid >> 5; rm < nrl * NC; rm += 8) {
-        const int rr = rm / NC, m = rm - rr * NC;
-        const float* src = Mb + (size_t)m * n + (size_t)(ylo + rr) * w + xlo;
-        float* d = Ms + (size_t)rm * ncl;
-        for (int xx = tid & 31; xx < ncl; xx += 32) d[xx] = __ldg(src + xx);
+    xlo &= ~3;
+    const int nrl = yhi - ylo + 1, ncl = (xhi + 1 - xlo + 3) & ~3;
+    stage_rect<NC, 256>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, tid);   // commit group 0
+    cp_async_commit();
+    // Issue the first U rows (one commit group per row, empty groups keep the count uniform).
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (act && u < nrows)
+#pragma unroll
+            for (int j = 0; j < CI; ++j)
+                cp_async_px<V::BYTES>(&ring[(u * CI + j) * 256 + tid], Ip + j * N + (size_t)u * W);
+        cp_async_commit();
     }
     int oa[PX], ob[PX];
     float fx[PX];
@@ -933,6 +956,7 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
         oa[i] -= xlo;
         ob[i] -= xlo;
     }
+    cp_async_wait<U>();                             // the rectangle (group 0) has landed
     __syncthreads();
 
     int cy = -2, cy1 = -2;
@@ -999,6 +1023,195 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
         cp_async_commit();
         qp += W;
         Ipf += W;
+    }
+    cp_async_wait<0>();
+}
+
+// ------------------------------------------------------------------ K4, channel split
+//
+// Colour guidance with several p channels (NC = 4 C_p maps).  One thread per (output channel
+// c, 4-pixel group) keeps the interpolated rows of only its channel's C_I + 1 maps and
+// writes q_c, instead of one thread per pixel carrying all NC maps.  The guidance rows stream
+// through ONE shared ring per CTA, each float4 loaded once by cp.async (64 * C_I loads per
+// row spread over the CTA); completion is tracked per slot by an mbarrier that every thread
+// arrives on when its copies land ("full"), and slot reuse by a second mbarrier every thread
+// arrives on after reading the row ("empty"); a slot is refilled one row late so the empty
+// wait rarely blocks.  CTA: 64 groups x C_p channels, 256 pixels wide.
+template <int CI, int CP>
+struct SplitCfg {
+    static constexpr int NC = (CI + 1) * CP;
+    static constexpr int PX = 4;
+    static constexpr int NT = 64 * CP;
+    static constexpr int U = 8;
+    static constexpr size_t RING_BYTES = (size_t)U * CI * 64 * PX * 4;   // + 2U mbarriers
+    static constexpr size_t BAR_BYTES = 2 * U * 8;
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init_cta(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// arrive once this thread's earlier cp.async copies have landed (count not incremented)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITP_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITP_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int CI, int CP>
+__global__ void __launch_bounds__(SplitCfg<CI, CP>::NT) output_split_kernel(OutParams P) {
+    using C = SplitCfg<CI, CP>;
+    constexpr int NC = C::NC, PX = C::PX, NT = C::NT, U = C::U, NM = CI + 1;
+    constexpr int LOADS = 64 * CI;                                // float4 per ring row
+    using V = Vec<float, PX>;
+    using VT = typename V::T;
+    __shared__ int s_ya[kMaxTR];
+    __shared__ int s_y1[kMaxTR];
+    __shared__ float s_fy[kMaxTR];
+    extern __shared__ __align__(16) float smx[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smx);            // [U]
+    uint64_t* empty = full + U;                                   // [U]
+    VT* ring = reinterpret_cast<VT*>(smx + C::BAR_BYTES / 4);     // [U][CI][64]
+    float* Ms = smx + (C::BAR_BYTES + C::RING_BYTES) / 4;         // [nrl][NC][ncl]
+    const int H = P.H, W = P.W, h = P.hm, w = P.w;
+    const int tid = threadIdx.x;
+    const int ch = tid >> 6, g = tid & 63;                        // output channel, pixel group
+    const int Y0 = blockIdx.y * P.TR;
+    const int nrows = min(P.TR, H - Y0);
+    const int X0 = blockIdx.x * 64 * PX;
+    const bool act = X0 + g * PX < W;
+    const int X = act ? X0 + g * PX : X0;
+    const int img = blockIdx.z;
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+    const float* Ib = static_cast<const float*>(P.I) + (size_t)img * CI * N + (size_t)Y0 * W + X0;
+    float* qp = static_cast<float*>(P.q) + ((size_t)img * CP + ch) * N + (size_t)Y0 * W + X;
+    const float* Mb = P.M + (size_t)img * NC * n;
+
+    if (tid == 0) {
+        for (int u = 0; u < U; ++u) {
+            mbar_init_cta(&full[u], NT);
+            mbar_init_cta(&empty[u], NT);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // this thread's copies of ring row t: float4 k = tid, tid + NT, ... of [CI][64]
+    auto issue = [&](int t) {
+        if (t < nrows) {
+            const float* rowp = Ib + (size_t)t * W;
+            VT* slot = ring + (size_t)(t & (U - 1)) * LOADS;
+            for (int k = tid; k < LOADS; k += NT) {
+                const int j = k >> 6, gg = k & 63;
+                if (X0 + gg * PX < W) cp_async_px<16>(&slot[k], rowp + (size_t)j * N + gg * PX);
+            }
+        }
+        cp_async_mbar_arrive(&full[t & (U - 1)]);
+    };
+
+    for (int t = tid; t < nrows; t += NT) {
+        int ya, yb;
+        float fy;
+        src_coord(P.Yoff + Y0 + t, P.hg, P.Hg, ya, yb, fy);
+        s_ya[t] = ya - P.yoff;
+        s_y1[t] = yb - P.yoff;
+        s_fy[t] = fy;
+    }
+    int ylo, yd, yhi, xlo, xd, xhi;
+    float fd;
+    src_coord(P.Yoff + Y0, P.hg, P.Hg, ylo, yd, fd);
+    src_coord(P.Yoff + Y0 + nrows - 1, P.hg, P.Hg, yd, yhi, fd);
+    ylo -= P.yoff;
+    yhi -= P.yoff;
+    src_coord(X0, w, W, xlo, xd, fd);
+    src_coord(min(W, X0 + 64 * PX) - 1, w, W, xd, xhi, fd);
+    xlo &= ~3;
+    const int nrl = yhi - ylo + 1, ncl = (xhi + 1 - xlo + 3) & ~3;
+    stage_rect<NC, NT>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, tid);
+    cp_async_commit();                              // the rectangle: the only commit group
+#pragma unroll 1
+    for (int u = 0; u < U; ++u) issue(u);           // ring rows: tracked by the full mbarriers
+    cp_async_wait<0>();
+    int oa[PX], ob[PX];
+    float fx[PX];
+#pragma unroll
+    for (int i = 0; i < PX; ++i) {
+        src_coord(min(X + i, W - 1), w, W, oa[i], ob[i], fx[i]);
+        oa[i] -= xlo;
+        ob[i] -= xlo;
+    }
+    __syncthreads();
+
+    const int mb = ch * NM;                                       // this channel's maps
+    int cy = -2, cy1 = -2;
+    float H0[NM][PX], H1[NM][PX], D[NM][PX];
+    auto hrow = [&](int y, float (&out)[NM][PX]) {
+        const float* mr = Ms + ((size_t)(y - ylo) * NC + mb) * ncl;
+#pragma unroll
+        for (int m = 0; m < NM; ++m)
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                const float va = mr[m * ncl + oa[i]], vb = mr[m * ncl + ob[i]];
+                out[m][i] = fmaf(fx[i], vb - va, va);
+            }
+    };
+    for (int t = 0; t < nrows; ++t) {
+        const int ya = s_ya[t];
+        const float fy = s_fy[t];
+        if (__any_sync(0xffffffffu, ya != cy)) {   // CTA-uniform branch
+            if (ya == cy1) {
+#pragma unroll
+                for (int m = 0; m < NM; ++m)
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) H0[m][i] = H1[m][i];
+            } else {
+                hrow(ya, H0);
+            }
+            cy1 = s_y1[t];
+            hrow(cy1, H1);
+#pragma unroll
+            for (int m = 0; m < NM; ++m)
+#pragma unroll
+                for (int i = 0; i < PX; ++i) D[m][i] = H1[m][i] - H0[m][i];
+            cy = ya;
+        }
+        const int slot = t & (U - 1);
+        mbar_wait_parity(&full[slot], (uint32_t)((t / U) & 1));   // row t landed (all copies)
+        if (act) {
+            const VT* sr = ring + (size_t)slot * LOADS + g;
+            VT iv[CI];
+#pragma unroll
+            for (int j = 0; j < CI; ++j) iv[j] = sr[j * 64];
+            float o[PX];
+#pragma unroll
+            for (int i = 0; i < PX; ++i) {
+                float acc = fmaf(fy, D[CI][i], H0[CI][i]);
+#pragma unroll
+                for (int j = 0; j < CI; ++j)
+                    acc = fmaf(fmaf(fy, D[j][i], H0[j][i]), V::get(iv[j], i), acc);
+                o[i] = acc;
+            }
+            V::st(qp, o);
+        }
+        mbar_arrive_cta(&empty[slot]);
+        // refill the slot read one row ago (everyone is past it by now, so rarely a wait)
+        if (t >= 1 && t - 1 + U < nrows) {
+            const int s1 = (t - 1) & (U - 1);
+            mbar_wait_parity(&empty[s1], (uint32_t)(((t - 1) / U) & 1));
+            issue(t - 1 + U);
+        }
+        qp += W;
     }
     cp_async_wait<0>();
 }

@@ -265,3 +265,23 @@ def test_debug_sync_mode(monkeypatch):
     monkeypatch.setenv("FGF_DEBUG_SYNC", "1")
     q2 = gpu_filter(I, p, **prm)
     assert torch.equal(q1, q2)
+
+
+@pytest.mark.parametrize("CP", [2, 3, 4])
+def test_k4_variants_agree(monkeypatch, CP):
+    """The opt-in K4 variants (channel-split walker with the mbarrier ring, FGF_K4_SPLIT; the
+    register-prefetch walker, FGF_NO_ASYNC) compute the same per-pixel expression in the same
+    order as the default cp.async walker: identical q, and within tolerance of the oracle."""
+    g = torch.Generator().manual_seed(31 + CP)
+    B, H, W = 2, 203, 964                        # ragged rows, W % 4 == 0, several column blocks
+    I = torch.rand((B, 3, H, W), generator=g).cuda()
+    p = torch.rand((B, CP, H, W), generator=g).cuda()
+    q0 = gpu_filter(I, p, 8, 0.01, 4, 1)
+    for knob in ("FGF_K4_SPLIT", "FGF_NO_ASYNC"):
+        monkeypatch.setenv(knob, "1")
+        q1 = gpu_filter(I, p, 8, 0.01, 4, 1)
+        torch.cuda.synchronize()
+        monkeypatch.delenv(knob)
+        assert torch.equal(q0, q1), knob
+    ref = oracle.fast_guided_filter(I[:1].cpu().numpy(), p[:1].cpu().numpy(), 8, 0.01, 4, 1)
+    assert np.abs(q0[:1].double().cpu().numpy() - ref).max() <= 1e-4
