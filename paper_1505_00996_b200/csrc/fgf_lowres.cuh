@@ -38,6 +38,7 @@ namespace fgf {
 // in the parameters.
 struct LowresLayout {
     int NT, NCA, NCS, nrA, nrB, PA, PB, VPA, VPB, RBA, RBI, THA, THB;
+    int RVB, ROS, RAB;     // row pitches (floats) of VsB, Os and the a, b ring slots
     size_t oVsA, oVsB, oInvxA, oInvxB, oInvyA, oInvyB, oABr, oINr, oOs, total;
 };
 
@@ -84,16 +85,26 @@ struct LowresCfg {
         L.RBI = 2 * R + 2;                       // sample rows [ya - R - 1, ya + R]
         L.THA = TH + 2 * R + 2;                  // a, b rows of a segment (1 / count table)
         L.THB = TH;
+        // Row pitches p = q (mod 32) words, q = the runs of a row times the run length: the
+        // run threads of one warp span consecutive rows, and with this pitch lane l of the
+        // warp addresses word 9 l + const (mod 32) -- distinct banks (K odd).
+        auto pitch = [](int base, int runs, int K) {
+            const int want = (runs * K) & 31;
+            return base + ((want - base) & 31);
+        };
+        L.RVB = pitch(NAB * L.VPB, L.nrB, KB);
+        L.ROS = pitch(NAB * L.PB, L.nrB, KB);
+        L.RAB = pitch(NAB * L.PA, L.nrA, KA);
         size_t o = 0;
         L.oVsA = o; o = al16(o + (size_t)G * NMAP * L.VPA * 8);
-        L.oVsB = o; o = al16(o + (size_t)G * NAB * L.VPB * 4);
+        L.oVsB = o; o = al16(o + (size_t)G * L.RVB * 4);
         L.oInvxA = o; o = al16(o + (size_t)L.PA * 8);
         L.oInvxB = o; o = al16(o + (size_t)L.PB * 4);
         L.oInvyA = o; o = al16(o + (size_t)L.THA * 8);
         L.oInvyB = o; o = al16(o + (size_t)L.THB * 4);
-        L.oABr = o; o = al16(o + (size_t)L.RBA * NAB * L.PA * 4);
+        L.oABr = o; o = al16(o + (size_t)L.RBA * L.RAB * 4);
         L.oINr = o; o = al16(o + (RING ? (size_t)L.RBI * NIN * NT * 4 : 0));
-        L.oOs = o; o = al16(o + (size_t)G * NAB * L.PB * 4);
+        L.oOs = o; o = al16(o + (size_t)G * L.ROS * 4);
         L.total = o;
         return L;
     }
@@ -125,14 +136,14 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     const int h = P.h, w = P.w, R = P.R, TW = P.TW;
     const LowresLayout& L = P.L;
     double* VsA = reinterpret_cast<double*>(smem + L.oVsA);     // [G][NMAP][VPA]
-    float* VsB = reinterpret_cast<float*>(smem + L.oVsB);       // [G][NAB][VPB]
+    float* VsB = reinterpret_cast<float*>(smem + L.oVsB);       // [G] (pitch RVB) [NAB][VPB]
     double* invxA = reinterpret_cast<double*>(smem + L.oInvxA); // [PA], 0 = outside the image
     float* invxB = reinterpret_cast<float*>(smem + L.oInvxB);   // [PB]
     double* invyA = reinterpret_cast<double*>(smem + L.oInvyA); // [THA] per a, b row - yA0
     float* invyB = reinterpret_cast<float*>(smem + L.oInvyB);   // [THB] per output row - y0
-    float* ABr = reinterpret_cast<float*>(smem + L.oABr);       // [RBA][NAB][PA]
+    float* ABr = reinterpret_cast<float*>(smem + L.oABr);       // [RBA] (pitch RAB) [NAB][PA]
     float* INr = reinterpret_cast<float*>(smem + L.oINr);       // [RBI][NIN][NT]
-    float* Os = reinterpret_cast<float*>(smem + L.oOs);         // [G][NAB][PB]
+    float* Os = reinterpret_cast<float*>(smem + L.oOs);         // [G] (pitch ROS) [NAB][PB]
 
     const int img = blockIdx.z;
     const int x0 = blockIdx.x * TW;
@@ -147,7 +158,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     // ---- tables and zero pads (the zeros make out-of-image columns contribute nothing
     // and make a = b = 0 there: inv = 0 turns every mean into 0)
     for (int i = tid; i < G * NMAP * VPA; i += NT) VsA[i] = 0.0;
-    for (int i = tid; i < G * NAB * VPB; i += NT) VsB[i] = 0.0f;
+    for (int i = tid; i < G * L.RVB; i += NT) VsB[i] = 0.0f;
     for (int j = tid; j < PA; j += NT) {
         const int ca = x0 - R + j;
         invxA[j] = (j < L.NCA && ca >= 0 && ca < w) ? inv_count(ca, w, R) : 0.0;
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     const int gB = qB / L.nrB, kB0 = (qB - gB * L.nrB) * KB;
     const bool runA = tid < TA, runB = qB >= 0 && qB < TB;
     const double* hvA = VsA + (size_t)gA * NMAP * VPA + jA0;
-    const float* hvB = VsB + (size_t)(runB ? gB : 0) * NAB * VPB + (runB ? kB0 : 0);
+    const float* hvB = VsB + (size_t)(runB ? gB : 0) * L.RVB + (runB ? kB0 : 0);
 
     const size_t n = (size_t)h * w;
     float* dstimg = P.dst + (size_t)img * NAB * n;
@@ -366,7 +377,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             const double invy = invyA[ya - yA0];
             int sl = sA + gA;
             if (sl >= RBA) sl -= RBA;
-            float* ab = ABr + (size_t)sl * NAB * PA + jA0;
+            float* ab = ABr + (size_t)sl * L.RAB + jA0;
             const double* ix = invxA + jA0;
             const double* vw = hvA + 2 * R + 1;
             double S[NMAP];
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             for (int k = 0; k <= 2 * R; ++k)
 #pragma unroll
                 for (int m = 0; m < NAB; ++m) S[m] += hvB[m * VPB + k];
-            float* o = Os + (size_t)gB * NAB * PB + kB0;
+            float* o = Os + (size_t)gB * L.ROS + kB0;
 #pragma unroll
             for (int i = 0; i < KB; ++i) {
                 const float inv = ix[i] * invy;
@@ -435,7 +446,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                     *d[m] = os[m * PB];
                     d[m] += w;
                 }
-                os += NAB * PB;
+                os += L.ROS;
             }
         }
         hbN = 0;
@@ -451,7 +462,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
         if (nB > 0) {
             if (colBv) {
                 // row y of the a, b ring (y >= yA - RBA): float offset of its slot
-                const int rstep = NAB * PA, rlen = RBA * NAB * PA;
+                const int rstep = L.RAB, rlen = RBA * L.RAB;
                 auto slot_off = [&](int y) {
                     int s = sA - (yA - y);
                     s = s < 0 ? s + RBA : s;
@@ -475,7 +486,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                     for (int g = 0; g < G; ++g) {
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) accB[m] += abc[oa + m * PA] - abc[os_ + m * PA];
-                        float* v = vcol + g * NAB * VPB;
+                        float* v = vcol + g * L.RVB;
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) {
                             *v = accB[m];
@@ -496,7 +507,7 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                         for (int m = 0; m < NAB; ++m)
                             accB[m] += (hasA ? abc[oa + m * PA] : 0.0f) - (hasS ? abc[os_ + m * PA] : 0.0f);
 #pragma unroll
-                        for (int m = 0; m < NAB; ++m) vcol[(g * NAB + m) * VPB] = accB[m];
+                        for (int m = 0; m < NAB; ++m) vcol[g * L.RVB + m * VPB] = accB[m];
                         if (hasA) { oa += rstep; if (oa >= rlen) oa -= rlen; }
                         if (hasS) { os_ += rstep; if (os_ >= rlen) os_ -= rlen; }
                     }
