@@ -238,6 +238,10 @@ struct StripParams {
     // channel c), k1 * mean otherwise -- the detail-enhancement fold (fgf_enhance_ws);
     // k1 = 1, k0 = 0 writes the means unchanged.
     float k1, k0;
+    // MEAN only: groups > 1 splits the maps of each image into `groups` launches-in-one of
+    // NIN consecutive planes (blockIdx.z = image * groups + group; group g reads planes and
+    // writes maps [g NIN, (g + 1) NIN) and folds k0 into its map g).
+    int groups;
 };
 
 // Rows per batch G (each warp slides along one row of a batch), odd run length K, smem.
@@ -272,7 +276,7 @@ struct StripEpilogue;
 template <int CP>
 struct StripEpilogue<MODE_STATS, 1, CP> {
     __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
-                                int ostride) {
+                                int ostride, int grp) {
         const double eps = P.eps;
         // The cancellations (var_I, cov_Ip: P:78-79) are formed in fp64; the quotient and b
         // (Eq.2-3) are well conditioned and are formed in fp32.
@@ -297,7 +301,7 @@ struct StripEpilogue<MODE_STATS, 1, CP> {
 template <int CP>
 struct StripEpilogue<MODE_STATS, 3, CP> {
     __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
-                                int ostride) {
+                                int ostride, int grp) {
         const double eps = P.eps;
         const double m0 = S[0] * inv, m1 = S[1] * inv, m2 = S[2] * inv;
         const double s00 = S[3] * inv - m0 * m0 + eps;
@@ -335,11 +339,12 @@ struct StripEpilogue<MODE_STATS, 3, CP> {
 template <int CI, int CP>
 struct StripEpilogue<MODE_MEAN, CI, CP> {
     __device__ static void emit(const double* S, double inv, const StripParams& P, float* dst,
-                                int ostride) {
+                                int ostride, int grp) {
 #pragma unroll
         for (int m = 0; m < (CI + 1) * CP; ++m) {
             const int c = m / (CI + 1), j = m - c * (CI + 1);
-            dst[m * ostride] = fmaf(P.k1, (float)(S[m] * inv), j == c ? P.k0 : 0.0f);
+            // grouped launch (one p channel per CTA, CP = 1 here): channel grp's diagonal
+            dst[m * ostride] = fmaf(P.k1, (float)(S[m] * inv), j == c + grp ? P.k0 : 0.0f);
         }
     }
 };
@@ -381,7 +386,8 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
     double* invx = reinterpret_cast<double*>(Os + (size_t)G * NOUT * NT);  // [NT]
 
     const int tid = threadIdx.x;
-    const int img = blockIdx.z;
+    const int groups = P.groups > 1 ? P.groups : 1;
+    const int img = blockIdx.z / groups, grp = blockIdx.z - img * groups;
     const int h = P.h, w = P.w, R = P.R;
     const int n = h * w;
     const int x0 = blockIdx.x * P.TW;
@@ -395,9 +401,9 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
     const bool colthr = tid < ncol;
     const int offc = (xs0 + (colthr ? tid : 0)) * P.col;
     const int row = P.row, planeI = P.planeI, planeP = P.planeP;
-    const float* bI = P.srcI + img * P.imgI;
+    const float* bI = P.srcI + img * P.imgI + (long long)grp * NIN * planeI;
     const float* bP = (MODE == MODE_STATS) ? P.srcP + img * P.imgP : bI;
-    float* dst = P.dst + (size_t)img * NOUT * n + x0;
+    float* dst = P.dst + ((size_t)img * groups + grp) * NOUT * n + x0;
 
     // Zero the padded column-sum rows once: the pads make every horizontal window read
     // in-bounds, and zeros contribute nothing, so sums equal the clipped sums (R1).
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
                 for (int m = 0; m < NMAP; ++m)
                     S[m] = pr[m * VP + hi] - (lo >= 0 ? pr[m * VP + lo] : 0.0);
                 StripEpilogue<MODE, CI, CP>::emit(S, invx[oc] * invy, P,
-                                                  Os + (size_t)g * NOUT * NT + oc, NT);
+                                                  Os + (size_t)g * NOUT * NT + oc, NT, grp);
             }
         }
         // ---- horizontal phase: branch-free sliding window along each snapshotted row.
@@ -552,7 +558,7 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
 #pragma unroll
             for (int i = 0; i < K; ++i) {
                 if (oc0 + i < ocn)
-                    StripEpilogue<MODE, CI, CP>::emit(S, invx[oc0 + i] * invy, P, orow + i, NT);
+                    StripEpilogue<MODE, CI, CP>::emit(S, invx[oc0 + i] * invy, P, orow + i, NT, grp);
                 if (i + 1 < K) {
 #pragma unroll
                     for (int m = 0; m < NMAP; ++m) S[m] += vr[m * VP + i + R + 1] - vr[m * VP + i - R];

@@ -71,6 +71,14 @@ int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream
 
 template <int MODE>
 int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
+    if (MODE == MODE_MEAN && P.CI == 3 && P.CP > 1 && getenv("FGF_MEAN_NOGROUP") == nullptr) {
+        // colour box of a, b: the 4 C_p maps as C_p groups of 4 in one launch (the 3 / 1
+        // kernel: 4 fp64 running sums per thread instead of 4 C_p, so 4 CTAs per SM instead of
+        // one -- measured on config 3 below)
+        StripParams g = sp;
+        g.groups = P.CP;
+        return launch_strip_nt<MODE, 3, 1>(g, images * P.CP, P, st);
+    }
     switch (P.CI * 10 + P.CP) {
         case 11: return launch_strip_nt<MODE, 1, 1>(sp, images, P, st);
         case 12: return launch_strip_nt<MODE, 1, 2>(sp, images, P, st);
