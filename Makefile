@@ -18,11 +18,13 @@ all: $(LIB) $(ORACLE)
 # K13 compiled through nvcc's split-compile path: there its loop and ring indices stay on the
 # uniform datapath (550 uniform instructions vs 68), measured 4.14 -> 4.03 ms on config 4; the
 # same path slows the strip engine's statistics kernel (0.564 -> 0.591 ms on config 3).
+# nvcc hides the make jobserver's tokens from split-compile when it sees MAKEFLAGS (then it
+# compiles unsplit, i.e. the other code), so the recipe runs it without MAKEFLAGS.
 TUFLAGS_fgf_k_lowres := --split-compile=2
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) $(TUFLAGS_$*) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+	env -u MAKEFLAGS -u MFLAGS $(NVCC) $(NVFLAGS) $(TUFLAGS_$*) -c -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
