@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--dtype", choices=["f32", "f16", "bf16"], default="f32",
+    ap.add_argument("--dtype", choices=["f32", "f16", "bf16", "u8"], default="f32",
                     help="element type of I, p, q (f16 / bf16: the reduced-precision I/O variant)")
     ap.add_argument("--band-mode", choices=["single", "two-step"], default="single",
                     help="config 5: one 2r'+1-row exchange of I', p', or r' rows then r'+1 rows of a, b")
@@ -237,15 +237,20 @@ def main():
 
     # Inputs resident in HBM before timing; rank k owns global images [k*B, (k+1)*B).
     I, p = synth.make_batch(args.config, dev, batch=B, first=rank * B)
-    # --dtype f16 / bf16: the reduced-precision I/O variant (fgf_filter_ex_ws; not the
+    # --dtype f16 / bf16 / u8: the reduced-precision I/O variant (fgf_filter_ex_ws; not the
     # BASELINE.json configuration, which is fp32)
-    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[args.dtype]
-    code = {"f32": fgf.FGF_F32, "f16": fgf.FGF_F16, "bf16": fgf.FGF_BF16}[args.dtype]
-    esize = 4 if args.dtype == "f32" else 2
+    tdt = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16,
+           "u8": torch.uint8}[args.dtype]
+    code = {"f32": fgf.FGF_F32, "f16": fgf.FGF_F16, "bf16": fgf.FGF_BF16, "u8": fgf.FGF_U8}[args.dtype]
+    esize = {"f32": 4, "f16": 2, "bf16": 2, "u8": 1}[args.dtype]
     if args.dtype != "f32":
         same = p is I
-        I = I.to(tdt).contiguous()
-        p = I if same else p.to(tdt).contiguous()
+        if args.dtype == "u8":   # 8-bit codes k / 255 (R19)
+            conv = lambda t: torch.round(t.clamp(0, 1) * 255.0).to(torch.uint8).contiguous()
+        else:
+            conv = lambda t: t.to(tdt).contiguous()
+        I = conv(I)
+        p = I if same else conv(p)
     q = torch.empty((B, CP, H, W), dtype=tdt, device=dev)
     ws_bytes = fgf.fgf_workspace_bytes_ex(B, H, W, CI, CP, r, s, code)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)

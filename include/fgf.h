@@ -75,7 +75,10 @@ enum {
 enum {
     FGF_F32 = 0,          /* float                                                          */
     FGF_F16 = 1,          /* IEEE binary16 (__half)                                          */
-    FGF_BF16 = 2          /* bfloat16 (__nv_bfloat16)                                        */
+    FGF_BF16 = 2,         /* bfloat16 (__nv_bfloat16)                                        */
+    FGF_U8 = 3            /* 8-bit codes: code k is the value fl(k x fl(1/255)); q is
+                             stored as the nearest code to 255 q, saturated to [0, 255]
+                             (R19; the paper's data are 8-bit images)            */
 };
 
 enum {
@@ -205,11 +208,12 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
                               int nranks, void* workspace, size_t ws_bytes, void* cuda_stream);
 
 /* Reduced-precision I/O: fgf_filter_ws with I, p and q of element type
- * dtype (FGF_F32 / FGF_F16 / FGF_BF16; all three buffers the same type, 2-byte alignment for
- * the 16-bit types).  Only the storage changes: samples are widened to fp32 / fp64 on load
- * exactly as in the fp32 path, and q is rounded to the element type once, on store.  16-bit
- * types support C_I / C_p = 1 / 1, 3 / 1 and 3 / 3 (else FGF_ERR_UNSUPPORTED).  Workspace:
- * fgf_workspace_bytes_ex().  Other errors as fgf_filter_ws; a bad dtype is FGF_ERR_PARAM. */
+ * dtype (FGF_F32 / FGF_F16 / FGF_BF16 / FGF_U8; all three buffers the same type, aligned to
+ * the element size).  Only the storage changes: samples are widened to fp32 / fp64 on load
+ * exactly as in the fp32 path (8-bit code k -> fl(k x fl(1/255))), and q is rounded to the element type
+ * once, on store (8-bit: nearest code, saturated).  The reduced types support C_I / C_p =
+ * 1 / 1, 3 / 1 and 3 / 3 (else FGF_ERR_UNSUPPORTED).  Workspace: fgf_workspace_bytes_ex().
+ * Other errors as fgf_filter_ws; a bad dtype is FGF_ERR_PARAM. */
 size_t fgf_workspace_bytes_ex(int batch, int H, int W, int C_I, int C_p, int r, int s, int dtype);
 int fgf_filter_ex_ws(const void* I, const void* p, void* q, int batch, int H, int W, int C_I,
                      int C_p, int r, double eps, int s, int sub_mode, int dtype, void* workspace,

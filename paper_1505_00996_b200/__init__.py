@@ -35,6 +35,7 @@ FGF_ERR_DEVICE = 10
 FGF_F32 = 0
 FGF_F16 = 1
 FGF_BF16 = 2
+FGF_U8 = 3
 FGF_BAND_SINGLE = 0
 FGF_BAND_TWO_STEP = 1
 FGF_SUB_NEAREST = 0
@@ -377,11 +378,12 @@ def filter(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None, w
     Enqueued on `stream` (default: torch's current stream); returns q."""
     import torch
     B, H, W, C_I, C_p = _geom(I, p)
-    codes = {torch.float32: FGF_F32, torch.float16: FGF_F16, torch.bfloat16: FGF_BF16}
+    codes = {torch.float32: FGF_F32, torch.float16: FGF_F16, torch.bfloat16: FGF_BF16,
+             torch.uint8: FGF_U8}
     for t in (I, p):
         if not t.is_cuda or t.dtype not in codes or not t.is_contiguous() or t.dtype != I.dtype:
             raise ValueError("I and p must be contiguous CUDA tensors of one dtype "
-                             "(float32, float16 or bfloat16)")
+                             "(float32, float16, bfloat16 or uint8 codes k / 255)")
     dt = codes[I.dtype]
     if out is None:
         out = torch.empty((B, C_p, H, W), dtype=I.dtype, device=I.device)

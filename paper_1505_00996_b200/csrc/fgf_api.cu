@@ -84,9 +84,10 @@ size_t plan_ws(const Plan& P, bool need_mean) {
 // Reduced-precision I/O: the strip engine reads fp32 planes, so at s = 1 a non-fp32 image is
 // first converted into the planes region (K0 with s = 1), which then always exists.
 int set_dtype(Plan& P, int dtype) {
-    if (dtype != FGF_F32 && dtype != FGF_F16 && dtype != FGF_BF16) return FGF_ERR_PARAM;
+    if (dtype != FGF_F32 && dtype != FGF_F16 && dtype != FGF_BF16 && dtype != FGF_U8)
+        return FGF_ERR_PARAM;
     P.dtype = dtype;
-    P.esize = dtype == FGF_F32 ? 4 : 2;
+    P.esize = dtype == FGF_F32 ? 4 : (dtype == FGF_U8 ? 1 : 2);
     if (dtype != FGF_F32 && P.ws_planes == 0) {
         P.ws_planes = align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float));
         P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;

@@ -26,6 +26,7 @@ int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cud
     switch (P.dtype) {
         case FGF_F16: return launch_subsample_e<__half>(src, dst, planes, P, st);
         case FGF_BF16: return launch_subsample_e<__nv_bfloat16>(src, dst, planes, P, st);
+        case FGF_U8: return launch_subsample_e<unsigned char>(src, dst, planes, P, st);
     }
     return launch_subsample_e<float>(src, dst, planes, P, st);
 }

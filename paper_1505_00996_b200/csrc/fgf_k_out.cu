@@ -64,16 +64,20 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
             }
         }
     }
-    ProfScope ps(KIND_OUT, st);
-    if (s1) {
-        output_kernel<CI, CP, PX, true, 0, 0, 0, E><<<grid, 256, 0, st>>>(op);
+    if constexpr (PX * sizeof(float) > 16) {
+        return FGF_ERR_UNSUPPORTED;   // the register walker moves fp32 map vectors of PX
     } else {
-        auto kern = output_kernel<CI, CP, PX, false, 0, 0, 0, E>;
-        set_smem(kern, smem);
-        kern<<<grid, 256, smem, st>>>(op);
+        ProfScope ps(KIND_OUT, st);
+        if (s1) {
+            output_kernel<CI, CP, PX, true, 0, 0, 0, E><<<grid, 256, 0, st>>>(op);
+        } else {
+            auto kern = output_kernel<CI, CP, PX, false, 0, 0, 0, E>;
+            set_smem(kern, smem);
+            kern<<<grid, 256, smem, st>>>(op);
+        }
+        ++g_last_launches;
+        return last_error();
     }
-    ++g_last_launches;
-    return last_error();
 }
 
 // Colour guidance with several p channels, fp32, 4-pixel alignment: the channel-split K4
@@ -118,6 +122,14 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     constexpr uintptr_t ES = sizeof(E);
     const uintptr_t ai = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
     const uintptr_t am = reinterpret_cast<uintptr_t>(op.M);
+    if constexpr (ES == 1) {   // 8-bit codes: 8 pixels (8 bytes) per thread and row
+        const bool s1 = op.hg == op.Hg && P.w == P.W;
+        if (NC <= 2 && !s1 && P.W % 8 == 0 && (ai & 7u) == 0 && (am & 15u) == 0 &&
+            getenv("FGF_K4_U8PX4") == nullptr) {
+            const int rc = launch_output_px<CI, CP, (NC <= 2 ? 8 : 1), E>(op, images, P, st);
+            if (rc != FGF_ERR_UNSUPPORTED) return rc;
+        }
+    }
     if (NC <= 2 && P.W % 4 == 0 && (ai & (4 * ES - 1)) == 0 && (am & 15u) == 0)
         return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1), E>(op, images, P, st);
     if (NC <= 4 && P.W % 2 == 0 && (ai & (2 * ES - 1)) == 0 && (am & 7u) == 0)
@@ -132,7 +144,11 @@ int launch_output(const void* I, const float* M, void* q, int images, const Plan
     if (P.dtype != FGF_F32) {
         // reduced-precision I/O: gray -> gray, colour -> colour, colour guide -> one channel
         const int key = P.CI * 10 + P.CP;
-        if (P.dtype == FGF_F16) {
+        if (P.dtype == FGF_U8) {
+            if (key == 11) return launch_output_t<1, 1, unsigned char>(op, images, P, st);
+            if (key == 31) return launch_output_t<3, 1, unsigned char>(op, images, P, st);
+            if (key == 33) return launch_output_t<3, 3, unsigned char>(op, images, P, st);
+        } else if (P.dtype == FGF_F16) {
             if (key == 11) return launch_output_t<1, 1, __half>(op, images, P, st);
             if (key == 31) return launch_output_t<3, 1, __half>(op, images, P, st);
             if (key == 33) return launch_output_t<3, 3, __half>(op, images, P, st);

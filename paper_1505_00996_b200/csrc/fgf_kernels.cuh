@@ -36,7 +36,8 @@ namespace fgf {
 
 enum { MODE_STATS = 0, MODE_MEAN = 1 };
 
-// Packed PX-element vectors of the I / q element type E (float, __half, __nv_bfloat16) as raw
+// Packed PX-element vectors of the I / q element type E (float, __half, __nv_bfloat16,
+// unsigned char) as raw
 // 32-bit words: one streaming load / store per thread and row, elements converted to fp32
 // (reduced-precision I/O: storage only, every operation is fp32).
 template <int BYTES> struct RawT;
@@ -44,16 +45,19 @@ template <> struct RawT<16> { using T = uint4; };
 template <> struct RawT<8> { using T = uint2; };
 template <> struct RawT<4> { using T = unsigned int; };
 template <> struct RawT<2> { using T = unsigned short; };
+template <> struct RawT<1> { using T = unsigned char; };
 __device__ __forceinline__ unsigned raw_word(const uint4& r, int k) {
     return k == 0 ? r.x : (k == 1 ? r.y : (k == 2 ? r.z : r.w));
 }
 __device__ __forceinline__ unsigned raw_word(const uint2& r, int k) { return k == 0 ? r.x : r.y; }
 __device__ __forceinline__ unsigned raw_word(unsigned r, int) { return r; }
 __device__ __forceinline__ unsigned raw_word(unsigned short r, int) { return r; }
+__device__ __forceinline__ unsigned raw_word(unsigned char r, int) { return r; }
 __device__ __forceinline__ void raw_make(uint4& r, const unsigned* w) { r = make_uint4(w[0], w[1], w[2], w[3]); }
 __device__ __forceinline__ void raw_make(uint2& r, const unsigned* w) { r = make_uint2(w[0], w[1]); }
 __device__ __forceinline__ void raw_make(unsigned& r, const unsigned* w) { r = w[0]; }
 __device__ __forceinline__ void raw_make(unsigned short& r, const unsigned* w) { r = (unsigned short)w[0]; }
+__device__ __forceinline__ void raw_make(unsigned char& r, const unsigned* w) { r = (unsigned char)w[0]; }
 
 template <typename E> struct ElemT;
 template <> struct ElemT<float> {
@@ -71,6 +75,15 @@ template <> struct ElemT<__nv_bfloat16> {
     __device__ static unsigned bits(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
     __device__ static float load(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
 };
+// 8-bit codes (R19): code k is the value fl(k x fl(1/255)) (one fp32 product, within
+// an ulp of k / 255); a value is stored as the code nearest to 255 x, saturated to [0, 255].
+template <> struct ElemT<unsigned char> {
+    __device__ static float f(unsigned b) { return __fmul_rn((float)(b & 0xffu), 1.0f / 255.0f); }
+    __device__ static unsigned bits(float x) {
+        return __float2uint_rn(fminf(fmaxf(x * 255.0f, 0.0f), 255.0f));
+    }
+    __device__ static float load(const unsigned char* p) { return f(__ldg(p)); }
+};
 
 template <typename E, int PX>
 struct Vec {
@@ -80,7 +93,7 @@ struct Vec {
     __device__ static float get(const T& v, int i) {
         const int bit = i * EB * 8;
         const unsigned w = raw_word(v, bit >> 5) >> (bit & 31);
-        return ElemT<E>::f(EB == 4 ? w : (w & 0xffffu));
+        return ElemT<E>::f(EB == 4 ? w : (w & ((1u << (EB * 8)) - 1u)));
     }
     __device__ static void st(E* p, const float* v) {
         unsigned w[BYTES >= 4 ? BYTES / 4 : 1] = {};
