@@ -8,7 +8,7 @@ PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 # one translation unit per kernel family, compiled in parallel (make -j), each in a single
 # ptxas pass: nvcc --split-compile made register allocation depend on the split count
-TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_lowres
+TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_lowres fgf_k_lowres_v3
 OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
 ORACLE := oracle/libfgf_oracle.so
@@ -21,6 +21,9 @@ all: $(LIB) $(ORACLE)
 # nvcc hides the make jobserver's tokens from split-compile when it sees MAKEFLAGS (then it
 # compiles unsplit, i.e. the other code), so the recipe runs it without MAKEFLAGS.
 TUFLAGS_fgf_k_lowres := --split-compile=2
+# the default fp32 variant alone in its unit: its split-compile code does not depend on the
+# other instantiations (adding the 8-bit variants to the shared unit had changed it)
+TUFLAGS_fgf_k_lowres_v3 := --split-compile=2
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile
 	@mkdir -p build

@@ -1,0 +1,108 @@
+// fgf_lowres_launch.cuh -- K13 launch helpers shared by fgf_k_lowres.cu (geometry, dispatch,
+// the other variants) and fgf_k_lowres_v3.cu (the default fp32 variant in a unit of its own).
+#pragma once
+#include "fgf_host.cuh"
+
+namespace fgf {
+
+// ---- K13: fused low-res chain (gray guidance), fgf_lowres.cuh
+constexpr size_t kLrSmemMax = 227 * 1024;
+
+// Kernel variants (rows per batch G, horizontal run lengths KA / KB); the first that fits
+// is used unless FGF_LR_V selects one (development sweep).
+//   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
+//   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
+// (measured on config 4, profiles/round1/k13_variants.txt: G 8 / K 17 and G 6 / K 13 without
+// the ring, and a lane-pair split of the runs, were slower)
+// (also slower: K 5/17 and K 7/17, rebalancing the two concurrent horizontal phases)
+constexpr int kLrNumVariants = 4;
+
+// Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
+struct LrGeom {
+    int NT = 0, TW = 0, strips = 0, TH = 0, V = -1;
+    size_t smem = 0;
+};
+
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512>
+inline bool lowres_fits(LrGeom& g, int R, int v) {
+    using C = LowresCfg<CP, G, KA, KB, RING>;
+    const auto L = C::layout(g.NT, g.TW, g.TH, R);
+    // both horizontal phases run concurrently on disjoint threads
+    if (L.total > kLrSmemMax || G * (L.nrA + L.nrB) > g.NT || g.NT > MAXT) return false;
+    g.smem = L.total;
+    g.V = v;
+    return true;
+}
+
+template <int CP>
+inline bool lowres_fits_v(LrGeom& g, int R, int v) {
+    if (CP > 1 && v != 0) return false;          // one variant for several p channels
+    switch (v) {
+        case 0: return lowres_fits<CP, 4, 9, 9>(g, R, v);
+        case 1: return lowres_fits<CP, 8, 9, 9>(g, R, v);
+        case 2: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
+        case 3: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
+    }
+    return false;
+}
+
+template <int CP>
+inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
+    // Target ~160 threads (5 warps) per CTA: three CTAs per SM, halo overhead (TW + 4R) / TW.
+    int want_nt = 160;
+    if (const char* e = getenv("FGF_LR_NT")) want_nt = atoi(e);
+    LrGeom best;
+    for (int ns = 1; ns <= w; ++ns) {
+        const int TW = (w + ns - 1) / ns;
+        if ((ns - 1) * TW >= w) continue;
+        const int NT = (TW + 4 * R + 31) / 32 * 32;
+        if (NT > 512) continue;
+        const long long tot = (long long)ns * NT, btot = (long long)best.strips * best.NT;
+        // closest to the target size; on ties the fewer total threads
+        const bool better = best.NT == 0 || std::abs(NT - want_nt) < std::abs(best.NT - want_nt) ||
+                            (std::abs(NT - want_nt) == std::abs(best.NT - want_nt) && tot < btot);
+        if (better) { best.NT = NT; best.TW = TW; best.strips = ns; }
+        if (NT < 64) break;
+    }
+    if (best.NT == 0) return false;
+    // Segment height: long segments amortise the 2r'+1 warm-up rows (up to 256 rows); small
+    // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
+    const long long cols = (long long)best.strips * images;
+    long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
+    th = std::min<long long>(256, std::max<long long>(th, std::max(8, 2 * R + 2)));
+    if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
+    best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
+    if (const char* e = getenv("FGF_LR_V")) {
+        if (lowres_fits_v<CP>(best, R, atoi(e))) { g = best; return true; }
+        return false;
+    }
+    static const int order[kLrNumVariants] = {3, 0, 1, 2};   // measured: 3 fastest (config 4)
+    for (int v : order)
+        if (lowres_fits_v<CP>(best, R, v)) { g = best; return true; }
+    return false;
+}
+
+template <int CP, int G, int KA, int KB, bool RING = true, int MAXT = 512, int MINB = 1,
+          typename E = float>
+int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
+                         cudaStream_t st) {
+    auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, E>;
+    LowresParams lpl = lp;
+    lpl.L = LowresCfg<CP, G, KA, KB, RING>::layout(g.NT, lp.TW, lp.TH, P.R);
+    size_t smem = g.smem;
+    // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
+    // previous chunk can be co-resident (overlap experiment knob)
+    if (const char* e = getenv("FGF_LR_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
+    set_smem(kern, smem);
+    dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
+    ProfScope ps(KIND_LOWRES, st);
+    kern<<<grid, g.NT, smem, st>>>(lpl);
+    ++g_last_launches;
+    return last_error();
+}
+
+// The default variant for fp32 samples (fgf_k_lowres_v3.cu).
+int launch_lowres_v3_f32(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
+                         cudaStream_t st);
+
+}  // namespace fgf
