@@ -1,8 +1,11 @@
 """Randomised geometry sweep on the GPU against the fp64 oracle: sizes from 1 pixel to a few
 hundred, every radius regime (r' from 1 up to beyond the image), every subsampling ratio the
 ABI accepts, both subsampling modes, gray / colour guidance with 1-4 p channels, fp32 and
-16-bit I/O, self-guidance.  Seeded, so a failure reproduces."""
+16-bit and 8-bit I/O, self-guidance.  Seeded, so a failure reproduces; FGF_FUZZ_SEEDS=n runs
+n seeds instead of 200."""
 from __future__ import annotations
+
+import os
 
 import numpy as np
 import pytest
@@ -32,23 +35,43 @@ def _case(seed):
     B = int(rng.integers(1, 3))
     dtype = torch.float32
     if (CI, CP) in ((1, 1), (3, 1), (3, 3)) and rng.random() < 0.3:
-        dtype = torch.float16 if rng.random() < 0.5 else torch.bfloat16
+        u = rng.random()
+        dtype = torch.float16 if u < 1 / 3 else (torch.bfloat16 if u < 2 / 3 else torch.uint8)
     self_guided = CI == 1 and CP == 1 and rng.random() < 0.3
     return B, H, W, CI, CP, r, eps, s, sub, dtype, self_guided
 
 
-@pytest.mark.parametrize("seed", range(200))
+INV255 = torch.tensor(1.0 / 255.0, dtype=torch.float32)   # 8-bit codes decode as k x fl(1/255)
+
+
+def _store(t, dtype):
+    if dtype == torch.uint8:
+        return torch.round(t * 255.0).to(torch.uint8).contiguous()
+    return t.to(dtype).contiguous()
+
+
+def _values(t):
+    return t.float() * INV255.to(t.device) if t.dtype == torch.uint8 else t.float()
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FGF_FUZZ_SEEDS", "200"))))
 def test_fuzz_against_oracle(seed):
     B, H, W, CI, CP, r, eps, s, sub, dtype, self_guided = _case(seed)
     g = torch.Generator(device="cuda").manual_seed(1000 + seed)
-    I = torch.rand((B, CI, H, W), device="cuda", generator=g).to(dtype).contiguous()
-    p = I if self_guided else torch.rand((B, CP, H, W), device="cuda", generator=g).to(dtype).contiguous()
+    I = _store(torch.rand((B, CI, H, W), device="cuda", generator=g), dtype)
+    p = I if self_guided else _store(torch.rand((B, CP, H, W), device="cuda", generator=g), dtype)
     q = fgf.filter(I, p, r, eps, s, sub)
     torch.cuda.synchronize()
     tol = 1e-4 if eps >= 1e-3 else 1e-3
     for b in range(B):
-        ref = oracle.fast_guided_filter(I[b:b + 1].float().cpu().numpy(),
-                                        p[b:b + 1].float().cpu().numpy(), r, eps, s, sub)
+        ref = oracle.fast_guided_filter(_values(I[b:b + 1]).cpu().numpy(),
+                                        _values(p[b:b + 1]).cpu().numpy(), r, eps, s, sub)
+        if dtype == torch.uint8:   # codes: fp32 bound in codes + half a code, vs clamped q
+            got = q[b:b + 1].double().cpu().numpy()
+            err = np.abs(got - np.clip(ref, 0.0, 1.0) * 255.0)
+            assert (err <= 0.5 + 255.0 * tol + 1e-3).all(), (seed, B, H, W, CI, CP, r, eps, s,
+                                                             sub, float(err.max()))
+            continue
         got = q[b:b + 1].double().cpu().numpy()
         assert np.isfinite(got).all()
         bound = tol + HALF_ULP[dtype] * np.maximum(1.0, np.abs(ref))
