@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="override the config batch per GPU")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay each step from a CUDA graph (small single-image configs: no "
+                         "per-launch host overhead)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dtype", choices=["f32", "f16", "bf16", "u8"], default="f32",
                     help="element type of I, p, q (f16 / bf16: the reduced-precision I/O variant)")
@@ -256,17 +259,29 @@ def main():
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(st=stream):
         if args.dtype == "f32":
-            fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, ws_bytes, stream)
+            fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, ws_bytes, st)
         else:
             fgf.fgf_filter_ex_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, code, ws, ws_bytes,
-                                 stream)
+                                 st)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
     launches_per_step = fgf.fgf_last_launch_count()
+    eager_step = step
+    if args.graph:
+        # the same call captured once; each timed step replays it on `stream`
+        gstream = torch.cuda.Stream(dev)
+        gstream.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gstream):
+            step(gstream)
+        torch.cuda.synchronize()
+        graph.replay()
+        torch.cuda.synchronize()
+        step = lambda st=stream: graph.replay()   # noqa: E731
 
     props = torch.cuda.get_device_properties(dev)
     gpu_id = "GPU-" + str(props.uuid) if getattr(props, "uuid", None) else str(local)
@@ -300,7 +315,7 @@ def main():
     # ---------------- per-kernel CUDA events over the same K steps (diagnostic pass).
     fgf.fgf_profile_enable(True)
     for _ in range(args.steps):
-        step()
+        eager_step()        # the library records its events at enqueue time (not in a graph)
     torch.cuda.synchronize()
     prof = fgf.fgf_profile_read()
     fgf.fgf_profile_enable(False)
@@ -384,7 +399,8 @@ def main():
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": dict(config_json(c, prm, B, world), io_dtype=args.dtype),
+                "config": dict(config_json(c, prm, B, world), io_dtype=args.dtype,
+                               cuda_graph=bool(args.graph)),
                 "gpu_launches": launches_per_step * args.steps,
                 "roofline": roofline, "hbm_whole_filter": whole, "kernels": kern,
                 "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

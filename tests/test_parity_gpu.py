@@ -287,3 +287,35 @@ def test_k4_variants_agree(monkeypatch, CP):
         assert torch.equal(q0, q1), knob
     ref = oracle.fast_guided_filter(I[:1].cpu().numpy(), p[:1].cpu().numpy(), 8, 0.01, 4, 1)
     assert np.abs(q0[:1].double().cpu().numpy() - ref).max() <= 1e-4
+
+
+@pytest.mark.parametrize("cfg,chunk_mb", [(1, None), (3, None), (1, "1")])
+def test_cuda_graph_capture_and_replay(monkeypatch, cfg, chunk_mb):
+    """fgf_filter_ws is capturable into a CUDA graph (small single-image calls replay without
+    per-launch host overhead): the replayed graph writes the same q, bit for bit, as the eager
+    call -- gray (K13 + K4), colour (K0, K1, K3, K4) and the two-stream chunk pipeline (fork /
+    join through events inside the capture)."""
+    if chunk_mb:
+        monkeypatch.setenv("FGF_CHUNK_MB", chunk_mb)
+    else:
+        monkeypatch.delenv("FGF_CHUNK_MB", raising=False)
+    H, W, B = (540, 960, 4) if cfg == 1 else (270, 480, 2)
+    I, p = synth.make_batch(cfg, "cuda", batch=B, H=H, W=W)
+    prm = synth.params(cfg)
+    CI, CP = I.shape[1], p.shape[1]
+    nb = fgf.fgf_workspace_bytes(B, H, W, CI, CP, prm["r"], prm["s"])
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    q_ref = torch.empty((B, CP, H, W), device="cuda")
+    q = torch.empty_like(q_ref)
+    side = torch.cuda.Stream()
+    args = (B, H, W, CI, CP, prm["r"], prm["eps"], prm["s"], prm["sub_mode"], ws, nb)
+    with torch.cuda.stream(side):
+        fgf.fgf_filter_ws(I, p, q_ref, *args, side)          # eager (also warms up)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        fgf.fgf_filter_ws(I, p, q, *args, side)
+    q.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(q, q_ref)
