@@ -1,0 +1,66 @@
+"""Compile one CUDA translation unit several times and keep the object whose code for a given
+kernel uses the uniform datapath most.
+
+nvcc's --split-compile NVVM output is not deterministic (the same source gives different PTX
+from run to run), and for the default K13 variant the two outcomes differ in speed: with its
+loop and ring indices on the uniform datapath (~540 uniform SASS instructions) K13 takes
+3.91 ms on config 4, otherwise (~200, or ~60 unsplit) 4.1-4.2 ms (build).  This
+picks the former: up to --tries compiles, stopping at the first whose uniform-instruction
+count reaches --want.
+
+usage: python tools/nvcc_pick.py --out build/x.o --kernel <mangled name> [--tries 8]
+                                 [--want 400] -- nvcc <args without -o>
+"""
+import argparse
+import os
+import re
+import shutil
+import subprocess
+import sys
+import tempfile
+
+
+def uniform_count(obj, kernel):
+    out = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
+    n, on = 0, False
+    for line in out.splitlines():
+        if "Function :" in line:
+            on = line.strip().endswith(kernel)
+            continue
+        if on:
+            m = re.match(r"\s+/\*[0-9a-f]+\*/\s+(@!?U?P\w+\s+)?(\S+)", line)
+            if m and m.group(2).startswith("U"):
+                n += 1
+    return n
+
+
+def main():
+    argv = sys.argv[1:]
+    k = argv.index("--")
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--kernel", required=True)
+    ap.add_argument("--tries", type=int, default=8)
+    ap.add_argument("--want", type=int, default=400)
+    a = ap.parse_args(argv[:k])
+    cmd = argv[k + 1:]
+    env = {x: y for x, y in os.environ.items() if x not in ("MAKEFLAGS", "MFLAGS")}
+    best, best_n = None, -1
+    tmp = tempfile.mkdtemp(prefix="nvcc_pick_")
+    try:
+        for t in range(a.tries):
+            obj = os.path.join(tmp, f"try{t}.o")
+            subprocess.run(cmd + ["-o", obj], check=True, env=env)
+            n = uniform_count(obj, a.kernel)
+            print(f"nvcc_pick: try {t}: {n} uniform instructions in {a.kernel[:48]}...", file=sys.stderr)
+            if n > best_n:
+                best, best_n = obj, n
+            if n >= a.want:
+                break
+        shutil.copyfile(best, a.out)
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+
+
+if __name__ == "__main__":
+    main()
