@@ -27,7 +27,7 @@ TUFLAGS_fgf_k_lowres_v3 := --split-compile=2
 
 # the default fp32 K13 variant: the split-compile outcome with its indices on the uniform
 # datapath (tools/nvcc_pick.py; nvcc's split-compile NVVM output varies from run to run)
-K13_V3 := _ZN3fgf18lowres_gray_kernelILi1ELi4ELi9ELi9ELb0ELi160ELi3EfEEvNS_12LowresParamsE
+K13_V3 := _ZN3fgf18lowres_gray_kernelILi1ELi4ELi9ELi17ELb0ELi160ELi3EfEEvNS_12LowresParamsE
 build/fgf_k_lowres_v3.o: $(PKG)/csrc/fgf_k_lowres_v3.cu $(HDRS) Makefile tools/nvcc_pick.py
 	@mkdir -p build
 	python3 tools/nvcc_pick.py --out $@ --kernel $(K13_V3) -- $(NVCC) $(NVFLAGS) $(TUFLAGS_fgf_k_lowres_v3) -c $< 2> build/fgf_k_lowres_v3.ptxas.log || (cat build/fgf_k_lowres_v3.ptxas.log; false)

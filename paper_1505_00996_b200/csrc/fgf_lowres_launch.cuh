@@ -11,10 +11,11 @@ constexpr size_t kLrSmemMax = 227 * 1024;
 // Kernel variants (rows per batch G, horizontal run lengths KA / KB); the first that fits
 // is used unless FGF_LR_V selects one (development sweep).
 //   0: G 4, K 9/9, sample ring        1: G 8, K 9/9, sample ring
-//   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM   3: as 2 with <= 3 CTAs/SM
+//   2: G 4, K 9/9, no ring, <=160 threads x 4 CTAs/SM
+//   3: G 4, K 9/17 (stage-B runs of 17), no ring, <= 3 CTAs/SM -- the default
 // (measured on config 4, profiles/round1/k13_variants.txt: G 8 / K 17 and G 6 / K 13 without
-// the ring, and a lane-pair split of the runs, were slower)
-// (also slower: K 5/17 and K 7/17, rebalancing the two concurrent horizontal phases)
+// the ring, and a lane-pair split of the runs, were slower; so were K 5/17, K 7/17, K 7/9 and
+// K 9/25; K 9/17 beat K 9/9 by 1.5 %)
 constexpr int kLrNumVariants = 4;
 
 // Strip geometry of K13: NT = round32(TW + 4R) <= 512 threads per CTA.
@@ -41,7 +42,7 @@ inline bool lowres_fits_v(LrGeom& g, int R, int v) {
         case 0: return lowres_fits<CP, 4, 9, 9>(g, R, v);
         case 1: return lowres_fits<CP, 8, 9, 9>(g, R, v);
         case 2: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
-        case 3: return lowres_fits<CP, 4, 9, 9, false, 160>(g, R, v);
+        case 3: return lowres_fits<CP, 4, 9, 17, false, 160>(g, R, v);
     }
     return false;
 }

@@ -22,15 +22,18 @@ import tempfile
 
 def uniform_count(obj, kernel):
     out = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
-    n, on = 0, False
+    n, on, found = 0, False, False
     for line in out.splitlines():
         if "Function :" in line:
             on = line.strip().endswith(kernel)
+            found = found or on
             continue
         if on:
             m = re.match(r"\s+/\*[0-9a-f]+\*/\s+(@!?U?P\w+\s+)?(\S+)", line)
             if m and m.group(2).startswith("U"):
                 n += 1
+    if not found:
+        sys.exit(f"nvcc_pick: kernel {kernel} not in {obj} (Makefile K13_V3 out of date?)")
     return n
 
 
