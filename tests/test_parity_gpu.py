@@ -271,7 +271,8 @@ def test_debug_sync_mode(monkeypatch):
 def test_k4_variants_agree(monkeypatch, CP):
     """The opt-in K4 variants (channel-split walker with the mbarrier ring, FGF_K4_SPLIT; the
     register-prefetch walker, FGF_NO_ASYNC) compute the same per-pixel expression in the same
-    order as the default cp.async walker, and the ungrouped colour box of a, b
+    order as the default cp.async walker (as does the one-pixel-per-thread walker,
+    FGF_K4_PX1), and the ungrouped colour box of a, b
     (FGF_MEAN_NOGROUP) the same sums as the grouped one: identical q, and within tolerance of
     the oracle."""
     g = torch.Generator().manual_seed(31 + CP)
@@ -279,7 +280,7 @@ def test_k4_variants_agree(monkeypatch, CP):
     I = torch.rand((B, 3, H, W), generator=g).cuda()
     p = torch.rand((B, CP, H, W), generator=g).cuda()
     q0 = gpu_filter(I, p, 8, 0.01, 4, 1)
-    for knob in ("FGF_K4_SPLIT", "FGF_NO_ASYNC", "FGF_MEAN_NOGROUP"):
+    for knob in ("FGF_K4_SPLIT", "FGF_NO_ASYNC", "FGF_MEAN_NOGROUP", "FGF_K4_PX1"):
         monkeypatch.setenv(knob, "1")
         q1 = gpu_filter(I, p, 8, 0.01, 4, 1)
         torch.cuda.synchronize()
