@@ -265,7 +265,7 @@ struct StripConfig {
     static constexpr int NMAP = T::NMAP;
     static constexpr int NOUT = T::NOUT;
     static constexpr int NW = NT / 32;
-    static constexpr int VPMAX = NT == 128 ? 256 : (NT == 256 ? 448 : 992);   // worst-case padded row
+    static constexpr int VPMAX = NT == 64 ? 128 : (NT == 128 ? 256 : (NT == 256 ? 448 : 992));   // worst-case padded row
     static constexpr int ROWB = NMAP * VPMAX * 8 + NOUT * NT * 4;
     static constexpr int G0 = (160 * 1024) / ROWB;
     static constexpr int G1 = G0 >= 8 ? 8 : (G0 >= 4 ? 4 : (G0 >= 2 ? 2 : 1));

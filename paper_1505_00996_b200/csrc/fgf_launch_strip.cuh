@@ -66,10 +66,19 @@ int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_
 template <int MODE, int CI, int CP>
 int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
     if constexpr (MODE == MODE_STATS && CI == 3) {
-        // colour statistics (21 / 13 fp64 running sums, ~230 registers): 128-thread CTAs, two
-        // per SM instead of one of 256 -- measured 0.565 -> 0.493 ms (config 3), 0.066 -> 0.060
-        // ms (config 2); FGF_STATS_NT256=1 keeps the plan's width
-        if (getenv("FGF_STATS_NT256") == nullptr && 128 - 2 * P.R >= 64) {
+        // colour statistics (21 / 13 fp64 running sums, ~230 registers): small CTAs, several
+        // per SM instead of one of 256 threads -- 128 threads: 0.565 -> 0.493 ms (config 3),
+        // 0.066 -> 0.060 ms (config 2); 64 threads where r' <= 8: 0.475 ms (config 3);
+        // FGF_STATS_NT256=1 keeps the plan's width
+        const bool keep = getenv("FGF_STATS_NT256") != nullptr;
+        if (!keep && 64 - 2 * P.R >= 48) {       // narrow windows: 64 threads (config 3 0.475 ms)
+            Plan Q = P;
+            Q.nt = 64;
+            Q.TW = std::min(P.w, 64 - 2 * P.R);
+            Q.strips = (P.w + Q.TW - 1) / Q.TW;
+            return launch_strip_t<MODE, CI, CP, 64>(sp, images, Q, st);
+        }
+        if (!keep && 128 - 2 * P.R >= 64) {
             Plan Q = P;
             Q.nt = 128;
             Q.TW = std::min(P.w, 128 - 2 * P.R);
