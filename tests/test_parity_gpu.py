@@ -324,13 +324,15 @@ def test_cuda_graph_capture_and_replay(monkeypatch, cfg, chunk_mb):
 
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_colour_stats_cta_widths_agree(monkeypatch, cfg):
-    """The colour statistics kernel at 128-thread CTAs (default) and at the plan's 256-thread
-    width (FGF_STATS_NT256): both within tolerance of the oracle, and of each other."""
+    """The colour statistics and box-of-a,b kernels at their narrow CTAs (default: 64 / 128
+    threads) and at the plan's 256-thread width (FGF_STATS_NT256, FGF_MEAN_NT256): both within
+    tolerance of the oracle, and of each other."""
     H, W = (300, 400) if cfg == 2 else (270, 480)
     I, p = synth.make_batch(cfg, "cuda", batch=1, H=H, W=W)
     prm = synth.params(cfg)
     q128 = gpu_filter(I, p, **prm)
     monkeypatch.setenv("FGF_STATS_NT256", "1")
+    monkeypatch.setenv("FGF_MEAN_NT256", "1")
     q256 = gpu_filter(I, p, **prm)
     tol = 1e-4 if prm["eps"] >= 1e-3 else 1e-3
     assert compare(I, p, q128, **prm) <= tol
