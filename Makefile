@@ -8,7 +8,8 @@ PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 # one translation unit per kernel family, compiled in parallel (make -j), each in a single
 # ptxas pass: nvcc --split-compile made register allocation depend on the split count
-TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_lowres fgf_k_lowres_v3
+TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_lowres fgf_k_lowres_v3 fgf_k_lowres_v3h \
+       fgf_k_lowres_v3bf fgf_k_lowres_v3b
 OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
 ORACLE := oracle/libfgf_oracle.so
@@ -23,14 +24,19 @@ all: $(LIB) $(ORACLE)
 TUFLAGS_fgf_k_lowres := --split-compile=2
 # the default fp32 variant alone in its unit: its split-compile code does not depend on the
 # other instantiations (adding the 8-bit variants to the shared unit had changed it)
-TUFLAGS_fgf_k_lowres_v3 := --split-compile=2
 
-# the default fp32 K13 variant: the split-compile outcome with its indices on the uniform
-# datapath (tools/nvcc_pick.py; nvcc's split-compile NVVM output varies from run to run)
-K13_V3 := _ZN3fgf18lowres_gray_kernelILi1ELi4ELi9ELi17ELb0ELi160ELi3EfEEvNS_12LowresParamsE
-build/fgf_k_lowres_v3.o: $(PKG)/csrc/fgf_k_lowres_v3.cu $(HDRS) Makefile tools/nvcc_pick.py
+# the default K13 variant, one unit per sample type: the split-compile outcome with its
+# indices on the uniform datapath (tools/nvcc_pick.py; nvcc's split-compile NVVM output varies
+# from run to run)
+K13_SYM = _ZN3fgf18lowres_gray_kernelILi1ELi4ELi9ELi17ELb0ELi160ELi3E$(1)EEvNS_12LowresParamsE
+K13_fgf_k_lowres_v3 := $(call K13_SYM,f)
+K13_fgf_k_lowres_v3h := $(call K13_SYM,6__half)
+K13_fgf_k_lowres_v3bf := $(call K13_SYM,13__nv_bfloat16)
+K13_fgf_k_lowres_v3b := $(call K13_SYM,h)
+PICKED := fgf_k_lowres_v3 fgf_k_lowres_v3h fgf_k_lowres_v3bf fgf_k_lowres_v3b
+$(patsubst %,build/%.o,$(PICKED)): build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile tools/nvcc_pick.py
 	@mkdir -p build
-	python3 tools/nvcc_pick.py --out $@ --kernel $(K13_V3) -- $(NVCC) $(NVFLAGS) $(TUFLAGS_fgf_k_lowres_v3) -c $< 2> build/fgf_k_lowres_v3.ptxas.log || (cat build/fgf_k_lowres_v3.ptxas.log; false)
+	python3 tools/nvcc_pick.py --out $@ --kernel $(K13_$*) -- $(NVCC) $(NVFLAGS) --split-compile=2 -c $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile
 	@mkdir -p build

@@ -17,13 +17,13 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
     if (P.dtype != FGF_F32) {   // reduced-precision inputs: the default variant and the wide one
         const bool h = P.dtype == FGF_F16;
         if (P.dtype == FGF_U8) {
-            if (g.V == 3) return launch_lowres_gray_g<1, 4, 9, 17, false, 160, 3, unsigned char>(lp, g, images, P, st);
+            if (g.V == 3) return launch_lowres_v3<unsigned char>(lp, g, images, P, st);
             if (g.V == 0) return launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, unsigned char>(lp, g, images, P, st);
             return FGF_ERR_UNSUPPORTED;
         }
         if (g.V == 3)
-            return h ? launch_lowres_gray_g<1, 4, 9, 17, false, 160, 3, __half>(lp, g, images, P, st)
-                     : launch_lowres_gray_g<1, 4, 9, 17, false, 160, 3, __nv_bfloat16>(lp, g, images, P, st);
+            return h ? launch_lowres_v3<__half>(lp, g, images, P, st)
+                     : launch_lowres_v3<__nv_bfloat16>(lp, g, images, P, st);
         if (g.V == 0)
             return h ? launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __half>(lp, g, images, P, st)
                      : launch_lowres_gray_g<1, 4, 9, 9, true, 512, 1, __nv_bfloat16>(lp, g, images, P, st);
@@ -33,7 +33,7 @@ int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cud
         case 0: return launch_lowres_gray_g<1, 4, 9, 9>(lp, g, images, P, st);
         case 1: return launch_lowres_gray_g<1, 8, 9, 9>(lp, g, images, P, st);
         case 2: return launch_lowres_gray_g<1, 4, 9, 9, false, 160, 4>(lp, g, images, P, st);
-        case 3: return launch_lowres_v3_f32(lp, g, images, P, st);
+        case 3: return launch_lowres_v3<float>(lp, g, images, P, st);
     }
     return FGF_ERR_UNSUPPORTED;
 }

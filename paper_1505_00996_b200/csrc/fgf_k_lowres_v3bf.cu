@@ -1,5 +1,5 @@
-// fgf_k_lowres_v3.cu -- the default K13 variant (G 4, K 9/17, no sample ring, <= 160 threads x 3 CTAs/SM)
-// for fp32 samples, in a translation unit of its own: built through tools/nvcc_pick.py,
+// fgf_k_lowres_v3bf.cu -- the default K13 variant (G 4, K 9/17, no sample ring, <= 160 threads x 3 CTAs/SM)
+// for bf16 samples, in a translation unit of its own: built through tools/nvcc_pick.py,
 // which keeps the split-compile outcome with the kernel's indices on the uniform datapath
 // (see the Makefile).
 #include "fgf_lowres_launch.cuh"
@@ -11,6 +11,6 @@ int launch_lowres_v3(const LowresParams& lp, const LrGeom& g, int images, const 
                      cudaStream_t st) {
     return launch_lowres_gray_g<1, 4, 9, 17, false, 160, 3, E>(lp, g, images, P, st);
 }
-template int launch_lowres_v3<float>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
+template int launch_lowres_v3<__nv_bfloat16>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
 
 }  // namespace fgf

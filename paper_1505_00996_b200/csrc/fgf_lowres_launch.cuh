@@ -102,8 +102,15 @@ int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, co
     return last_error();
 }
 
-// The default variant for fp32 samples (fgf_k_lowres_v3.cu).
-int launch_lowres_v3_f32(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
-                         cudaStream_t st);
+// The default variant (G 4, K 9/17, no sample ring, <= 160 threads x 3 CTAs/SM) for samples of
+// type E; each element type is instantiated in a translation unit of its own
+// (fgf_k_lowres_v3*.cu, built through tools/nvcc_pick.py).
+template <typename E>
+int launch_lowres_v3(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
+                     cudaStream_t st);
+extern template int launch_lowres_v3<float>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
+extern template int launch_lowres_v3<__half>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
+extern template int launch_lowres_v3<__nv_bfloat16>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
+extern template int launch_lowres_v3<unsigned char>(const LowresParams&, const LrGeom&, int, const Plan&, cudaStream_t);
 
 }  // namespace fgf
