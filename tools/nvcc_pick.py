@@ -41,6 +41,8 @@ def uniform_count(obj, kernel):
 
 def main():
     argv = sys.argv[1:]
+    if "--" not in argv:
+        sys.exit(__doc__)
     k = argv.index("--")
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
