@@ -66,11 +66,14 @@ inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
         if (NT < 64) break;
     }
     if (best.NT == 0) return false;
-    // Segment height: long segments amortise the 2r'+1 warm-up rows (up to 256 rows); small
+    // Segment height: long segments amortise the 2r'+1 warm-up rows (up to h / 2 rows); small
     // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
     const long long cols = (long long)best.strips * images;
     long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
-    th = std::min<long long>(256, std::max<long long>(th, std::max(8, 2 * R + 2)));
+    // (cap: half the image height, at least 256 rows -- config 4 s = 4: 512-row segments
+    // 3.90 -> 3.78 ms; s = 8: 256 (= h / 2) best; whole-image segments were slower)
+    const long long cap = std::max<long long>(256, (h + 1) / 2);
+    th = std::min<long long>(cap, std::max<long long>(th, std::max(8, 2 * R + 2)));
     if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
     if (const char* e = getenv("FGF_LR_V")) {
