@@ -16,12 +16,18 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
     sp.VP = NT + 2 * P.R + C::K + 1;
     const size_t smem = C::smem(sp.VP);
     if (smem > 227 * 1024) return FGF_ERR_UNSUPPORTED;
-    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 4G (and 2R) and 64.
+    // Segment height: ~4 waves of 148 SMs, a multiple of G rows, between 4G (and 2R) and 64
+    // (256 for r' >= 16).
     const long long want = 4LL * 148;
     const long long strips_imgs = (long long)P.strips * images;
     long long th = (P.h * strips_imgs + want - 1) / want;
     th = std::max<long long>(th, std::max(4 * C::G, 2 * P.R));
-    int TH = (int)std::min<long long>(64, th);
+    // wide windows (r' >= 16) amortise their 2r'+1 warm-up rows over taller segments: config 4
+    // s = 1 15.38 -> 14.72 ms per 32 images, s = 2 35.09 -> 34.77 ms per 256 images; narrow
+    // ones keep 64 (config 3's colour statistics are slower with taller segments)
+    long long thmax = P.R >= 16 ? 256 : 64;
+    if (const char* e = getenv("FGF_STRIP_THMAX")) thmax = atoi(e);
+    int TH = (int)std::min<long long>(thmax, th);
     TH = (TH + C::G - 1) / C::G * C::G;
     sp.TH = TH;
     sp.TW = P.TW;
