@@ -54,6 +54,7 @@ def _load():
         lib.fgfo_coefficients.argtypes = [F, F, i, i, i, i, i, i, d, i, i, D, D]
         lib.fgfo_upsample_output.argtypes = [F, D, D, i, i, i, i, i, i]
         lib.fgfo_filter.argtypes = [F, F, D, i, i, i, i, i, i, d, i, i]
+        lib.fgfo_lowres_chain.argtypes = [D, D, i, i, i, i, i, i, d, D]
         _lib = lib
     return _lib
 
@@ -196,21 +197,40 @@ def enhance(I, gain: float, r: int, eps: float, s: int, sub_mode: int = NEAREST)
     return (I.astype(np.float64) - base) * gain + base
 
 
+def lowres_chain(Is, ps, r_low: int, eps: float) -> np.ndarray:
+    """Alg. 2 steps 2-5 on given low-res planes, all in double: Is [B,C_I,h,w],
+    ps [B,C_p,h,w] (any float dtype, widened exactly), radius r_low = r'.  Returns the mean
+    maps [B, C_p, C_I+1, h, w]."""
+    Is = _f64(Is)
+    ps = _f64(ps)
+    B, C_I, h, w = Is.shape
+    C_p = ps.shape[1]
+    if ps.shape[0] != B or ps.shape[2:] != (h, w):
+        raise ValueError("I' and p' shapes disagree")
+    mean_ab = np.empty((B, C_p, C_I + 1, h, w), np.float64)
+    rc = _load().fgfo_lowres_chain(_dptr(Is), _dptr(ps), B, h, w, C_I, C_p, r_low, float(eps),
+                                   _dptr(mean_ab))
+    if rc:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return mean_ab
+
+
 def joint_upsample(I, p_low, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
     """Joint upsampling (R18; the setting P:18 names, no procedure in the paper):
     p is given only at low resolution and IS the p' of Alg. 2; I' = f_sub(I, s), the
     low-res steps run at s = 1 with r' = radius_lowres(r, s), and the output
-    uses the full-resolution I.  I: [B,C_I,H,W]; p_low: [B,C_p,h,w]."""
+    uses the full-resolution I.  I: [B,C_I,H,W]; p_low: [B,C_p,h,w] (fp32 or fp64,
+    used as given).  Every step is in double: I' is not rounded."""
     I = _f32(I)
     if I.ndim == 2:
         I = I[None, None]
-    p_low = _f32(p_low)
+    p_low = _f64(p_low)
     if p_low.ndim == 2:
         p_low = p_low[None, None]
     B, C_I, H, W = I.shape
     Is = np.stack([np.stack([subsample(I[b, c], s, sub_mode) for c in range(C_I)])
-                   for b in range(B)]).astype(np.float32)
+                   for b in range(B)])
     if p_low.shape[2:] != Is.shape[2:]:
         raise ValueError("p_low must be [B, C_p, ceil(H/s), ceil(W/s)]")
-    mean_ab = coefficients(Is, p_low, radius_lowres(r, s), eps, 1, NEAREST)
+    mean_ab = lowres_chain(Is, p_low, radius_lowres(r, s), eps)
     return upsample_output(I, mean_ab, s)

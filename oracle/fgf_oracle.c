@@ -190,39 +190,24 @@ static int check_args(int batch, int H, int W, int C_I, int C_p, int r, double e
     return FGFO_OK;
 }
 
-/* Steps 1-5 of Alg. 2 for one image.  Ip: [C_I][H][W], pp: [C_p][H][W] (float, widened
- * to double).  Outputs low-res maps [C_p][C_I+1][h][w]: for each p channel c the
- * C_I components of a_c (mean_a_c) followed by b_c (mean_b_c).  ab may be NULL. */
-static int coefficients_one(const float* Ip, const float* pp, int H, int W, int C_I, int C_p,
-                            int r, double eps, int s, int sub_mode, double* ab,
-                            double* mean_ab) {
-    const int h = fgfo_lowres_dim(H, s), w = fgfo_lowres_dim(W, s);
-    const int rl = fgfo_radius_lowres(r, s);
-    const size_t N = (size_t)H * W, n = (size_t)h * w;
+/* Steps 2-5 of Alg. 2 for one image, on given fp64 low-res planes
+ * Is: [C_I][h][w] (I') and ps: [C_p][h][w] (p'), radius rl = r'.  Outputs low-res maps
+ * [C_p][C_I+1][h][w]: for each p channel c the C_I components of a_c (mean_a_c) followed
+ * by b_c (mean_b_c).  ab may be NULL. */
+static int lowres_chain_one(const double* Is, const double* ps, int h, int w, int C_I,
+                            int C_p, int rl, double eps, double* ab, double* mean_ab) {
+    const size_t n = (size_t)h * w;
     int rc = FGFO_OK;
 
-    double* full = (double*)malloc(sizeof(double) * N);
-    double* Is = (double*)malloc(sizeof(double) * n * C_I);   /* I' */
-    double* ps = (double*)malloc(sizeof(double) * n * C_p);   /* p' */
     double* tmp = (double*)malloc(sizeof(double) * n);
     double* meanI = (double*)malloc(sizeof(double) * n * C_I);
     double* corrII = (double*)malloc(sizeof(double) * n * C_I * C_I);
     double* meanp = (double*)malloc(sizeof(double) * n);
     double* corrIp = (double*)malloc(sizeof(double) * n * C_I);
     double* coef = (double*)malloc(sizeof(double) * n * (C_I + 1));
-    if (!full || !Is || !ps || !tmp || !meanI || !corrII || !meanp || !corrIp || !coef) {
+    if (!tmp || !meanI || !corrII || !meanp || !corrIp || !coef) {
         rc = FGFO_ENOMEM;
         goto done;
-    }
-
-    /* Step 1: I' = f_subsample(I, s), p' = f_subsample(p, s). */
-    for (int j = 0; j < C_I; ++j) {
-        for (size_t i = 0; i < N; ++i) full[i] = (double)Ip[(size_t)j * N + i];
-        fgfo_subsample(full, H, W, s, sub_mode, Is + (size_t)j * n);
-    }
-    for (int c = 0; c < C_p; ++c) {
-        for (size_t i = 0; i < N; ++i) full[i] = (double)pp[(size_t)c * N + i];
-        fgfo_subsample(full, H, W, s, sub_mode, ps + (size_t)c * n);
     }
 
     /* Step 2 (guidance part): mean_I = f(I'), corr_I = f(I'.*I') (all j,k pairs). */
@@ -277,9 +262,52 @@ static int coefficients_one(const float* Ip, const float* pp, int H, int W, int 
         }
     }
 done:
-    free(full); free(Is); free(ps); free(tmp); free(meanI); free(corrII);
-    free(meanp); free(corrIp); free(coef);
+    free(tmp); free(meanI); free(corrII); free(meanp); free(corrIp); free(coef);
     return rc;
+}
+
+/* Steps 1-5 of Alg. 2 for one image.  Ip: [C_I][H][W], pp: [C_p][H][W] (float, widened
+ * to double).  Step 1 into fp64 planes, then steps 2-5 (lowres_chain_one). */
+static int coefficients_one(const float* Ip, const float* pp, int H, int W, int C_I, int C_p,
+                            int r, double eps, int s, int sub_mode, double* ab,
+                            double* mean_ab) {
+    const int h = fgfo_lowres_dim(H, s), w = fgfo_lowres_dim(W, s);
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+    int rc = FGFO_ENOMEM;
+    double* full = (double*)malloc(sizeof(double) * N);
+    double* Is = (double*)malloc(sizeof(double) * n * C_I);   /* I' */
+    double* ps = (double*)malloc(sizeof(double) * n * C_p);   /* p' */
+    if (full && Is && ps) {
+        /* Step 1: I' = f_subsample(I, s), p' = f_subsample(p, s). */
+        for (int j = 0; j < C_I; ++j) {
+            for (size_t i = 0; i < N; ++i) full[i] = (double)Ip[(size_t)j * N + i];
+            fgfo_subsample(full, H, W, s, sub_mode, Is + (size_t)j * n);
+        }
+        for (int c = 0; c < C_p; ++c) {
+            for (size_t i = 0; i < N; ++i) full[i] = (double)pp[(size_t)c * N + i];
+            fgfo_subsample(full, H, W, s, sub_mode, ps + (size_t)c * n);
+        }
+        rc = lowres_chain_one(Is, ps, h, w, C_I, C_p, fgfo_radius_lowres(r, s), eps, ab, mean_ab);
+    }
+    free(full); free(Is); free(ps);
+    return rc;
+}
+
+/* Steps 2-5 of Alg. 2 over a batch of given fp64 low-res planes
+ * Is [batch][C_I][h][w], ps [batch][C_p][h][w] with radius rl: the low-res chain of joint
+ * upsampling (R18), where p' is an input and I' = f_sub(I, s) stays in double. */
+int fgfo_lowres_chain(const double* Is, const double* ps, int batch, int h, int w, int C_I,
+                      int C_p, int rl, double eps, double* mean_ab) {
+    if (batch < 1 || h < 1 || w < 1 || (C_I != 1 && C_I != 3) || C_p < 1 || C_p > 4 || rl < 1 ||
+        !(eps > 0.0))
+        return FGFO_EINVAL;
+    const size_t n = (size_t)h * w, per = n * (size_t)C_p * (C_I + 1);
+    for (int b = 0; b < batch; ++b) {
+        int rc = lowres_chain_one(Is + (size_t)b * C_I * n, ps + (size_t)b * C_p * n, h, w, C_I,
+                                  C_p, rl, eps, NULL, mean_ab + b * per);
+        if (rc) return rc;
+    }
+    return FGFO_OK;
 }
 
 /* Steps 6-7 for one image: upsample every low-res mean map, then

@@ -369,11 +369,11 @@ def test_joint_upsample_reduces_to_fgf(sub):
     I = rng.random((1, 3, 37, 45)).astype(np.float32)
     p = rng.random((1, 2, 37, 45)).astype(np.float32)
     s, r, eps = 3, 7, 0.01
-    p_low = np.stack([oracle.subsample(p[0, c], s, sub) for c in range(2)])[None].astype(np.float32)
+    p_low = np.stack([oracle.subsample(p[0, c], s, sub) for c in range(2)])[None]   # fp64
     q_joint = oracle.joint_upsample(I, p_low, r, eps, s, sub)
     q_fgf = oracle.fast_guided_filter(I, p, r, eps, s, sub)
-    # nearest: identical samples; block mean: I', p' rounded to fp32 on the joint side
-    assert np.abs(q_joint - q_fgf).max() <= (1e-12 if sub == 0 else 1e-5)
+    # both modes: the same fp64 I', p' on both sides (R18: steps 2-7 unchanged)
+    assert np.abs(q_joint - q_fgf).max() <= 1e-12
 
 
 def test_joint_upsample_constant_input():
