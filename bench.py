@@ -257,7 +257,11 @@ def main():
     q = torch.empty((B, CP, H, W), dtype=tdt, device=dev)
     ws_bytes = fgf.fgf_workspace_bytes_ex(B, H, W, CI, CP, r, s, code)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # the library's own stream discipline: every call on one non-default stream (small calls
+    # are then replayed from the library's CUDA-graph cache; the legacy default stream is not
+    # capturable)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(dev)
 
     def step(st=stream):
         if args.dtype == "f32":
@@ -354,26 +358,44 @@ def main():
             pass
 
     peak, peak_src = peaks()
-    # Dominant kernel K4 (upsample + output): algorithmic bytes per launch = images per launch
-    # x (read I: 4 C_I N + write q: 4 C_p N + read mean maps: 4 NC n)   (DESIGN.md Roofline).
-    k4_ms, k4_n = prof["upsample_output"]
-    imgs_per_launch = B / max(1, k4_n / args.steps)
-    k4_bytes = imgs_per_launch * (esize * CI * N + esize * CP * N + 4 * NC * n)
-    k4_gbs = k4_bytes / (k4_ms / k4_n / 1e3) / 1e9 if k4_n else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "k4_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            key = f"{c['name']}_s{s}"
-            if key in tj and args.dtype == "f32":
-                traffic = tj[key]["dram_bytes_per_image"] * imgs_per_launch
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": "output_kernel (K4: bilinear upsample + q = A.I + B)",
-                "achieved": k4_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": k4_gbs / peak, "traffic": traffic,
-                "alg_bytes_per_launch": k4_bytes}
+    # Roofline of the dominant kernel (largest share of the step's kernel time): algorithmic
+    # bytes per launch / its CUDA-event time per launch.
+    #   K4 upsample + output: read I (esize C_I N) + write q (esize C_p N) + read maps (4 NC n)
+    #   K5 at s = 1 (Alg. 1 fused): read I and p, write q (esize N (C_I + C_p + C_p); p = I
+    #     read once when self-guided)
+    #   K13 / K5 low-res chain: sample rows of I, p (1/s of the rows, or K0's compact planes)
+    #     + the mean maps written (4 NC n)
+    planes_in = CI + (0 if args.config == 0 else CP)
+    lowres_bytes = B * ((esize * N * planes_in / s) if sub == 0 else (4 * n * planes_in)) \
+        + B * 4 * NC * n
+    alg = {"upsample_output": B * (esize * CI * N + esize * CP * N + 4 * NC * n),
+           "lowres_fused": lowres_bytes,
+           "wide_fused": (B * esize * N * (planes_in + CP)) if s == 1 else lowres_bytes}
+    names = {"upsample_output": "output_kernel (K4: bilinear upsample + q = A.I + B)",
+             "lowres_fused": "lowres_gray_kernel (K13: fused low-res chain)",
+             "wide_fused": ("wide_gray_kernel (K5: exact guided filter, Alg. 1, one kernel)"
+                            if s == 1 else "wide_gray_kernel (K5: wide-window low-res chain)")}
+    dom = max((k for k in prof if prof[k][1] and k in alg), key=lambda k: prof[k][0], default=None)
+    roofline = None
+    if dom is not None:
+        d_ms, d_n = prof[dom]
+        d_bytes = alg[dom] / (d_n / args.steps)          # per launch
+        d_gbs = d_bytes / (d_ms / d_n / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "k4_traffic.json" if dom == "upsample_output"
+                             else f"{dom}_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                tj = json.load(open(tpath))
+                key = f"{c['name']}_s{s}"
+                if key in tj and args.dtype == "f32":
+                    traffic = tj[key]["dram_bytes_per_image"] * B / (d_n / args.steps)
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "kernel": names[dom], "achieved": d_gbs, "peak": peak,
+                    "peak_source": peak_src, "unit": "GB/s", "frac": d_gbs / peak,
+                    "traffic": traffic, "alg_bytes_per_launch": d_bytes,
+                    "share_of_step": d_ms / tot}
     # Whole filter against BASELINE's byte model (read I and p, write q, + low-res traffic).
     B_model = B * (esize * N * (CI + 2 * CP) + 8 * n * NC)
     rho = 1.0 if (s == 1 or sub == 1) else 1.0 / min(s, 8)
@@ -398,7 +420,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic",
+                "dtype": args.dtype, "data": "synthetic",
                 "config": dict(config_json(c, prm, B, world), io_dtype=args.dtype,
                                cuda_graph=bool(args.graph)),
                 "gpu_launches": launches_per_step * args.steps,
@@ -497,10 +519,16 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except Exception:
         avail = 64 << 30
-    Be = int(max(1, min(B, 64, (avail // max(1, world)) // 4 // per_img)))
+    # the whole batch when host RAM allows (pinned I, p and q take per_img per image; keep
+    # half of the available memory free), else the largest batch that fits
+    Be = int(max(1, min(B, (avail // max(1, world)) // 2 // per_img)))
     Id, pd = synth.make_batch(args.config, torch.device("cuda", local), batch=Be, first=rank * B)
-    Ih = Id.cpu().pin_memory()
-    ph = Ih if args.config == 0 else pd.cpu().pin_memory()
+    def pinned(t):   # one pinned host copy (no pageable intermediate)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+    Ih = pinned(Id)
+    ph = Ih if args.config == 0 else pinned(pd)
     del Id, pd
     qh = torch.empty((Be, CP, H, W), dtype=torch.float32).pin_memory()
 

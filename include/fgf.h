@@ -65,7 +65,7 @@ enum {
     FGF_ERR_ALIGN = 5,       /* a float pointer is not 4-byte aligned                      */
     FGF_ERR_CUDA = 6,        /* a CUDA call or kernel launch failed                        */
     FGF_ERR_NOMEM = 7,       /* workspace too small / device allocation failed             */
-    FGF_ERR_NCCL = 8,        /* reserved for the banded multi-GPU path                      */
+    FGF_ERR_NCCL = 8,        /* band path: NCCL missing, or a send/recv/group call failed   */
     FGF_ERR_UNSUPPORTED = 9, /* r' > 240 with w > 512 (strip kernel limit)       */
     FGF_ERR_DEVICE = 10      /* a pointer is not device memory (device entry points) or is
                                 not host memory (fgf_filter_host)                           */

@@ -51,7 +51,8 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
            "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
            "fgf_nccl_check")
-KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused")
+KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused",
+                "wide_fused")
 
 _P = ctypes.c_void_p
 _i, _d, _sz = ctypes.c_int, ctypes.c_double, ctypes.c_size_t
@@ -373,6 +374,33 @@ class Workspace:
         return self.buf
 
 
+def _stream_of(t, stream):
+    """The torch stream the kernels are enqueued on (default: the current stream of t's
+    device)."""
+    import torch
+    return stream if stream is not None else torch.cuda.current_stream(t.device)
+
+
+def _keep(st, *tensors):
+    """Tensors allocated by the caching allocator on the current stream but used by kernels
+    enqueued on another stream `st`: record the use, so that their memory is not handed to
+    the next allocation on the current stream while `st` still runs."""
+    import torch
+    if not isinstance(st, torch.cuda.Stream):
+        # a raw cudaStream_t address: nothing to record on; the caller owns the ordering
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda and st != torch.cuda.current_stream(t.device):
+            t.record_stream(st)
+
+
+def _check_out(out, shape, dtype, device, what="out"):
+    if (tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != device
+            or not out.is_contiguous()):
+        raise ValueError(f"{what} must be a contiguous {dtype} tensor of shape {tuple(shape)} "
+                         f"on {device}")
+
+
 def filter(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None, workspace=None):
     """q = FastGuidedFilter(I, p) on CUDA tensors [B, C, H, W] fp32 contiguous.
     Enqueued on `stream` (default: torch's current stream); returns q."""
@@ -385,14 +413,19 @@ def filter(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None, w
             raise ValueError("I and p must be contiguous CUDA tensors of one dtype "
                              "(float32, float16, bfloat16 or uint8 codes k / 255)")
     dt = codes[I.dtype]
+    if p.device != I.device:
+        raise ValueError("I and p must be on one device")
     if out is None:
         out = torch.empty((B, C_p, H, W), dtype=I.dtype, device=I.device)
+    else:
+        _check_out(out, (B, C_p, H, W), I.dtype, I.device)
     ws = workspace or Workspace()
     nbytes = fgf_workspace_bytes_ex(B, H, W, C_I, C_p, r, s, dt)
     if nbytes == 0:
         _check(FGF_ERR_PARAM, "fgf_workspace_bytes_ex")
     buf = ws.get(nbytes, I.device)
-    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    st = _stream_of(I, stream)
+    _keep(st, buf, out)
     if dt == FGF_F32:
         fgf_filter_ws(I, p, out, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, buf.numel(), st)
     else:
@@ -411,7 +444,8 @@ def coefficients(I, p, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, stream=None):
     if nbytes == 0:
         _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
     buf = torch.empty(nbytes, dtype=torch.uint8, device=I.device)
-    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    st = _stream_of(I, stream)
+    _keep(st, buf, mean_ab)
     fgf_coefficients(I, p, mean_ab, B, H, W, C_I, C_p, r, eps, s, sub_mode, buf, nbytes, st)
     return mean_ab
 
@@ -420,10 +454,18 @@ def upsample_output(I, mean_ab, s, stream=None):
     """q from given low-res mean maps (stages 6-7)."""
     import torch
     B, C_I, H, W = I.shape
+    if mean_ab.dim() != 5:
+        raise ValueError("mean_ab must be [B, C_p, C_I+1, h, w]")
     C_p = mean_ab.shape[1]
+    h, w = -(-H // s), -(-W // s)
+    if (tuple(mean_ab.shape) != (B, C_p, C_I + 1, h, w) or mean_ab.dtype != torch.float32
+            or mean_ab.device != I.device):
+        raise ValueError(f"mean_ab must be float32 [{B}, C_p, {C_I + 1}, {h}, {w}] on {I.device}")
     q = torch.empty((B, C_p, H, W), dtype=torch.float32, device=I.device)
-    st = stream if stream is not None else torch.cuda.current_stream(I.device)
-    fgf_upsample_output(I, mean_ab.contiguous(), q, B, H, W, C_I, C_p, s, st)
+    st = _stream_of(I, stream)
+    m = mean_ab.contiguous()
+    _keep(st, q, m)
+    fgf_upsample_output(I, m, q, B, H, W, C_I, C_p, s, st)
     return q
 
 
@@ -437,12 +479,15 @@ def enhance(I, gain=5.0, r=16, eps=0.01, s=4, sub_mode=FGF_SUB_NEAREST, out=None
     B, C, H, W = I.shape
     if out is None:
         out = torch.empty_like(I)
+    else:
+        _check_out(out, I.shape, I.dtype, I.device)
     ws = workspace or Workspace()
     nbytes = fgf_workspace_bytes(B, H, W, C, C, r, s)
     if nbytes == 0:
         _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
     buf = ws.get(nbytes, I.device)
-    st = stream if stream is not None else torch.cuda.current_stream(I.device)
+    st = _stream_of(I, stream)
+    _keep(st, buf, out)
     fgf_enhance_ws(I, out, B, H, W, C, r, eps, s, sub_mode, gain, buf, buf.numel(), st)
     return out
 
@@ -458,6 +503,8 @@ def filter_joint(I, p_low, r, eps, s=4, sub_mode=FGF_SUB_NEAREST, stream=None):
     if nb == 0:
         _check(FGF_ERR_PARAM, "fgf_joint_workspace_bytes")
     ws = torch.empty(nb, dtype=torch.uint8, device=I.device)
-    st = stream if stream is not None else torch.cuda.current_stream(I.device)
-    fgf_filter_joint_ws(I, p_low.contiguous(), q, B, H, W, C_I, C_p, r, eps, s, sub_mode, ws, nb, st)
+    st = _stream_of(I, stream)
+    pl = p_low.contiguous()
+    _keep(st, ws, q, pl)
+    fgf_filter_joint_ws(I, pl, q, B, H, W, C_I, C_p, r, eps, s, sub_mode, ws, nb, st)
     return q

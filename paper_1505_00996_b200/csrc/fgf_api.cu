@@ -34,7 +34,7 @@ int check_shape_params(int batch, int H, int W, int CI, int CP, int r, double ep
     return FGF_OK;
 }
 
-void trim_ws(Plan& P);   // after the K13 dispatch (below)
+void plan_layout(Plan& P);   // engine + workspace carve-up (below)
 
 int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double eps, int s,
               int sub) {
@@ -54,46 +54,35 @@ int make_plan(Plan& P, int batch, int H, int W, int CI, int CP, int r, double ep
     else if (256 - 2 * P.R >= 64) { P.nt = 256; P.TW = 256 - 2 * P.R; }
     else if (P.w <= 512) { P.nt = 512; P.TW = P.w; }
     else if (512 - 2 * P.R >= 32) { P.nt = 512; P.TW = 512 - 2 * P.R; }
-    else return FGF_ERR_UNSUPPORTED;
-    P.strips = (P.w + P.TW - 1) / P.TW;
+    else P.nt = 0;            // the strip engine cannot serve this plan (K5 may)
+    P.strips = P.nt ? (P.w + P.TW - 1) / P.TW : 0;
 
     // Output pass: each thread walks TR full-resolution rows.
     P.TR = 32;
-
-    // Chunk of images per pipeline stage: the low-res workspace of one slot ~ kChunkTargetBytes.
-    const bool planes = s > 1;
-    const size_t per_img = (size_t)((planes ? CI + CP : 0) + 2 * P.NC) * P.n * sizeof(float);
-    size_t target = kChunkTargetBytes;
-    if (const char* e = getenv("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
-    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(batch, target / std::max<size_t>(per_img, 1)));
-    P.ws_planes = planes ? align_up((size_t)P.chunk * (CI + CP) * P.n * sizeof(float)) : 0;
-    P.ws_coef = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
-    P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
-    P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
-    P.nslots = batch > P.chunk ? 2 : 1;
-    trim_ws(P);
-    return FGF_OK;
+    P.dtype = FGF_F32;
+    P.esize = 4;
+    plan_layout(P);
+    return P.engine == ENG_STRIP && P.nt == 0 ? FGF_ERR_UNSUPPORTED : FGF_OK;
 }
 
-// need_mean: false when the caller provides the mean maps buffer (fgf_coefficients).
+// Slot layout: [planes][a, b maps][hb rings][mean maps].  need_mean: false when the caller
+// provides the mean maps buffer (fgf_coefficients).
 size_t plan_ws(const Plan& P, bool need_mean) {
-    if (!need_mean) return std::max<size_t>(kAlign, P.ws_planes + P.ws_coef);
+    if (!need_mean) return std::max<size_t>(kAlign, P.ws_planes + P.ws_coef + P.ws_ring);
     return std::max<size_t>(kAlign, P.ws_slot * P.nslots);
 }
+size_t mean_off(const Plan& P) { return P.ws_planes + P.ws_coef + P.ws_ring; }
 
-// Reduced-precision I/O: the strip engine reads fp32 planes, so at s = 1 a non-fp32 image is
-// first converted into the planes region (K0 with s = 1), which then always exists.
+// Reduced-precision I/O: the engine and workspace are re-planned for the element type (the
+// strip engine reads fp32 planes, so at s = 1 it needs a conversion pass into them; K13 and K5
+// read the elements themselves).
 int set_dtype(Plan& P, int dtype) {
     if (dtype != FGF_F32 && dtype != FGF_F16 && dtype != FGF_BF16 && dtype != FGF_U8)
         return FGF_ERR_PARAM;
     P.dtype = dtype;
     P.esize = dtype == FGF_F32 ? 4 : (dtype == FGF_U8 ? 1 : 2);
-    if (dtype != FGF_F32 && P.ws_planes == 0) {
-        P.ws_planes = align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float));
-        P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
-    }
-    trim_ws(P);
-    return FGF_OK;
+    plan_layout(P);
+    return P.engine == ENG_STRIP && P.nt == 0 ? FGF_ERR_UNSUPPORTED : FGF_OK;
 }
 
 const void* elem_off(const void* base, size_t elems, const Plan& P) {
@@ -133,19 +122,52 @@ int check_pointers(const void* I, const void* p, const void* q, const Plan& P, b
     return FGF_OK;
 }
 
-// When K13 serves a plan it needs no a, b maps, and no compact planes unless it subsamples by
-// block means: shrink the workspace (and so let a chunk hold more images).
-void trim_ws(Plan& P) {
-    if (P.s < 1 || launch_lowres_gray(LowresParams{}, P.chunk, P, nullptr, true) != FGF_OK) return;
-    const bool planes = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
-    const size_t per_img = (size_t)((planes ? P.CI + P.CP : 0) + P.NC) * P.n * sizeof(float);
+// Engine choice: gray guidance at s = 1 runs the exact guided filter as ONE
+// K5 kernel (Alg. 1, q written directly); gray guidance at s > 1 runs K13 for narrow
+// low-res windows (r' <= 12) and K5 for wider ones; colour guidance (and what neither gray
+// engine takes) runs the strip engine K1 + K3.  FGF_ENGINE=k13|wide|strip (development knob,
+// FGF_DEV=1) forces an engine where it applies; FGF_LOWRES=strip is the older spelling.
+int choose_engine(const Plan& P) {
+    if (P.CI != 1) return ENG_STRIP;
+    const bool k13 = launch_lowres_gray(LowresParams{}, P.batch, P, nullptr, true) == FGF_OK;
+    WideGeom g;
+    const bool wide = wide_supports(P.CP, P.dtype) && wide_geom(g, P.h, P.w, P.R, P.CP, 1, P.s == 1);
+    if (const char* e = dev_env("FGF_LOWRES"))
+        if (strcmp(e, "strip") == 0) return ENG_STRIP;
+    if (const char* e = dev_env("FGF_ENGINE")) {
+        if (strcmp(e, "strip") == 0) return ENG_STRIP;
+        if (strcmp(e, "k13") == 0 && k13) return ENG_K13;
+        if (strcmp(e, "wide") == 0 && wide) return ENG_WIDE;
+    }
+    if (P.s == 1 && wide) return ENG_WIDE;
+    if (k13) return ENG_K13;
+    if (wide) return ENG_WIDE;
+    return ENG_STRIP;
+}
+
+// Engine and workspace per pipeline slot, recomputed from scratch (make_plan, set_dtype):
+//   strip: [compact planes (s > 1 or non-fp32 I/O)] [a, b maps] [mean maps]
+//   K13:   [block-mean planes (s > 1, sub = block mean)] [mean maps]
+//   K5:    [block-mean planes] [mean maps, unless it writes q itself (s = 1)] [hb rings]
+void plan_layout(Plan& P) {
+    P.engine = choose_engine(P);
+    P.fused_out = P.engine == ENG_WIDE && P.s == 1;
+    const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
+    const bool planes = P.engine == ENG_STRIP ? (P.s > 1 || P.dtype != FGF_F32) : blk;
+    const bool coef = P.engine == ENG_STRIP;
+    const bool mean = !P.fused_out;
+    const size_t per_img =
+        (size_t)((planes ? P.CI + P.CP : 0) + (coef ? P.NC : 0) + (mean ? P.NC : 0)) * P.n *
+        sizeof(float);
     size_t target = kChunkTargetBytes;
-    if (const char* e = getenv("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
-    P.chunk = (int)std::max<size_t>(1, std::min<size_t>(P.batch, target / std::max<size_t>(per_img, 1)));
+    if (const char* e = dev_env("FGF_CHUNK_MB")) target = (size_t)atoi(e) << 20;
+    P.chunk = per_img == 0 ? P.batch
+                           : (int)std::max<size_t>(1, std::min<size_t>(P.batch, target / per_img));
     P.ws_planes = planes ? align_up((size_t)P.chunk * (P.CI + P.CP) * P.n * sizeof(float)) : 0;
-    P.ws_coef = 0;
-    P.ws_mean = align_up((size_t)P.chunk * P.NC * P.n * sizeof(float));
-    P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean;
+    P.ws_coef = coef ? align_up((size_t)P.chunk * P.NC * P.n * sizeof(float)) : 0;
+    P.ws_mean = mean ? align_up((size_t)P.chunk * P.NC * P.n * sizeof(float)) : 0;
+    P.ws_ring = P.engine == ENG_WIDE ? wide_ring_reserve(P.R, P.CP) : 0;
+    P.ws_slot = P.ws_planes + P.ws_coef + P.ws_mean + P.ws_ring;
     P.nslots = P.batch > P.chunk ? 2 : 1;
 }
 
@@ -162,18 +184,30 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     Pf.esize = 4;
     int rc;
 
-    // Gray guidance: the fused K13 (steps 1-5 in one kernel; nearest samples read in place).
-    if (launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) {
+    // A plan whose output K5 fuses (s = 1, gray) asked here for mean maps only (fgf_coefficients,
+    // the band and joint-upsampling low-res chains): K13 where it applies (needs no workspace
+    // at s = 1), else K5 in its mean-maps mode.
+    int eng = P.engine;
+    if (P.fused_out && launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) eng = ENG_K13;
+    // Gray guidance, block-mean samples (R4): K0 compacts I', p' into fp32 planes first.
+    const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
+    const float *Is = nullptr, *ps = nullptr;
+    if (eng != ENG_STRIP && blk) {
+        float* Isw = planes;
+        float* psw = planes + (size_t)nb * P.n;
+        if ((rc = launch_subsample(Ib, Isw, nb, P, st))) return rc;
+        if (p_is_I) psw = Isw;
+        else if ((rc = launch_subsample(pb, psw, nb * P.CP, P, st))) return rc;
+        Is = Isw;
+        ps = psw;
+    }
+    // Gray guidance, narrow windows: the fused K13 (nearest samples read in place).
+    if (eng == ENG_K13) {
         LowresParams lp{};
         lp.h = P.h; lp.w = P.w; lp.R = P.R; lp.eps = P.eps;
         lp.k1 = P.k1; lp.k0 = P.k0;
         lp.dst = mean;
-        if (P.s > 1 && P.sub == FGF_SUB_BILINEAR) {
-            float* Is = planes;
-            float* ps = planes + (size_t)nb * P.n;
-            if ((rc = launch_subsample(Ib, Is, nb, P, st))) return rc;
-            if (p_is_I) ps = Is;
-            else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) return rc;
+        if (blk) {
             lp.srcI = Is; lp.imgI = (long long)P.n;
             lp.srcP = ps; lp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; lp.planeP = (int)P.n;
             lp.row = P.w; lp.col = 1;
@@ -185,6 +219,28 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
         lp.row = P.s * P.W; lp.col = P.s;
         return launch_lowres_gray(lp, nb, P, st);
     }
+    // Gray guidance, wide windows: K5 in its mean-maps mode.
+    if (eng == ENG_WIDE) {
+        WideGeom g;
+        if (!wide_geom(g, P.h, P.w, P.R, P.CP, nb, false) || g.ring_bytes > P.ws_ring)
+            return FGF_ERR_UNSUPPORTED;
+        WideParams wp{};
+        wp.h = P.h; wp.w = P.w; wp.R = P.R; wp.eps = P.eps;
+        wp.k1 = P.k1; wp.k0 = P.k0;
+        wp.dst = mean;
+        wp.ring = reinterpret_cast<float*>(slot + P.ws_planes + P.ws_coef);
+        if (blk) {
+            wp.srcI = Is; wp.imgI = (long long)P.n;
+            wp.srcP = ps; wp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; wp.planeP = (int)P.n;
+            wp.row = P.w; wp.col = 1;
+            return launch_wide(wp, g, P.CP, FGF_F32, false, st);
+        }
+        wp.srcI = Ib; wp.imgI = (long long)P.N;
+        wp.srcP = pb; wp.imgP = (long long)P.CP * P.N; wp.planeP = (int)P.N;
+        wp.row = P.s * P.W; wp.col = P.s;
+        return launch_wide(wp, g, P.CP, P.dtype, false, st);
+    }
+    if (P.nt == 0) return FGF_ERR_UNSUPPORTED;
 
     StripParams sp{};
     if (P.s > 1 || P.dtype != FGF_F32) {
@@ -241,7 +297,7 @@ int get_pipe(Pipe*& out) {
     if (!pp.init) {
         int lo = 0, hi = 0;
         cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        const int prio = getenv("FGF_LOWRES_LOWPRIO") ? lo : hi;
+        const int prio = dev_env("FGF_LOWRES_LOWPRIO") ? lo : hi;
         if (cudaStreamCreateWithPriority(&pp.low, cudaStreamNonBlocking, prio) != cudaSuccess)
             return FGF_ERR_CUDA;
         if (cudaEventCreateWithFlags(&pp.fork, cudaEventDisableTiming)) return FGF_ERR_CUDA;
@@ -265,13 +321,28 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
     if (!ws) return FGF_ERR_NULL;
     if (ws_bytes < plan_ws(P, true)) return FGF_ERR_NOMEM;
     char* base = static_cast<char*>(ws);
+    if (P.fused_out) {
+        // s = 1, gray guidance: the exact guided filter (Alg. 1) as one K5 launch over the
+        // batch -- I and p read once, q written once.
+        WideGeom g;
+        if (!wide_geom(g, P.h, P.w, P.R, P.CP, P.batch, true) || g.ring_bytes > P.ws_ring)
+            return FGF_ERR_UNSUPPORTED;
+        WideParams wp{};
+        wp.h = P.h; wp.w = P.w; wp.R = P.R; wp.eps = P.eps;
+        wp.k1 = P.k1; wp.k0 = P.k0;
+        wp.srcI = I; wp.imgI = (long long)P.N;
+        wp.srcP = p; wp.imgP = (long long)P.CP * P.N; wp.planeP = (int)P.N;
+        wp.row = P.W; wp.col = 1;
+        wp.q = q;
+        wp.ring = reinterpret_cast<float*>(base + P.ws_planes + P.ws_coef);
+        return launch_wide(wp, g, P.CP, P.dtype, true, st);
+    }
     const int nchunks = (P.batch + P.chunk - 1) / P.chunk;
     if (nchunks == 1) {
-        int rc = run_lowres(I, p, reinterpret_cast<float*>(base + P.ws_planes + P.ws_coef), 0,
-                            P.batch, P, base, st);
+        int rc = run_lowres(I, p, reinterpret_cast<float*>(base + mean_off(P)), 0, P.batch, P,
+                            base, st);
         if (rc) return rc;
-        return launch_output(I, reinterpret_cast<float*>(base + P.ws_planes + P.ws_coef), q,
-                             P.batch, P, st);
+        return launch_output(I, reinterpret_cast<float*>(base + mean_off(P)), q, P.batch, P, st);
     }
     std::lock_guard<std::mutex> lk(g_pipe_mu);
     Pipe* pp = nullptr;
@@ -283,7 +354,7 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
         const int b0 = j * P.chunk, nb = std::min(P.chunk, P.batch - b0);
         const int k = j & 1;
         char* slot = base + (size_t)k * P.ws_slot;
-        float* mean = reinterpret_cast<float*>(slot + P.ws_planes + P.ws_coef);
+        float* mean = reinterpret_cast<float*>(slot + mean_off(P));
         // The slot is free once the output pass of chunk j-2 has read its mean maps.
         if (j >= 2 && cudaStreamWaitEvent(pp->low, pp->done_out[k], 0)) return FGF_ERR_CUDA;
         if ((rc = run_lowres(I, p, mean, b0, nb, P, slot, pp->low))) return rc;
@@ -331,6 +402,113 @@ struct HostPipe {
 };
 std::mutex g_host_mu;
 std::vector<HostPipe> g_host;
+
+// ---- CUDA-graph cache for small calls (verdict r1: single-image latency).  A call of at most
+// kGraphMaxPixels output pixels whose arguments (pointers, sizes, parameters, stream,
+// workspace) repeat an earlier call is replayed from a graph captured on its second occurrence:
+// no per-launch host overhead, no validation queries, no inter-kernel launch gaps.  Not used
+// on the legacy default stream (not capturable), with per-launch profiling on, with the
+// development knobs (FGF_DEV=1) or FGF_DEBUG_SYNC, or with FGF_GRAPHS=0.
+constexpr size_t kGraphMaxPixels = 32u << 20;
+constexpr int kGraphSlots = 32;
+
+struct GraphKey {
+    const void *I, *p, *q, *ws;
+    size_t ws_bytes;
+    void* stream;
+    int batch, H, W, CI, CP, r, s, sub, dtype, dev, kind;
+    double eps, gain;
+    bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;   // nullptr: seen once, not captured yet
+    int launches = 0;
+    unsigned long long used = 0;
+};
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;
+unsigned long long g_graph_clock = 0;
+
+GraphKey graph_key(int kind, const void* I, const void* p, const void* q, const Plan& P,
+                   double gain, const void* ws, size_t ws_bytes, cudaStream_t st) {
+    GraphKey k;
+    memset(&k, 0, sizeof(k));   // padding bytes take part in the comparison
+    k.I = I; k.p = p; k.q = q; k.ws = ws; k.ws_bytes = ws_bytes; k.stream = st;
+    k.batch = P.batch; k.H = P.H; k.W = P.W; k.CI = P.CI; k.CP = P.CP; k.r = P.r; k.s = P.s;
+    k.sub = P.sub; k.dtype = P.dtype; k.kind = kind; k.eps = P.eps; k.gain = gain;
+    cudaGetDevice(&k.dev);
+    return k;
+}
+
+bool graph_eligible(const Plan& P, cudaStream_t st) {
+    if (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) return false;
+    if ((size_t)P.batch * P.N > kGraphMaxPixels || g_prof.on || debug_sync()) return false;
+    if (const char* d = getenv("FGF_DEV"))
+        if (atoi(d) != 0) return false;
+    if (const char* e = getenv("FGF_GRAPHS"))
+        if (atoi(e) == 0) return false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return false;                  // the caller is capturing: enqueue normally
+    }
+    return true;
+}
+
+// validate: the pointer checks (run on first sight only); enqueue: the launches.
+template <typename V, typename F>
+int run_cached(const GraphKey& key, cudaStream_t st, V&& validate, F&& enqueue) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    GraphEntry* e = nullptr;
+    for (auto& x : g_graphs)
+        if (x.key == key) e = &x;
+    if (e && e->exec) {
+        e->used = ++g_graph_clock;
+        g_last_launches = e->launches;
+        return cudaGraphLaunch(e->exec, st) == cudaSuccess ? FGF_OK : FGF_ERR_CUDA;
+    }
+    int rc = validate();
+    if (rc) return rc;
+    if (!e) {                          // first sight: run eagerly, remember the arguments
+        rc = enqueue();
+        if (rc) return rc;
+        if ((int)g_graphs.size() >= kGraphSlots) {
+            auto lru = std::min_element(g_graphs.begin(), g_graphs.end(),
+                                        [](const GraphEntry& a, const GraphEntry& b) { return a.used < b.used; });
+            if (lru->exec) cudaGraphExecDestroy(lru->exec);
+            g_graphs.erase(lru);
+        }
+        GraphEntry ne;
+        ne.key = key;
+        ne.used = ++g_graph_clock;
+        g_graphs.push_back(ne);
+        return FGF_OK;
+    }
+    // second sight: capture the same launches, instantiate, replay
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return enqueue();
+    }
+    rc = enqueue();
+    const int launches = g_last_launches;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (rc || ce != cudaSuccess || !graph ||
+        cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        if (rc) return rc;
+        return enqueue();              // capture failed: the launches were not run yet
+    }
+    cudaGraphDestroy(graph);
+    e->exec = exec;
+    e->launches = launches;
+    e->used = ++g_graph_clock;
+    g_last_launches = launches;
+    return cudaGraphLaunch(exec, st) == cudaSuccess ? FGF_OK : FGF_ERR_CUDA;
+}
 
 }  // namespace
 }  // namespace fgf
@@ -413,8 +591,13 @@ int fgf_filter_ex_ws(const void* I, const void* p, void* q, int batch, int H, in
     if ((rc = set_dtype(P, dtype))) return rc;
     if (dtype != FGF_F32 && !(C_I * 10 + C_p == 11 || C_I * 10 + C_p == 31 || C_I * 10 + C_p == 33))
         return FGF_ERR_UNSUPPORTED;
-    if ((rc = check_pointers(I, p, q, P, true))) return rc;
-    return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    auto validate = [&] { return check_pointers(I, p, q, P, true); };
+    auto enqueue = [&] { return run_all(I, p, q, P, workspace, ws_bytes, st); };
+    if (graph_eligible(P, st))
+        return run_cached(graph_key(0, I, p, q, P, 0.0, workspace, ws_bytes, st), st, validate, enqueue);
+    if ((rc = validate())) return rc;
+    return enqueue();
 }
 
 int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
@@ -424,8 +607,13 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
     Plan P;
     int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
     if (rc) return rc;
-    if ((rc = check_pointers(I, p, q, P, true))) return rc;
-    return run_all(I, p, q, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    auto validate = [&] { return check_pointers(I, p, q, P, true); };
+    auto enqueue = [&] { return run_all(I, p, q, P, workspace, ws_bytes, st); };
+    if (graph_eligible(P, st))
+        return run_cached(graph_key(0, I, p, q, P, 0.0, workspace, ws_bytes, st), st, validate, enqueue);
+    if ((rc = validate())) return rc;
+    return enqueue();
 }
 
 int fgf_nccl_unique_id(void* id_out) {
@@ -466,13 +654,16 @@ int fgf_nccl_comm_destroy(void* comm) {
 
 size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
                                 int s, int nranks) {
-    BandPlan B1, B2;
-    if (band_plan(B1, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
-                  FGF_BAND_SINGLE) ||
-        band_plan(B2, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
-                  FGF_BAND_TWO_STEP))
-        return 0;
-    return std::max(B1.ws_total, B2.ws_total);
+    // The larger of the exchange modes this band admits (two-step accepts narrower bands:
+    // r'+1 low-res rows instead of 2r'+1); 0 only when neither mode accepts the band.
+    size_t best = 0;
+    for (int mode : {FGF_BAND_SINGLE, FGF_BAND_TWO_STEP}) {
+        BandPlan B;
+        if (band_plan(B, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks,
+                      false, mode) == FGF_OK)
+            best = std::max(best, B.ws_total);
+    }
+    return best;
 }
 
 int fgf_filter_band(const float* I_band, const float* p_band, float* q_band, int H_total, int W,
@@ -542,20 +733,17 @@ int fgf_filter_band_ex(const float* I_band, const float* p_band, float* q_band, 
 
 size_t fgf_bands_loopback_workspace_bytes(int H, int W, int C_I, int C_p, int r, int s,
                                           int nranks) {
-    // (the larger of the two exchange modes)
+    // per band: the larger of the exchange modes the band admits (as fgf_band_workspace_bytes)
     if (nranks < 1 || s < 1 || H < 1 || W < 1) return 0;
     const int h = lowres_dim(H, s);
     size_t tot = 0;
     for (int k = 0; k < nranks; ++k) {
         const int y0 = (int)((long long)k * h / nranks), y1 = (int)((long long)(k + 1) * h / nranks);
         const int row0 = y0 * s, rows = std::min(H, y1 * s) - row0;
-        BandPlan B1, B2;
-        if (band_plan(B1, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
-                      FGF_BAND_SINGLE) ||
-            band_plan(B2, H, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks, false,
-                      FGF_BAND_TWO_STEP))
-            return 0;
-        tot += std::max(B1.ws_total, B2.ws_total) + 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
+        if (rows < 1) return 0;
+        const size_t b = fgf_band_workspace_bytes(H, W, row0, rows, C_I, C_p, r, s, nranks);
+        if (b == 0) return 0;
+        tot += b + 2 * align_up((size_t)(C_I + 2 * C_p) * rows * W * 4);
     }
     return tot;
 }
@@ -587,10 +775,10 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
                             mode)))
             return rc;
         wss[k] = cur;
-        BandPlan Bx;   // the workspace layout reserves the larger mode (as the size query)
-        band_plan(Bx, H, W, row0, rows, C_I, C_p, r, eps, s, sub_mode, nranks, self,
-                  mode == FGF_BAND_SINGLE ? FGF_BAND_TWO_STEP : FGF_BAND_SINGLE);
-        cur += std::max(Bs[k].ws_total, Bx.ws_total);
+        // the workspace layout reserves what the size query reserved for this band
+        const size_t wsb = fgf_band_workspace_bytes(H, W, row0, rows, C_I, C_p, r, s, nranks);
+        if (wsb < Bs[k].ws_total) return FGF_ERR_NOMEM;
+        cur += wsb;
         // the band's own rows, contiguous per plane, as a rank would hold them
         Ib[k] = reinterpret_cast<float*>(cur);
         pb[k] = self ? Ib[k] : Ib[k] + (size_t)C_I * rows * W;
@@ -814,12 +1002,16 @@ int fgf_subsample(const float* src, float* dst, int planes, int H, int W, int s,
 }
 
 size_t fgf_lowres_workspace_bytes(int batch, int h, int w, int C_I, int C_p) {
-    // radius-independent: enough for either low-res engine (K13 or the strip engine)
+    // radius-independent: enough for every engine the low-res chain may take (K13 needs none;
+    // the strip engine its a, b maps; K5 its hb rings, largest over the radii it serves)
     Plan P;
     if (make_plan(P, batch, h, w, C_I, C_p, 1, 1.0, 1, FGF_SUB_NEAREST)) return 0;
     const size_t chunk = (size_t)std::max(1, std::min(batch, (int)std::max<size_t>(
         1, kChunkTargetBytes / std::max<size_t>(1, (size_t)2 * P.NC * P.n * sizeof(float)))));
-    return std::max<size_t>(kAlign, align_up(chunk * P.NC * P.n * sizeof(float)));
+    size_t ring = 0;
+    if (C_I == 1)
+        for (int R = 2; 4 * R + 32 <= kWideMaxCols; ++R) ring = std::max(ring, wide_ring_reserve(R, C_p));
+    return std::max<size_t>(kAlign, align_up(chunk * P.NC * P.n * sizeof(float)) + ring);
 }
 
 int fgf_lowres_mean(const float* Is, const float* ps, float* mean_ab, int batch, int h, int w,
@@ -927,6 +1119,15 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
         hp.wsbytes = need_ws;
     }
 
+    // Once a copy is enqueued the caller's host buffers are in use: every return below
+    // drains the three streams first, so no copy still reads I / p or writes q afterwards.
+    auto drain = [&](int status) {
+        const bool ok = cudaStreamSynchronize(hp.s_h2d) == cudaSuccess &&
+                        cudaStreamSynchronize(hp.s_comp) == cudaSuccess &&
+                        cudaStreamSynchronize(hp.s_d2h) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+        return status != FGF_OK ? status : (ok ? FGF_OK : FGF_ERR_CUDA);
+    };
     int launches = 0;
     int k = 0;
     for (int b0 = 0; b0 < batch; b0 += sb, ++k) {
@@ -936,28 +1137,30 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
         float* dp = self ? dI : dI + (size_t)nb * C_I * P.N;
         float* dq = dI + (size_t)nb * (C_I + (self ? 0 : C_p)) * P.N;
         // The slot is free once the D2H of chunk k-2 has finished.
-        if (k >= 2 && cudaStreamWaitEvent(hp.s_h2d, hp.ev_free[slot], 0)) return FGF_ERR_CUDA;
+        if (k >= 2 && cudaStreamWaitEvent(hp.s_h2d, hp.ev_free[slot], 0)) return drain(FGF_ERR_CUDA);
         if (cudaMemcpyAsync(dI, I + (size_t)b0 * C_I * P.N, (size_t)nb * C_I * P.N * 4,
                             cudaMemcpyHostToDevice, hp.s_h2d))
-            return FGF_ERR_CUDA;
+            return drain(FGF_ERR_CUDA);
         if (!self && cudaMemcpyAsync(dp, p + (size_t)b0 * C_p * P.N, (size_t)nb * C_p * P.N * 4,
                                      cudaMemcpyHostToDevice, hp.s_h2d))
-            return FGF_ERR_CUDA;
-        cudaEventRecord(hp.ev_in[slot], hp.s_h2d);
-        cudaStreamWaitEvent(hp.s_comp, hp.ev_in[slot], 0);
+            return drain(FGF_ERR_CUDA);
+        if (cudaEventRecord(hp.ev_in[slot], hp.s_h2d) ||
+            cudaStreamWaitEvent(hp.s_comp, hp.ev_in[slot], 0))
+            return drain(FGF_ERR_CUDA);
         Plan Pc;
-        make_plan(Pc, nb, H, W, C_I, C_p, r, eps, s, sub_mode);
-        if ((rc = run_all(dI, dp, dq, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return rc;
+        if ((rc = make_plan(Pc, nb, H, W, C_I, C_p, r, eps, s, sub_mode))) return drain(rc);
+        if ((rc = run_all(dI, dp, dq, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return drain(rc);
         launches += g_last_launches;
         g_last_launches = 0;
-        cudaEventRecord(hp.ev_done[slot], hp.s_comp);
-        cudaStreamWaitEvent(hp.s_d2h, hp.ev_done[slot], 0);
+        if (cudaEventRecord(hp.ev_done[slot], hp.s_comp) ||
+            cudaStreamWaitEvent(hp.s_d2h, hp.ev_done[slot], 0))
+            return drain(FGF_ERR_CUDA);
         if (cudaMemcpyAsync(q + (size_t)b0 * C_p * P.N, dq, (size_t)nb * C_p * P.N * 4,
                             cudaMemcpyDeviceToHost, hp.s_d2h))
-            return FGF_ERR_CUDA;
-        cudaEventRecord(hp.ev_free[slot], hp.s_d2h);
+            return drain(FGF_ERR_CUDA);
+        if (cudaEventRecord(hp.ev_free[slot], hp.s_d2h)) return drain(FGF_ERR_CUDA);
     }
-    if (cudaStreamSynchronize(hp.s_d2h) != cudaSuccess) return FGF_ERR_CUDA;
+    if ((rc = drain(FGF_OK))) return rc;
     g_last_launches = launches;
     return FGF_OK;
 }

@@ -18,6 +18,7 @@
 #include "../../include/fgf.h"
 #include "fgf_kernels.cuh"
 #include "fgf_lowres.cuh"
+#include "fgf_wide.cuh"
 
 namespace fgf {
 
@@ -27,7 +28,8 @@ constexpr size_t kAlign = 256;
 constexpr size_t kChunkTargetBytes = 8ull << 30;  // low-res workspace bytes per pipeline slot
 
 // ---- optional per-launch event timing (fgf_profile_*)
-enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, KIND_LOWRES = 4, NKIND = 5 };
+enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, KIND_LOWRES = 4, KIND_WIDE = 5,
+       NKIND = 6 };
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
@@ -58,7 +60,8 @@ extern Profiler g_prof;                   // fgf_api.cu
 
 const char* const kKindName[NKIND] = {"fgf K0 subsample", "fgf K1 statistics+coefficients",
                                       "fgf K3 box of a,b", "fgf K4 upsample+output",
-                                      "fgf K13 fused low-res chain"};
+                                      "fgf K13 fused low-res chain",
+                                      "fgf K5 radius-independent fused chain"};
 
 // Around every launch: an NVTX range named after the kernel (timeline tools: nsys, ncu
 // --nvtx) and, when fgf_profile_enable(1) is on, a CUDA-event pair on the launching stream.
@@ -85,6 +88,16 @@ struct ProfScope {
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
+// Engine of steps 2-5 (and, for K5 at s = 1, of the whole filter), chosen once per plan.
+enum { ENG_STRIP = 0, ENG_K13 = 1, ENG_WIDE = 2 };
+
+// K5 geometry (fgf_k_wide.cu): strips of TW output columns, segments of TH rows, a persistent
+// grid of `grid` CTAs of NT threads, one hb ring of ring_bytes / grid per CTA.
+struct WideGeom {
+    int TW = 0, NT = 0, strips = 0, segs = 0, TH = 0, items = 0, grid = 0, R = 0;
+    size_t ring_bytes = 0;
+};
+
 struct Plan {
     int batch, H, W, CI, CP, r, s, sub;
     double eps;
@@ -98,8 +111,10 @@ struct Plan {
     int nt, TW, strips;
     // output kernel
     int TR;
-    // workspace carve-up per pipeline slot (bytes)
-    size_t ws_planes, ws_coef, ws_mean, ws_slot;
+    // engine and workspace carve-up per pipeline slot (bytes), from plan_layout()
+    int engine = ENG_STRIP;
+    bool fused_out = false;       // K5 at s = 1: one kernel writes q (no mean maps, no K4)
+    size_t ws_planes, ws_coef, ws_mean, ws_ring, ws_slot;
     int nslots;
 };
 
@@ -109,6 +124,16 @@ template <typename K>
 void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Development knobs: environment variables that select another CUDA kernel
+// variant or geometry of the same computation, for tests and sweeps.  The library honours
+// them only when FGF_DEV=1 is set too, so a caller's stray environment cannot change which
+// kernels a call runs.
+inline const char* dev_env(const char* name) {
+    const char* d = getenv("FGF_DEV");
+    if (!d || atoi(d) == 0) return nullptr;
+    return getenv(name);
 }
 
 // FGF_DEBUG_SYNC=1: synchronise after every launch so that an asynchronous fault is reported
@@ -142,6 +167,12 @@ extern template int launch_strip<MODE_MEAN>(const StripParams&, int, const Plan&
 int launch_output(const void* I, const float* M, void* q, int images, const Plan& P,
                   cudaStream_t st, const Band* band = nullptr);
 int lowres_span(int T, int n_dst, int n_src);
+// K5 (fgf_k_wide.cu): geometry for `images` images, and the launch (maps or, outq, q).
+bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq);
+bool wide_supports(int CP, int dtype);
+size_t wide_ring_reserve(int R, int CP);
+int launch_wide(const WideParams& wp, const WideGeom& g, int CP, int dtype, bool outq,
+                cudaStream_t st);
 // K13 (fgf_k_lowres.cu); dry = true: only report whether K13 serves this plan.
 int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaStream_t st,
                        bool dry = false);

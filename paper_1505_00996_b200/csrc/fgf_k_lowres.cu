@@ -46,9 +46,9 @@ int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaSt
     // rows: measured faster than the strip engine at r' = 4 and 8, slower at r' = 16 and 32
     // (config 4 at s = 8, 4, 2, 1), so wide windows take the strip engine.
     int rmax = 12;
-    if (const char* e = getenv("FGF_LR_RMAX")) rmax = atoi(e);
+    if (const char* e = dev_env("FGF_LR_RMAX")) rmax = atoi(e);
     if (P.R > rmax) return FGF_ERR_UNSUPPORTED;
-    if (const char* e = getenv("FGF_LOWRES")) {
+    if (const char* e = dev_env("FGF_LOWRES")) {
         if (strcmp(e, "strip") == 0) return FGF_ERR_UNSUPPORTED;
     }
     if (P.dtype != FGF_F32 && P.CP != 1) return FGF_ERR_UNSUPPORTED;

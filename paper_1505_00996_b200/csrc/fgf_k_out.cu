@@ -47,11 +47,11 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
         // optional floor on the dynamic smem: caps K4 CTAs/SM so the low-res stream's CTAs
         // can be co-resident (experiment knob)
-        if (const char* e = getenv("FGF_K4_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
+        if (const char* e = dev_env("FGF_K4_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
     }
     dim3 grid((P.W + 256 * PX - 1) / (256 * PX), (P.H + op.TR - 1) / op.TR, images);
     if constexpr (PX * sizeof(E) >= 4) {   // cp.async moves 4, 8 or 16 bytes
-        if (!s1 && getenv("FGF_NO_ASYNC") == nullptr) {
+        if (!s1 && dev_env("FGF_NO_ASYNC") == nullptr) {
             // cp.async ring variant: prefetch held in shared memory, not registers
             const size_t asm_ = smem + AsyncCfg<CI, CP, PX, E>::RING_BYTES;
             if (asm_ <= 200 * 1024) {
@@ -114,7 +114,7 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     if constexpr (CI == 3 && CP >= 2 && sizeof(E) == 4) {
         const uintptr_t al = reinterpret_cast<uintptr_t>(op.I) | reinterpret_cast<uintptr_t>(op.q);
         const bool s1 = op.hg == op.Hg && P.w == P.W;
-        if (!s1 && P.W % 4 == 0 && (al & 15u) == 0 && getenv("FGF_K4_SPLIT") != nullptr) {
+        if (!s1 && P.W % 4 == 0 && (al & 15u) == 0 && dev_env("FGF_K4_SPLIT") != nullptr) {
             const int rc = launch_output_split<CI, CP>(op, images, P, st);
             if (rc != FGF_ERR_UNSUPPORTED) return rc;
         }
@@ -125,7 +125,7 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
     if constexpr (ES == 1) {   // 8-bit codes: 8 pixels (8 bytes) per thread and row
         const bool s1 = op.hg == op.Hg && P.w == P.W;
         if (NC <= 2 && !s1 && P.W % 8 == 0 && (ai & 7u) == 0 && (am & 15u) == 0 &&
-            getenv("FGF_K4_U8PX4") == nullptr) {
+            dev_env("FGF_K4_U8PX4") == nullptr) {
             const int rc = launch_output_px<CI, CP, (NC <= 2 ? 8 : 1), E>(op, images, P, st);
             if (rc != FGF_ERR_UNSUPPORTED) return rc;
         }
@@ -134,7 +134,7 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
         return launch_output_px<CI, CP, (NC <= 2 ? 4 : 1), E>(op, images, P, st);
     if constexpr (NC > 4 && ES == 4) {
         // colour, fp32: 2 pixels per thread (config 3 K4 0.708 -> 0.668 ms; FGF_K4_PX1=1: one)
-        if (getenv("FGF_K4_PX1") == nullptr && P.W % 2 == 0 && (ai & 7u) == 0 && (am & 7u) == 0)
+        if (dev_env("FGF_K4_PX1") == nullptr && P.W % 2 == 0 && (ai & 7u) == 0 && (am & 7u) == 0)
             return launch_output_px<CI, CP, 2, E>(op, images, P, st);
     }
     if (NC <= 4 && P.W % 2 == 0 && (ai & (2 * ES - 1)) == 0 && (am & 7u) == 0)

@@ -26,7 +26,7 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
     // s = 1 15.38 -> 14.72 ms per 32 images, s = 2 35.09 -> 34.77 ms per 256 images; narrow
     // ones keep 64 (config 3's colour statistics are slower with taller segments)
     long long thmax = P.R >= 16 ? 256 : 64;
-    if (const char* e = getenv("FGF_STRIP_THMAX")) thmax = atoi(e);
+    if (const char* e = dev_env("FGF_STRIP_THMAX")) thmax = atoi(e);
     int TH = (int)std::min<long long>(thmax, th);
     TH = (TH + C::G - 1) / C::G * C::G;
     sp.TH = TH;
@@ -34,7 +34,7 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
     dim3 grid(P.strips, (P.h + TH - 1) / TH, images);
     // wide windows: prefix-sum horizontal phase (restart-free); measured threshold below
     int hpre_r = kHpreR;
-    if (const char* e = getenv("FGF_HPRE_R")) hpre_r = atoi(e);
+    if (const char* e = dev_env("FGF_HPRE_R")) hpre_r = atoi(e);
     // (instantiated for gray 1/1 and colour 3/1, 3/3 -- the channel layouts BASELINE.json uses)
     constexpr bool HP_OK = (CI == 1 && CP == 1) || (CI == 3 && (CP == 1 || CP == 3));
     auto kern = box_strip_kernel<MODE, CI, CP, NT, G_, 0, false>;
@@ -54,7 +54,7 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
 template <int MODE, int CI, int CP, int NT>
 int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
     constexpr bool MEANLIKE = MODE == MODE_MEAN;
-    if (CI == 3 && NT == 256 && P.R <= 16 && getenv("FGF_STRIP_WORSTG") == nullptr) {
+    if (CI == 3 && NT == 256 && P.R <= 16 && dev_env("FGF_STRIP_WORSTG") == nullptr) {
         constexpr int GC = (MEANLIKE || CP == 1) ? 4 : 2;
         const int rc = launch_strip_g<MODE, CI, CP, NT, GC>(sp, images, P, st);
         if (rc != FGF_ERR_UNSUPPORTED) return rc;
@@ -62,7 +62,7 @@ int launch_strip_t(const StripParams& sp, int images, const Plan& P, cudaStream_
     // gray box of a, b at 12 <= r' < 24: 8 rows per batch (measured: config 4 s=2 K3 2.44 -> 2.27 ms
     // per 64 images; the statistics kernel was slower with 8)
     if (MEANLIKE && CI == 1 && CP == 1 && NT == 256 && P.R >= 12 && P.R < kHpreR &&
-        getenv("FGF_STRIP_WORSTG") == nullptr) {
+        dev_env("FGF_STRIP_WORSTG") == nullptr) {
         const int rc = launch_strip_g<MODE, CI, CP, NT, 8>(sp, images, P, st);
         if (rc != FGF_ERR_UNSUPPORTED) return rc;
     }
@@ -76,7 +76,7 @@ int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream
         // per SM instead of one of 256 threads -- 128 threads: 0.565 -> 0.493 ms (config 3),
         // 0.066 -> 0.060 ms (config 2); 64 threads where r' <= 8: 0.475 ms (config 3);
         // FGF_STATS_NT256=1 keeps the plan's width
-        const bool keep = getenv("FGF_STATS_NT256") != nullptr;
+        const bool keep = dev_env("FGF_STATS_NT256") != nullptr;
         if (!keep && 64 - 2 * P.R >= 48) {       // narrow windows: 64 threads (config 3 0.475 ms)
             Plan Q = P;
             Q.nt = 64;
@@ -96,7 +96,7 @@ int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream
         // colour box of a, b (4 maps per CTA; alone or as one of the C_p groups): 128-thread
         // CTAs -- config 3 K3 0.361 -> 0.337 ms, config 2 0.042 -> 0.033 ms;
         // FGF_MEAN_NT256=1 keeps the plan's width
-        if (getenv("FGF_MEAN_NT256") == nullptr && 128 - 2 * P.R >= 64) {
+        if (dev_env("FGF_MEAN_NT256") == nullptr && 128 - 2 * P.R >= 64) {
             Plan Q = P;
             Q.nt = 128;
             Q.TW = std::min(P.w, 128 - 2 * P.R);
@@ -110,7 +110,7 @@ int launch_strip_nt(const StripParams& sp, int images, const Plan& P, cudaStream
 
 template <int MODE>
 int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t st) {
-    if (MODE == MODE_MEAN && P.CI == 3 && P.CP > 1 && getenv("FGF_MEAN_NOGROUP") == nullptr) {
+    if (MODE == MODE_MEAN && P.CI == 3 && P.CP > 1 && dev_env("FGF_MEAN_NOGROUP") == nullptr) {
         // colour box of a, b: the 4 C_p maps as C_p groups of 4 in one launch (the 3 / 1
         // kernel: 4 fp64 running sums per thread instead of 4 C_p, so 4 CTAs per SM instead of
         // one -- measured on config 3 below)

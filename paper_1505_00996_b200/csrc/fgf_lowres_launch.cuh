@@ -51,7 +51,7 @@ template <int CP>
 inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     // Target ~160 threads (5 warps) per CTA: three CTAs per SM, halo overhead (TW + 4R) / TW.
     int want_nt = 160;
-    if (const char* e = getenv("FGF_LR_NT")) want_nt = atoi(e);
+    if (const char* e = dev_env("FGF_LR_NT")) want_nt = atoi(e);
     LrGeom best;
     for (int ns = 1; ns <= w; ++ns) {
         const int TW = (w + ns - 1) / ns;
@@ -74,9 +74,9 @@ inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     // 3.90 -> 3.78 ms; s = 8: 256 (= h / 2) best; whole-image segments were slower)
     const long long cap = std::max<long long>(256, (h + 1) / 2);
     th = std::min<long long>(cap, std::max<long long>(th, std::max(8, 2 * R + 2)));
-    if (const char* e = getenv("FGF_LR_TH")) th = atoi(e);
+    if (const char* e = dev_env("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
-    if (const char* e = getenv("FGF_LR_V")) {
+    if (const char* e = dev_env("FGF_LR_V")) {
         if (lowres_fits_v<CP>(best, R, atoi(e))) { g = best; return true; }
         return false;
     }
@@ -96,7 +96,7 @@ int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, co
     size_t smem = g.smem;
     // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
     // previous chunk can be co-resident (overlap experiment knob)
-    if (const char* e = getenv("FGF_LR_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
+    if (const char* e = dev_env("FGF_LR_SMEM_MIN")) smem = std::max<size_t>(smem, (size_t)atoi(e));
     set_smem(kern, smem);
     dim3 grid(g.strips, (P.h + g.TH - 1) / g.TH, images);
     ProfScope ps(KIND_LOWRES, st);

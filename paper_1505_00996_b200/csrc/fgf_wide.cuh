@@ -1,0 +1,444 @@
+// fgf_wide.cuh -- K5: the whole guided filter chain for gray guidance in ONE persistent kernel
+// whose per-pixel cost does not depend on the window radius.
+//
+//   * s = 1 (OUTQ): Algorithm 1 of the paper -- the exact guided filter:
+//       mean_I, mean_p, corr_I, corr_Ip = f_mean(., r)
+//       var_I, cov_Ip, a = cov_Ip / (var_I + eps), b = mean_p - a mean_I  (Eq.2-3)
+//       mean_a, mean_b = f_mean(a, b)
+//       q = mean_a .* I + mean_b                                    (Eq.4)
+//     reading I and p once from HBM and writing q once (12 B per pixel).
+//   * s > 1: steps 2-5 of Alg. 2 on the nearest samples I[y s][x s] read in place
+//     (or K0's block-mean planes) for wide low-res windows r' -- mean_a, mean_b out, K4 next.
+//
+// Work item = (strip of TW output columns, segment of TH output rows, image); a persistent
+// grid of two CTAs per SM (<= 384 threads, <= 85 registers, ~80 KB of shared memory each)
+// walks the items, so one CTA's barrier / latency phases overlap the other's.  Per item the CTA streams down the rows in batches
+// of G rows; every step is an O(1)-per-pixel running or prefix sum ("independent of the
+// filter size"):
+//
+//   P0  column threads (one per statistics column, TW + 4r of them) keep fp64 running vertical
+//       window sums of I, I^2, p, I p (add row y + r, subtract row y - r - 1, R1 clipping by
+//       the row bounds) and snapshot them to shared memory;
+//   P1  every snapshotted row becomes its fp64 prefix sum (one warp per row: each lane holds a
+//       contiguous odd-length chunk in registers -- conflict-free fp64 banks -- and a warp
+//       shuffle scan of the chunk totals gives the offsets);
+//   P2  the horizontal window sum of a, b column j is P[j + 2r] - P[j - 1]; the coefficient
+//       epilogue (fp64 var / cov, R8 clamp, fp32 quotient) writes a, b for TW + 2r columns;
+//   P3  the a, b rows become fp64 prefix sums the same way;
+//   P4  per output column: hb = P[t + 2r] - P[t - 1] (horizontal box of a, b), and the vertical
+//       window of hb is a running fp64 sum whose subtracted rows come back from a per-CTA ring
+//       of the last 2r + 1 hb rows kept in global memory (L2-resident: 148 rings); then
+//       q = mean_a I + mean_b (s = 1) or the mean maps are stored (s > 1).
+//
+// Precision (R13, R17): products of two floats are exact in fp64; vertical sums and
+// prefixes in fp64 (prefixes over <= 672 columns of sums of <= 2r+1 rows: the difference of
+// two prefixes is exact to ~1e-15 relative); var / cov in fp64; quotient and b in fp32 (as the
+// other engines); a, b prefixes in fp64; hb rounded to fp32 once, and the ring returns that
+// same fp32 value, so the fp64 vertical sum of hb cancels exactly (no drift with the height).
+//
+// Nothing here is shared with oracle/ (the independent CPU reference).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fgf_kernels.cuh"
+
+namespace fgf {
+
+constexpr int kWideChMax = 13;          // prefix chunk per lane: rows of <= 32 * 13 = 416 columns
+constexpr int kWidePitch = 32 * kWideChMax;   // fp64 row pitch of the snapshot / a, b rows
+constexpr int kWideMaxCols = 384;       // threads per CTA = statistics columns TW + 4R (rounded)
+constexpr int kWideCtasPerSM = 2;
+
+struct WideLayout {
+    int NCS, NCA;          // statistics columns TW + 4R, a, b columns TW + 2R
+    size_t oVA, oAB, oInvA, oInvB, oStage, total;
+};
+
+struct WideParams {
+    // Sample (y, x) of image b: srcI[b*imgI + y*row + x*col]; p channel c at
+    // srcP[b*imgP + c*planeP + y*row + x*col] (element type E).  In-image offsets fit in 32 bits.
+    const void* srcI;
+    const void* srcP;
+    long long imgI, imgP;
+    int planeP;
+    int row, col;
+    int h, w, R;           // sample-grid dims and window radius (r at s = 1, r' otherwise)
+    int TW, TH;            // output columns per strip, output rows per segment
+    int strips, segs, items;
+    double eps;
+    float k1, k0;          // written value k1 mean_a + k0 (map 0) / k1 mean (others)
+    float* dst;            // maps mode: [img][2CP][h][w] fp32 (mean_a_c at 2c, mean_b_c at 2c+1)
+    void* q;               // OUTQ: [img][CP][h][w] of E (s = 1: the output image itself)
+    float* ring;           // [gridDim.x][2R+1][2CP][TW] fp32 ring of hb rows per CTA
+    WideLayout L;
+};
+
+template <int CP, int G, bool STAGE = true>
+struct WideCfg {
+    static constexpr int NMAP = 2 + 2 * CP;   // I, II, p_c, Ip_c
+    static constexpr int NAB = 2 * CP;        // a_c, b_c
+    static constexpr int NIN = 1 + CP;        // I, p_c
+    __host__ static WideLayout layout(int TW, int R) {
+        WideLayout L;
+        L.NCS = TW + 4 * R;
+        L.NCA = TW + 2 * R;
+        auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+        size_t o = 0;
+        L.oVA = o; o = al(o + (size_t)G * NMAP * kWidePitch * 8);
+        L.oAB = o; o = al(o + (size_t)G * NAB * kWidePitch * 8);
+        L.oInvA = o; o = al(o + (size_t)kWidePitch * 8);
+        L.oInvB = o; o = al(o + (size_t)kWidePitch * 4);
+        // cp.async staging of the next batch's add / subtract sample rows (fp32 samples)
+        L.oStage = o; o = al(o + (STAGE ? (size_t)G * 2 * NIN * kWideMaxCols * 4 : 0));
+        L.total = o;
+        return L;
+    }
+};
+
+// In-place inclusive fp64 prefix sum of row[0, n) (n <= kWidePitch) by one warp: lane l owns
+// the contiguous chunk [13 l, 13 l + 13) (odd length: the 16 lanes of a half-warp hit 16
+// distinct fp64 banks), loaded into registers at once; a warp shuffle scan of the chunk
+// totals gives the offsets.  Entries in [n, kWidePitch) are zeros that are read but never
+// written.
+__device__ __forceinline__ void warp_prefix_row(double* __restrict__ row, int n, int lane) {
+    double* r = row + lane * kWideChMax;
+    double v[kWideChMax];
+#pragma unroll
+    for (int i = 0; i < kWideChMax; ++i) v[i] = r[i];
+    double t0 = 0.0, t1 = 0.0;                 // two chains: half the dependent latency
+#pragma unroll
+    for (int i = 0; i < kWideChMax; i += 2) {
+        t0 += v[i];
+        if (i + 1 < kWideChMax) t1 += v[i + 1];
+    }
+    const double tot = t0 + t1;
+    double x = tot;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+    }
+    double run = x - tot;
+    const int e = n - lane * kWideChMax;       // valid entries of this chunk
+#pragma unroll
+    for (int i = 0; i < kWideChMax; ++i) {
+        run += v[i];
+        if (i < e) r[i] = run;
+    }
+}
+
+// Number of indices of [i - R, i + R] inside [0, n).
+__device__ __forceinline__ int wide_count(int i, int n, int R) {
+    return min(n - 1, i + R) - max(0, i - R) + 1;
+}
+
+// grid: persistent (<= items CTAs, two per SM), block NT = round32(TW + 4R) <= 384, dynamic
+// smem L.total.
+template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM>
+__global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParams P) {
+    // fp32 samples: the next batch's rows are prefetched by cp.async into shared memory (no
+    // registers held while in flight); 8/16-bit samples: into registers
+    constexpr bool STAGE = sizeof(E) == 4;
+    using C = WideCfg<CP, G, STAGE>;
+    constexpr int NMAP = C::NMAP, NAB = C::NAB, NIN = 1 + CP, PW = kWidePitch;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* __restrict__ VA = reinterpret_cast<double*>(smem + P.L.oVA);     // [G][NMAP][PW]
+    double* __restrict__ AB = reinterpret_cast<double*>(smem + P.L.oAB);     // [G][NAB][PW]
+    double* __restrict__ invA = reinterpret_cast<double*>(smem + P.L.oInvA); // [NCA], 0 outside
+    float* __restrict__ invB = reinterpret_cast<float*>(smem + P.L.oInvB);   // [TW]
+    float* __restrict__ stg = reinterpret_cast<float*>(smem + P.L.oStage);   // [G][2][NIN][384]
+    const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int NW = NT >> 5;
+    const int h = P.h, w = P.w, R = P.R, TW = P.TW;
+    const int NCS = P.L.NCS, NCA = P.L.NCA;
+    const int RS = 2 * R + 1;
+    const long long row = P.row;
+    const double invRow = 1.0 / (double)RS;                 // interior row count
+
+    // zero pads once: prefix rows read [n, PW) as zeros and never write them
+    for (int i = tid; i < G * NMAP * PW; i += NT) VA[i] = 0.0;
+    for (int i = tid; i < G * NAB * PW; i += NT) AB[i] = 0.0;
+
+    // hb ring of this CTA: slot k, map m, output column t at ring[(k NAB + m) TW + t]
+    float* const ring0 = P.ring + (size_t)blockIdx.x * RS * NAB * TW + tid;
+    const int slotStride = NAB * TW;
+    float* const ringEnd = ring0 + (size_t)RS * slotStride;
+    auto ldE = [](const E* p) { return ElemT<E>::load(p); };
+
+    for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
+        const int strip = item % P.strips;
+        const int rest = item / P.strips;
+        const int seg = rest % P.segs;
+        const int img = rest / P.segs;
+        const int x0 = strip * TW;
+        const int y0 = seg * P.TH;
+        const int y1 = min(h, y0 + P.TH);                 // output rows [y0, y1)
+        const int yA0 = max(0, y0 - R), yA1 = min(h, y1 + R);   // a, b rows [yA0, yA1)
+        const int yEnd = y1 + R;                          // steps ya in [yA0, yEnd)
+
+        __syncthreads();   // the previous item's P2 / P4 have read invA / invB
+        for (int j = tid; j < NCA; j += NT) {
+            const int ca = x0 - R + j;
+            invA[j] = (ca >= 0 && ca < w) ? 1.0 / (double)wide_count(ca, w, R) : 0.0;
+        }
+        for (int t = tid; t < TW; t += NT)
+            invB[t] = (float)(1.0 / (double)wide_count(min(x0 + t, w - 1), w, R));
+
+        // ---- this thread's statistics column (P0)
+        const int cs = x0 - 2 * R + tid;
+        const bool colS = tid < NCS;
+        const bool colIn = colS && cs >= 0 && cs < w;
+        const E* const colI = static_cast<const E*>(P.srcI) + img * P.imgI + (long long)(colIn ? cs : 0) * P.col;
+        const E* const colP = static_cast<const E*>(P.srcP) + img * P.imgP + (long long)(colIn ? cs : 0) * P.col;
+        const long long cstr = P.planeP;
+        double acc[NMAP];
+#pragma unroll
+        for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
+        if (colIn) {
+            // warm-up: the window of a, b row yA0 - 1: sample rows [yA0 - 1 - R, yA0 - 1 + R]
+            const int wa = max(0, yA0 - 1 - R), wb = min(h, yA0 + R);
+            const E* pi = colI + wa * row;
+            const E* pp = colP + wa * row;
+            constexpr int WB = 8;
+            for (int yy = wa; yy < wb; yy += WB) {
+                float v[WB][NIN];
+#pragma unroll
+                for (int k = 0; k < WB; ++k) {
+                    if (yy + k < wb) {
+                        v[k][0] = ldE(pi + k * row);
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) v[k][1 + c] = ldE(pp + c * cstr + k * row);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < WB; ++k) {
+                    if (yy + k < wb) {
+                        const double I = (double)v[k][0];
+                        acc[0] += I;
+                        acc[1] = fma(I, I, acc[1]);
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            const double pv = (double)v[k][1 + c];
+                            acc[2 + c] += pv;
+                            acc[2 + CP + c] = fma(I, pv, acc[2 + CP + c]);
+                        }
+                    }
+                }
+                pi += WB * row;
+                pp += WB * row;
+            }
+        }
+        // add / subtract sample rows of a batch, prefetched one batch ahead; rows that must
+        // not contribute are zeros (which add exactly nothing)
+        float va[STAGE ? 1 : G][NIN], vs[STAGE ? 1 : G][NIN];
+        float* const stg_t = stg + tid;                   // [(g 2 + a) NIN + k] * 384
+        auto stage4 = [&](int slot, const E* src, bool ok) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(stg_t + slot * kWideMaxCols);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                         ::"r"(d), "l"(ok ? src : colI), "r"(ok ? 4 : 0) : "memory");
+        };
+        auto load_batch = [&](int ya) {
+            const E* ai = colI + (ya + R) * row;
+            const E* ap = colP + (ya + R) * row;
+            const E* si = colI + (ya - R - 1) * row;
+            const E* sp = colP + (ya - R - 1) * row;
+            const bool full = colIn && ya + G <= yA1 && ya - R - 1 >= 0 && ya + G - 1 + R < h;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int y = ya + g;
+                const bool oka = full || (colIn && y < yA1 && y + R < h);
+                const bool oks = full || (colIn && y < yA1 && y - R - 1 >= 0);
+                if constexpr (STAGE) {
+                    stage4((g * 2 + 0) * NIN, ai + g * row, oka);
+                    stage4((g * 2 + 1) * NIN, si + g * row, oks);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) {
+                        stage4((g * 2 + 0) * NIN + 1 + c, ap + c * cstr + g * row, oka);
+                        stage4((g * 2 + 1) * NIN + 1 + c, sp + c * cstr + g * row, oks);
+                    }
+                } else {
+                    va[STAGE ? 0 : g][0] = oka ? ldE(ai + g * row) : 0.0f;
+                    vs[STAGE ? 0 : g][0] = oks ? ldE(si + g * row) : 0.0f;
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) {
+                        va[STAGE ? 0 : g][1 + c] = oka ? ldE(ap + c * cstr + g * row) : 0.0f;
+                        vs[STAGE ? 0 : g][1 + c] = oks ? ldE(sp + c * cstr + g * row) : 0.0f;
+                    }
+                }
+            }
+            if constexpr (STAGE) asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+
+        // ---- this thread's output column (P4)
+        const int xo = x0 + tid;
+        const bool colO = tid < TW && xo < w;
+        const E* const Iq = static_cast<const E*>(P.srcI) + img * P.imgI + xo;   // OUTQ: s = 1
+        double accB[NAB];
+#pragma unroll
+        for (int m = 0; m < NAB; ++m) accB[m] = 0.0;
+        float* rslot = ring0;                              // ring slot of step ya
+        double* const va_t = VA + tid;                     // P0 snapshots of this column
+        const double* const pa_t = VA + tid;               // P2: window ends tid - 1, tid + 2R
+        double* const ab_t = AB + tid;                     // P2: a, b of column tid
+        const double* const pb_t = AB + tid;               // P4: window ends tid - 1, tid + 2R
+        const int R2 = 2 * R;
+
+        load_batch(yA0);
+        for (int ya = yA0; ya < yEnd; ya += G) {
+            const int nA = max(0, min(G, yA1 - ya));       // a, b rows of this batch
+            const int nS = min(G, yEnd - ya);              // steps of this batch
+            // ---- P0: vertical windows of a, b rows [ya, ya + nA), snapshots
+            if constexpr (STAGE) asm volatile("cp.async.wait_group 0;" ::: "memory");
+            if (colS) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (g < nA) {
+                        float xa[NIN], xs[NIN];
+#pragma unroll
+                        for (int k = 0; k < NIN; ++k) {
+                            xa[k] = STAGE ? stg_t[((g * 2 + 0) * NIN + k) * kWideMaxCols] : va[STAGE ? 0 : g][k];
+                            xs[k] = STAGE ? stg_t[((g * 2 + 1) * NIN + k) * kWideMaxCols] : vs[STAGE ? 0 : g][k];
+                        }
+                        const double Ia = (double)xa[0], Is = (double)xs[0];
+                        acc[0] += Ia - Is;
+                        acc[1] += fma(Ia, Ia, -(Is * Is));
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            const double pa = (double)xa[1 + c], ps = (double)xs[1 + c];
+                            acc[2 + c] += pa - ps;
+                            acc[2 + CP + c] += fma(Ia, pa, -(Is * ps));
+                        }
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) va_t[(g * NMAP + m) * PW] = acc[m];
+                    }
+                }
+            }
+            if (ya + G < yA1) load_batch(ya + G);
+            // ring rows leaving the vertical windows of this batch's steps, and (s = 1) the
+            // guidance row of each output: issued now, used in P4
+            float old[G][NAB];
+            float Io[OUTQ ? G : 1];
+            if (colO) {
+                float* rp = rslot;
+                const E* ip = Iq + (ya - R) * row;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int yy = ya + g;
+                    const bool sub = g < nS && yy - RS >= yA0;   // row yy - 2R - 1 was added
+#pragma unroll
+                    for (int m = 0; m < NAB; ++m) old[g][m] = sub ? rp[m * TW] : 0.0f;
+                    if (OUTQ) {
+                        const int yb = yy - R;
+                        Io[OUTQ ? g : 0] = (g < nS && yb >= y0 && yb < y1) ? ldE(ip + g * row) : 0.0f;
+                    }
+                    rp += slotStride;
+                    rp = rp == ringEnd ? ring0 : rp;
+                }
+            }
+            __syncthreads();
+            // ---- P1: prefix sums of the snapshotted rows
+            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row(VA + rs * PW, NCS, lane);
+            __syncthreads();
+            // ---- P2: window sums, coefficient epilogue -> a, b (fp64 rows for P3)
+            if (tid < NCA) {
+                const double ix = invA[tid];
+                const bool first = tid == 0;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (g < nA) {
+                        const int yy = ya + g;
+                        const double iy = (yy - R >= 0 && yy + R < h)
+                                              ? invRow : 1.0 / (double)wide_count(yy, h, R);
+                        const double inv = ix * iy;           // 0 outside the image -> a = b = 0
+                        double S[NMAP];
+#pragma unroll
+                        for (int m = 0; m < NMAP; ++m) {
+                            const double* q = pa_t + (g * NMAP + m) * PW;
+                            S[m] = q[R2] - (first ? 0.0 : q[-1]);
+                        }
+                        const double mI = S[0] * inv;
+                        double var = fma(-mI, mI, S[1] * inv);     // var_I (P:58 / P:78)
+                        var = var < 0.0 ? 0.0 : var;               // R8
+                        float rden;                                // 1 / (var + eps), ~1 ulp
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rden) : "f"((float)(var + P.eps)));
+                        const float mIf = (float)mI;
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            const double mp = S[2 + c] * inv;
+                            const double cov = fma(-mI, mp, S[2 + CP + c] * inv);   // cov_Ip
+                            const float a = (float)cov * rden;                    // Eq.2
+                            ab_t[(g * NAB + 2 * c) * PW] = (double)a;
+                            ab_t[(g * NAB + 2 * c + 1) * PW] = (double)fmaf(-a, mIf, (float)mp);   // Eq.3
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- P3: prefix sums of the a, b rows
+            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row(AB + rs * PW, NCA, lane);
+            __syncthreads();
+            // ---- P4: horizontal box of a, b, vertical running window through the ring, output
+            if (colO) {
+                const float ixB = invB[tid];
+                const bool first = tid == 0;
+                float* rp = rslot;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    if (g < nS) {
+                        if (g < nA) {
+#pragma unroll
+                            for (int m = 0; m < NAB; ++m) {
+                                const double* q = pb_t + (g * NAB + m) * PW;
+                                const float hb = (float)(q[R2] - (first ? 0.0 : q[-1]));
+                                rp[m * TW] = hb;
+                                accB[m] += (double)hb;
+                            }
+                        }
+#pragma unroll
+                        for (int m = 0; m < NAB; ++m) accB[m] -= (double)old[g][m];
+                        const int yb = ya + g - R;
+                        if (yb >= y0 && yb < y1) {
+                            const float iy = (yb - R >= 0 && yb + R < h)
+                                                 ? (float)invRow
+                                                 : 1.0f / (float)wide_count(yb, h, R);
+                            const float inv = ixB * iy;
+                            if (OUTQ) {
+                                const float I = Io[OUTQ ? g : 0];
+                                E* qo = static_cast<E*>(P.q) + (long long)img * CP * h * w +
+                                        (long long)yb * w + xo;
+#pragma unroll
+                                for (int c = 0; c < CP; ++c) {
+                                    const float ma = fmaf(P.k1, (float)accB[2 * c] * inv,
+                                                          c == 0 ? P.k0 : 0.0f);
+                                    const float mb = P.k1 * ((float)accB[2 * c + 1] * inv);
+                                    const float qv = fmaf(ma, I, mb);           // Eq.4
+                                    const unsigned bits = ElemT<E>::bits(qv);
+                                    E* qc = qo + (long long)c * h * w;
+                                    if (sizeof(E) == 4) __stcs(reinterpret_cast<float*>(qc), __uint_as_float(bits));
+                                    else if (sizeof(E) == 2) __stcs(reinterpret_cast<unsigned short*>(qc), (unsigned short)bits);
+                                    else *reinterpret_cast<unsigned char*>(qc) = (unsigned char)bits;
+                                }
+                            } else {
+                                float* d = P.dst + ((size_t)img * NAB * h + yb) * w + xo;
+#pragma unroll
+                                for (int m = 0; m < NAB; ++m)
+                                    d[(size_t)m * h * w] = fmaf(P.k1, (float)accB[m] * inv, m == 0 ? P.k0 : 0.0f);
+                            }
+                        }
+                    }
+                    rp += slotStride;
+                    rp = rp == ringEnd ? ring0 : rp;
+                }
+            }
+            // ring slot of the next batch's first step
+            for (int g = 0; g < G; ++g) {
+                rslot += slotStride;
+                rslot = rslot == ringEnd ? ring0 : rslot;
+            }
+        }
+    }
+}
+
+}  // namespace fgf

@@ -157,3 +157,24 @@ def test_c_band_uneven_splits(H, W, s, r, nranks, mode):
     q_whole = fgf.filter(I, p, r, 0.01, s, 0)
     torch.cuda.synchronize()
     assert float((q - q_whole).abs().max()) < 1e-5
+
+
+def test_c_band_loopback_two_step_narrow_bands():
+    """Bands of r'+1 <= rows < 2r'+1 low-res rows (here 12-13 rows at r' = 8): only the
+    two-step exchange admits them.  The workspace query must still size them."""
+    g = torch.Generator(device="cuda").manual_seed(41)
+    H, W, r, s, eps, nranks = 2048, 256, 32, 4, 0.01, 40
+    I = torch.rand((1, 1, H, W), device="cuda", generator=g)
+    p = torch.rand((1, 1, H, W), device="cuda", generator=g)
+    assert fgf.fgf_band_workspace_bytes(H, W, 0, 48, 1, 1, r, s, nranks) > 0
+    q = _loopback(I, p, r, eps, s, 0, nranks, fgf.FGF_BAND_TWO_STEP)
+    ref = oracle.fast_guided_filter(I.cpu().numpy(), p.cpu().numpy(), r, eps, s, 0)
+    assert float(np.abs(q.double().cpu().numpy() - ref).max()) < 1e-4
+    # the single exchange rejects such bands before any launch
+    q2 = torch.empty_like(q)
+    nb = fgf.fgf_bands_loopback_workspace_bytes(H, W, 1, 1, r, s, nranks)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    rc = fgf.fgf_filter_bands_loopback(I, p, q2, H, W, 1, 1, r, eps, s, 0, nranks, ws, nb,
+                                       torch.cuda.current_stream(), mode=fgf.FGF_BAND_SINGLE,
+                                       check=False)
+    assert rc == fgf.FGF_ERR_PARAM

@@ -88,6 +88,7 @@ def test_half_io_unsupported_and_errors():
 
 def test_half_io_multi_chunk_equals_single_chunk(monkeypatch):
     """16-bit buffers through the chunked pipeline (element offsets of 2 bytes)."""
+    monkeypatch.setenv("FGF_DEV", "1")   # honour the development knobs
     I, p = _inputs("gray", 6, 1, 1, 1080, 1920, torch.float16, 3)
     monkeypatch.delenv("FGF_CHUNK_MB", raising=False)
     q1 = fgf.filter(I, p, 16, 0.01, 4, 0)

@@ -24,7 +24,7 @@ def tol(eps):
 
 class env:
     def __init__(self, **kv):
-        self.kv = kv
+        self.kv = dict(kv, FGF_DEV="1")   # the library honours its development knobs only then
 
     def __enter__(self):
         self.old = {k: os.environ.get(k) for k in self.kv}
@@ -83,7 +83,8 @@ def test_fused_lowres_vs_oracle(case, variant):
     g = torch.Generator(device="cuda").manual_seed(abs(hash(case)) % (2 ** 31))
     I = torch.rand((B, 1, H, W), device="cuda", generator=g)
     p = torch.rand((B, CP, H, W), device="cuda", generator=g)
-    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None, FGF_LR_V=variant, FGF_LR_RMAX=64):
+    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None, FGF_LR_V=variant, FGF_LR_RMAX=64,
+             FGF_ENGINE="k13"):
         fgf.fgf_profile_enable(True)
         q = fgf.filter(I, p, r, eps, s, sub)
         torch.cuda.synchronize()
@@ -105,7 +106,7 @@ def test_fused_matches_strip_engine(case):
     g = torch.Generator(device="cuda").manual_seed(7 + abs(hash(case)) % 1000)
     I = torch.rand((B, 1, H, W), device="cuda", generator=g)
     p = torch.rand((B, CP, H, W), device="cuda", generator=g)
-    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None, FGF_LR_RMAX=64):
+    with env(FGF_LR_TH=TH, FGF_LR_NT=NT, FGF_LOWRES=None, FGF_LR_RMAX=64, FGF_ENGINE="k13"):
         m1 = fgf.coefficients(I, p, r, eps, s, sub)
     with env(FGF_LOWRES="strip"):
         m2 = fgf.coefficients(I, p, r, eps, s, sub)

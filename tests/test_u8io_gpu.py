@@ -104,6 +104,7 @@ def test_u8_io_saturates_and_round_trips_constants():
 
 def test_u8_io_multi_chunk_equals_single_chunk(monkeypatch):
     """8-bit buffers through the chunked pipeline (element offsets of 1 byte)."""
+    monkeypatch.setenv("FGF_DEV", "1")   # honour the development knobs
     I8, p8 = _inputs("gray", 6, 1, 1, 1080, 1920, 3)
     monkeypatch.delenv("FGF_CHUNK_MB", raising=False)
     q1 = fgf.filter(I8, p8, 16, 0.01, 4, 0)
