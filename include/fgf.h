@@ -152,6 +152,14 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
                              int W, int C_I, int C_p, int H_total, int h_total, int w, int Y0,
                              int y0_maps, int h_maps, void* cuda_stream);
 
+/* Row-band geometry of rank `rank` of `nranks` for one H x W image (the same
+ * rule fgf_filter_band and fgf_filter_bands_loopback use): rank k owns low-res rows
+ * [k h / n, (k + 1) h / n) of h = ceil(H/s) (R6) and so full-resolution rows on multiples of s.
+ * Host only (no GPU, no launch).  out[10] = {h, w, r', halo = 2r' + 1, own low-res rows y0, y1,
+ * own full-res rows Y0, Y1, extended low-res rows e0, e1 of the single exchange}.
+ * FGF_ERR_PARAM when a band of several holds fewer than 2r' + 1 low-res rows. */
+int fgf_band_geometry(int H, int W, int r, int s, int nranks, int rank, int* out);
+
 /* ---------------------------------------------------------------------------------------
  * One image split into row bands across ranks (BASELINE.json config 4b).
  * Rank `rank` of `nranks` owns full-resolution rows [row0, row0 + rows) of an image of

@@ -50,7 +50,7 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
            "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
-           "fgf_nccl_check")
+           "fgf_nccl_check", "fgf_band_geometry")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused",
                 "wide_fused")
 
@@ -113,6 +113,8 @@ _lib.fgf_joint_workspace_bytes.argtypes = [_i] * 7
 _lib.fgf_joint_workspace_bytes.restype = _sz
 _lib.fgf_filter_joint_ws.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
 _lib.fgf_filter_joint_ws.restype = _i
+_lib.fgf_band_geometry.argtypes = [_i, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int)]
+_lib.fgf_band_geometry.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -334,6 +336,13 @@ def fgf_nccl_check(comm) -> int:
 
 def fgf_nccl_comm_destroy(comm) -> None:
     _check(_lib.fgf_nccl_comm_destroy(comm), "fgf_nccl_comm_destroy")
+
+
+def fgf_band_geometry(H, W, r, s, nranks, rank):
+    """(h, w, r', halo, y0, y1, Y0, Y1, e0, e1) of the C band planner (host only)."""
+    out = (ctypes.c_int * 10)()
+    _check(_lib.fgf_band_geometry(H, W, r, s, nranks, rank, out), "fgf_band_geometry")
+    return tuple(out)
 
 
 def fgf_bands_loopback_workspace_bytes(H, W, C_I, C_p, r, s, nranks) -> int:

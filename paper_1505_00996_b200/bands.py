@@ -24,8 +24,9 @@ from dataclasses import dataclass
 
 
 def lowres_radius(r: int, s: int) -> int:
-    """R2: r' = max(1, floor(r/s + 1/2))."""
-    return max(1, (2 * r + s) // (2 * s))
+    """R2: r' = max(1, floor(r/s + 1/2)) -- from the C planner (fgf_band_geometry)."""
+    from paper_1505_00996_b200 import fgf_band_geometry
+    return fgf_band_geometry(max(1, s), 1, r, s, 1, 0)[2]
 
 
 @dataclass(frozen=True)
@@ -49,15 +50,16 @@ class BandPlan:
 
 
 def plan_band(H: int, W: int, r: int, s: int, world: int, rank: int) -> BandPlan:
-    h, w = -(-H // s), -(-W // s)
-    R = lowres_radius(r, s)
-    halo = 2 * R + 1
-    y0, y1 = rank * h // world, (rank + 1) * h // world
-    if world > 1 and min((k + 1) * h // world - k * h // world for k in range(world)) < halo:
-        raise ValueError(f"bands of {h // world} low-res rows are thinner than the halo "
-                         f"({halo} rows): use fewer ranks")
-    Y0, Y1 = y0 * s, min(H, y1 * s)
-    e0, e1 = max(0, y0 - halo), min(h, y1 + halo)
+    """The band of `rank`, from the C planner of libfgf.so (fgf_band_geometry: one rule for the
+    C band path and this one; host logic only, no GPU needed)."""
+    from paper_1505_00996_b200 import FGF_ERR_PARAM, FGFError, fgf_band_geometry
+    try:
+        h, w, R, halo, y0, y1, Y0, Y1, e0, e1 = fgf_band_geometry(H, W, r, s, world, rank)
+    except FGFError as e:
+        if e.status == FGF_ERR_PARAM:
+            raise ValueError(f"bands of {-(-H // s) // world} low-res rows are thinner than the "
+                             "halo (2r'+1 rows): use fewer ranks") from e
+        raise
     return BandPlan(H, W, s, r, world, rank, h, w, R, halo, y0, y1, Y0, Y1, e0, e1)
 
 

@@ -403,6 +403,34 @@ struct HostPipe {
 std::mutex g_host_mu;
 std::vector<HostPipe> g_host;
 
+// Band path: the library's comm stream (edge strips, NCCL halo, edge chains) and its events.
+struct BandStreams {
+    bool init = false;
+    cudaStream_t comm = nullptr;
+    cudaEvent_t fork = nullptr, interior = nullptr, edges = nullptr;
+};
+std::mutex g_band_mu;
+std::vector<BandStreams> g_band;
+
+int get_band_streams(BandStreams*& out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return FGF_ERR_CUDA;
+    if ((int)g_band.size() <= dev) g_band.resize(dev + 1);
+    BandStreams& b = g_band[dev];
+    if (!b.init) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        if (cudaStreamCreateWithPriority(&b.comm, cudaStreamNonBlocking, hi) ||
+            cudaEventCreateWithFlags(&b.fork, cudaEventDisableTiming) ||
+            cudaEventCreateWithFlags(&b.interior, cudaEventDisableTiming) ||
+            cudaEventCreateWithFlags(&b.edges, cudaEventDisableTiming))
+            return FGF_ERR_CUDA;
+        b.init = true;
+    }
+    out = &b;
+    return FGF_OK;
+}
+
 // ---- CUDA-graph cache for small calls (verdict r1: single-image latency).  A call of at most
 // kGraphMaxPixels output pixels whose arguments (pointers, sizes, parameters, stream,
 // workspace) repeat an earlier call is replayed from a graph captured on its second occurrence:
@@ -652,6 +680,23 @@ int fgf_nccl_comm_destroy(void* comm) {
     return n->commDestroy(static_cast<ncclComm_t>(comm)) == ncclSuccess ? FGF_OK : FGF_ERR_NCCL;
 }
 
+int fgf_band_geometry(int H, int W, int r, int s, int nranks, int rank, int* out) {
+    if (!out) return FGF_ERR_NULL;
+    if (H < 1 || W < 1) return FGF_ERR_SHAPE;
+    if (r < 1 || s < 1 || nranks < 1 || rank < 0 || rank >= nranks) return FGF_ERR_PARAM;
+    const int h = lowres_dim(H, s), w = lowres_dim(W, s), R = radius_lowres(r, s);
+    const int halo = 2 * R + 1;
+    // every band must hold a whole single-exchange halo, unless it is alone
+    for (int k = 0; k < nranks && nranks > 1; ++k)
+        if ((int)((long long)(k + 1) * h / nranks) - (int)((long long)k * h / nranks) < halo)
+            return FGF_ERR_PARAM;
+    const int y0 = (int)((long long)rank * h / nranks), y1 = (int)((long long)(rank + 1) * h / nranks);
+    const int g[10] = {h, w, R, halo, y0, y1, y0 * s, std::min(H, y1 * s), std::max(0, y0 - halo),
+                       std::min(h, y1 + halo)};
+    memcpy(out, g, sizeof(g));
+    return FGF_OK;
+}
+
 size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
                                 int s, int nranks) {
     // The larger of the exchange modes this band admits (two-step accepts narrower bands:
@@ -700,33 +745,59 @@ int fgf_filter_band_ex(const float* I_band, const float* p_band, float* q_band, 
     if (ws_bytes < B.ws_total) return FGF_ERR_NOMEM;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     char* ws = static_cast<char*>(workspace);
-    if ((rc = band_prepare(B, I_band, p_band, ws, st))) return rc;
     // one NCCL group: every plane's halo rows to / from rank-1 and rank+1
-    auto exchange = [&](int planes, bool ab) -> int {
-        if (nranks == 1) return FGF_OK;
+    auto nccl_exchange = [&](int planes, auto&& halo_of, cudaStream_t cs) -> int {
         const Nccl* n = nccl();
         if (!n) return FGF_ERR_NCCL;
         ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
         if (n->groupStart() != ncclSuccess) return FGF_ERR_NCCL;
         ncclResult_t e = ncclSuccess;
         for (int j = 0; j < planes && e == ncclSuccess; ++j) {
-            const Halo hl = ab ? band_halo_ab(B, ws, j, rank, nranks) : band_halo(B, ws, j, rank, nranks);
+            const Halo hl = halo_of(j);
             if (hl.n_up) {
-                e = n->send(hl.send_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
-                if (e == ncclSuccess) e = n->recv(hl.recv_up, hl.n_up, ncclFloat32, rank - 1, comm, st);
+                e = n->send(hl.send_up, hl.n_up, ncclFloat32, rank - 1, comm, cs);
+                if (e == ncclSuccess) e = n->recv(hl.recv_up, hl.n_up, ncclFloat32, rank - 1, comm, cs);
             }
             if (hl.n_down && e == ncclSuccess) {
-                e = n->send(hl.send_down, hl.n_down, ncclFloat32, rank + 1, comm, st);
-                if (e == ncclSuccess) e = n->recv(hl.recv_down, hl.n_down, ncclFloat32, rank + 1, comm, st);
+                e = n->send(hl.send_down, hl.n_down, ncclFloat32, rank + 1, comm, cs);
+                if (e == ncclSuccess) e = n->recv(hl.recv_down, hl.n_down, ncclFloat32, rank + 1, comm, cs);
             }
         }
         if (n->groupEnd() != ncclSuccess || e != ncclSuccess) return FGF_ERR_NCCL;
         return FGF_OK;
     };
-    if ((rc = exchange(B.NPL, false))) return rc;                      // I', p' (exchange A)
+    if (nranks == 1)   // one band = the whole image: the whole-image filter itself
+        return run_all(I_band, p_band, q_band, B.pb, ws, ws_bytes, st);
+    if (B.ovl) {
+        // overlapped single exchange (fgf_band.cuh): interior chain on the caller's stream,
+        // edge strips + NCCL halo + edge chains on the library's comm stream
+        std::lock_guard<std::mutex> lk(g_band_mu);
+        BandStreams* bs = nullptr;
+        if ((rc = get_band_streams(bs))) return rc;
+        const int launches0 = g_last_launches;
+        if (cudaEventRecord(bs->fork, st) || cudaStreamWaitEvent(bs->comm, bs->fork, 0)) return FGF_ERR_CUDA;
+        if ((rc = band_ovl_prepare(B, I_band, p_band, ws, bs->comm))) return rc;
+        if ((rc = nccl_exchange(B.NPL, [&](int j) { return band_ovl_halo(B, ws, j); }, bs->comm)))
+            return rc;
+        if ((rc = band_ovl_interior(B, I_band, p_band, ws, st))) return rc;
+        if ((rc = band_ovl_assemble(B, ws, false, st))) return rc;
+        if (cudaEventRecord(bs->interior, st)) return FGF_ERR_CUDA;
+        if ((rc = band_ovl_edges(B, ws, self, bs->comm))) return rc;
+        if (cudaStreamWaitEvent(bs->comm, bs->interior, 0)) return FGF_ERR_CUDA;
+        if ((rc = band_ovl_assemble(B, ws, true, bs->comm))) return rc;
+        if (cudaEventRecord(bs->edges, bs->comm) || cudaStreamWaitEvent(st, bs->edges, 0))
+            return FGF_ERR_CUDA;
+        rc = band_ovl_output(B, I_band, q_band, ws, st);
+        (void)launches0;
+        return rc;
+    }
+    if ((rc = band_prepare(B, I_band, p_band, ws, st))) return rc;
+    if ((rc = nccl_exchange(B.NPL, [&](int j) { return band_halo(B, ws, j, rank, nranks); }, st)))
+        return rc;                                                      // I', p' (exchange A)
     if (B.mode == FGF_BAND_TWO_STEP) {
         if ((rc = band_stats_ab(B, ws, st, self))) return rc;
-        if ((rc = exchange(B.lp.NC, true))) return rc;                 // a, b (exchange B)
+        if ((rc = nccl_exchange(B.lp.NC, [&](int j) { return band_halo_ab(B, ws, j, rank, nranks); }, st)))
+            return rc;                                                  // a, b (exchange B)
     }
     return band_finish(B, I_band, q_band, ws, st, self);
 }
@@ -793,19 +864,29 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
                 if (cudaMemcpyAsync(pb[k] + (size_t)j * rows * W, p + ((size_t)j * H + row0) * W,
                                     (size_t)rows * W * 4, cudaMemcpyDeviceToDevice, st))
                     return FGF_ERR_CUDA;
-        if ((rc = band_prepare(Bs[k], Ib[k], pb[k], wss[k], st))) return rc;
+    }
+    // the overlapped single exchange when every band takes it (as fgf_filter_band_ex)
+    bool use_ovl = mode == FGF_BAND_SINGLE && nranks > 1;
+    for (int k = 0; k < nranks; ++k) use_ovl = use_ovl && Bs[k].ovl;
+    for (int k = 0; k < nranks; ++k) {
+        if ((rc = use_ovl ? band_ovl_prepare(Bs[k], Ib[k], pb[k], wss[k], st)
+                          : band_prepare(Bs[k], Ib[k], pb[k], wss[k], st)))
+            return rc;
         launches += g_last_launches;
         g_last_launches = 0;
     }
     // the exchanges, rank k <-> k+1, with the same halo geometry the NCCL path sends
-    auto exchange = [&](bool ab) -> int {
+    // (0: I', p' of the compacting single / two-step forms, 1: a, b, 2: overlapped form)
+    auto exchange = [&](int kind) -> int {
         for (int k = 0; k + 1 < nranks; ++k) {
-            const int planes = ab ? Bs[k].lp.NC : Bs[k].NPL;
+            const int planes = kind == 1 ? Bs[k].lp.NC : Bs[k].NPL;
             for (int j = 0; j < planes; ++j) {
-                const Halo a = ab ? band_halo_ab(Bs[k], wss[k], j, k, nranks)
-                                  : band_halo(Bs[k], wss[k], j, k, nranks);
-                const Halo b = ab ? band_halo_ab(Bs[k + 1], wss[k + 1], j, k + 1, nranks)
-                                  : band_halo(Bs[k + 1], wss[k + 1], j, k + 1, nranks);
+                auto halo = [&](int kk) {
+                    return kind == 2 ? band_ovl_halo(Bs[kk], wss[kk], j)
+                         : kind == 1 ? band_halo_ab(Bs[kk], wss[kk], j, kk, nranks)
+                                     : band_halo(Bs[kk], wss[kk], j, kk, nranks);
+                };
+                const Halo a = halo(k), b = halo(k + 1);
                 if (a.n_down != b.n_up) return FGF_ERR_PARAM;   // both sides agree on the depth
                 if (cudaMemcpyAsync(a.recv_down, b.send_up, b.n_up * 4, cudaMemcpyDeviceToDevice, st) ||
                     cudaMemcpyAsync(b.recv_up, a.send_down, a.n_down * 4, cudaMemcpyDeviceToDevice, st))
@@ -814,14 +895,33 @@ int fgf_filter_bands_loopback(const float* I, const float* p, float* q, int H, i
         }
         return FGF_OK;
     };
-    if ((rc = exchange(false))) return rc;
+    if (use_ovl) {
+        if ((rc = exchange(2))) return rc;
+        for (int k = 0; k < nranks; ++k) {
+            if ((rc = band_ovl_interior(Bs[k], Ib[k], pb[k], wss[k], st)) ||
+                (rc = band_ovl_assemble(Bs[k], wss[k], false, st)) ||
+                (rc = band_ovl_edges(Bs[k], wss[k], self, st)) ||
+                (rc = band_ovl_assemble(Bs[k], wss[k], true, st)) ||
+                (rc = band_ovl_output(Bs[k], Ib[k], qb[k], wss[k], st)))
+                return rc;
+            launches += g_last_launches;
+            g_last_launches = 0;
+            for (int j = 0; j < C_p; ++j)
+                if (cudaMemcpyAsync(q + ((size_t)j * H + Bs[k].row0) * W, qb[k] + (size_t)j * Bs[k].rows * W,
+                                    (size_t)Bs[k].rows * W * 4, cudaMemcpyDeviceToDevice, st))
+                    return FGF_ERR_CUDA;
+        }
+        g_last_launches = launches;
+        return FGF_OK;
+    }
+    if ((rc = exchange(0))) return rc;
     if (mode == FGF_BAND_TWO_STEP) {
         for (int k = 0; k < nranks; ++k) {
             if ((rc = band_stats_ab(Bs[k], wss[k], st, self))) return rc;
             launches += g_last_launches;
             g_last_launches = 0;
         }
-        if ((rc = exchange(true))) return rc;
+        if ((rc = exchange(1))) return rc;
     }
     for (int k = 0; k < nranks; ++k) {
         if ((rc = band_finish(Bs[k], Ib[k], qb[k], wss[k], st, self))) return rc;

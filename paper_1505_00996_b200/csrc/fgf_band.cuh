@@ -76,13 +76,29 @@ struct BandPlan {
     int e0, e1;              // extended low-res rows of I', p' after (the first) exchange
     int f0, f1;              // two-step: rows of a, b after exchange B ([y0-r'-1, y1+r'+1))
     int CI, CP, NPL;         // planes exchanged: C_I (+ C_p unless self-guided)
+    int r_full;              // r (full resolution)
     size_t ext_plane;        // floats per extended plane: (e1 - e0) * w
     size_t ab_plane;         // two-step: floats per a, b / mean plane: (f1 - f0) * w
     // workspace carve-up (bytes)
     size_t o_ext, o_lowres, o_mean, o_ab, o_abx, ws_total;
     Plan lp;                 // the low-res plan on the extended band (s = 1, radius r')
     Plan lpB;                // two-step: the plan of the box of a, b on rows [f0, f1)
+    // overlapped single exchange (band_plan_overlap): the interior is the band's own image
+    bool ovl = false;
+    Plan pb;                 // the band's rows as an image (full resolution, s, r)
+    int m0, m1;              // rows of the assembled mean maps: [y0 - 1, y1 + 1) clipped
+    int t0, t1, b0, b1;      // top / bottom edge strips of low-res rows (halo + 4r' own rows)
+    Plan pe_t, pe_b;         // s = 1 plans of the edge strips (radius r')
+    size_t o_slot, o_int, o_et, o_etw, o_etm, o_eb, o_ebw, o_ebm, o_fin;
 };
+
+// Halo geometry of plane j: the rows this rank sends up / down and receives from up / down.
+struct Halo {
+    float *send_up, *send_down, *recv_up, *recv_down;
+    size_t n_up, n_down;     // floats (0 when there is no neighbour on that side)
+};
+
+int band_plan_overlap(BandPlan& B, bool self_guided, double eps);
 
 int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int r, double eps,
               int s, int sub, int nranks, bool self_guided, int mode = FGF_BAND_SINGLE) {
@@ -92,7 +108,7 @@ int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int
     if (rc) return rc;
     if (rows < 1 || row0 < 0 || row0 + rows > H) return FGF_ERR_SHAPE;
     if (row0 % s != 0 || ((row0 + rows) % s != 0 && row0 + rows != H)) return FGF_ERR_PARAM;
-    B.H = H; B.W = W; B.s = s; B.sub = sub; B.CI = CI; B.CP = CP;
+    B.H = H; B.W = W; B.s = s; B.sub = sub; B.CI = CI; B.CP = CP; B.r_full = r;
     B.h = lowres_dim(H, s);
     B.w = lowres_dim(W, s);
     B.R = radius_lowres(r, s);
@@ -119,6 +135,14 @@ int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int
     if (mode == FGF_BAND_SINGLE) {
         B.o_mean = B.o_lowres + align_up(plan_ws(B.lp, false));
         B.ws_total = B.o_mean + align_up((size_t)B.lp.NC * B.ext_plane * sizeof(float));
+        // the overlapped form when the band is tall enough (its workspace is reserved too);
+        // one rank: the band is the whole image and runs as such (fgf_filter_band_ex)
+        if (nranks > 1) {
+            band_plan_overlap(B, self_guided, eps);
+        } else {
+            if ((rc = make_plan(B.pb, 1, rows, W, CI, CP, r, eps, s, sub))) return rc;
+            B.ws_total = std::max(B.ws_total, plan_ws(B.pb, true));
+        }
         return FGF_OK;
     }
     if ((rc = make_plan(B.lpB, 1, B.f1 - B.f0, B.w, CI, CP, B.R, eps, 1, FGF_SUB_NEAREST)))
@@ -128,7 +152,163 @@ int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int
     B.o_ab = B.o_abx + align_up(nc * B.ext_plane * sizeof(float));    // a, b rows [f0, f1)
     B.o_mean = B.o_ab + align_up(nc * B.ab_plane * sizeof(float));    // mean rows [f0, f1)
     B.ws_total = B.o_mean + align_up(nc * B.ab_plane * sizeof(float));
+    if (nranks == 1) {            // one rank: the whole-image filter (fgf_filter_band_ex)
+        if ((rc = make_plan(B.pb, 1, rows, W, CI, CP, r, eps, s, sub))) return rc;
+        B.ws_total = std::max(B.ws_total, plan_ws(B.pb, true));
+    }
     return FGF_OK;
+}
+
+// Overlapped single exchange (the default when every band holds >= 4r' + 2 low-res rows):
+//   caller's stream: the low-res chain of the band's own rows as an image of its own (samples
+//     read in place, any engine) -> interior maps, exact on rows [y0 + 2r', y1 - 2r') (and on
+//     every row at a global image border); meanwhile on the library's comm stream:
+//   comm stream: K0 compacts the 4r' own rows next to each inner band edge into an edge strip,
+//     whose first / last 2r' + 1 rows are the halo the neighbour needs; NCCL send / recv of
+//     those rows straight into the neighbours' edge strips; the low-res chain of each edge
+//     strip gives the maps of rows [y0 - 1, y0 + 2r') and [y1 - 2r', y1 + 1);
+//   caller's stream (after both): the maps are assembled on rows [y0 - 1, y1 + 1) and K4
+//   writes the own rows.  The exchange runs under the interior chain; with one rank the path
+//   is exactly the whole-image filter.
+int band_plan_overlap(BandPlan& B, bool self_guided, double eps) {
+    B.ovl = false;
+    const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;   // neighbours above / below
+    const int R = B.R, hb = B.y1 - B.y0;
+    if (B.mode != FGF_BAND_SINGLE || hb < 4 * R + 2) return FGF_ERR_UNSUPPORTED;
+    int rc = make_plan(B.pb, 1, B.rows, B.W, B.CI, B.CP, B.r_full, eps, B.s, B.sub);
+    if (rc) return rc;
+    if (B.pb.h != hb || B.pb.w != B.w || B.pb.R != R) return FGF_ERR_UNSUPPORTED;
+    B.m0 = up ? B.y0 - 1 : B.y0;
+    B.m1 = down ? B.y1 + 1 : B.y1;
+    B.t0 = std::max(0, B.y0 - 2 * R - 1);
+    B.t1 = B.y0 + 4 * R;
+    B.b0 = B.y1 - 4 * R;
+    B.b1 = std::min(B.h, B.y1 + 2 * R + 1);
+    if ((rc = make_plan(B.pe_t, 1, B.t1 - B.t0, B.w, B.CI, B.CP, R, eps, 1, FGF_SUB_NEAREST)))
+        return rc;
+    if ((rc = make_plan(B.pe_b, 1, B.b1 - B.b0, B.w, B.CI, B.CP, R, eps, 1, FGF_SUB_NEAREST)))
+        return rc;
+    const size_t w = B.w, nc = B.pb.NC;
+    size_t o = 0;
+    B.o_slot = o; o += align_up(plan_ws(B.pb, false));
+    B.o_int = o;  o += align_up(nc * hb * w * sizeof(float));
+    B.o_et = o;   o += align_up((size_t)B.NPL * (B.t1 - B.t0) * w * sizeof(float));
+    B.o_etw = o;  o += align_up(plan_ws(B.pe_t, false));
+    B.o_etm = o;  o += align_up(nc * (B.t1 - B.t0) * w * sizeof(float));
+    B.o_eb = o;   o += align_up((size_t)B.NPL * (B.b1 - B.b0) * w * sizeof(float));
+    B.o_ebw = o;  o += align_up(plan_ws(B.pe_b, false));
+    B.o_ebm = o;  o += align_up(nc * (B.b1 - B.b0) * w * sizeof(float));
+    B.o_fin = o;  o += align_up(nc * (B.m1 - B.m0) * w * sizeof(float));
+    B.ws_total = std::max(B.ws_total, o);
+    B.ovl = true;
+    (void)self_guided;
+    return FGF_OK;
+}
+
+// Edge strips: K0 compacts the own rows [y0, t1) (top) and [b0, y1) (bottom) of every plane.
+int band_ovl_prepare(const BandPlan& B, const float* I, const float* p, char* ws, cudaStream_t st) {
+    const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;
+    const size_t own = (size_t)B.rows * B.W, w = B.w;
+    auto strip = [&](int e0, int e1, int a0, int a1, size_t off) -> int {
+        // own low-res rows [a0, a1) into the strip of rows [e0, e1) at offset off
+        float* ext = reinterpret_cast<float*>(ws + off);
+        Plan sp{};
+        sp.W = B.W; sp.s = B.s; sp.sub = B.sub; sp.w = B.w;
+        sp.h = a1 - a0;
+        sp.H = std::min(B.rows - (a0 - B.y0) * B.s, (a1 - a0) * B.s);
+        for (int j = 0; j < B.NPL; ++j) {
+            const float* src = (j < B.CI ? I + j * own : p + (j - B.CI) * own) +
+                               (size_t)(a0 - B.y0) * B.s * B.W;
+            float* dst = ext + (size_t)j * (e1 - e0) * w + (size_t)(a0 - e0) * w;
+            int rc = launch_subsample(src, dst, 1, sp, st);
+            if (rc) return rc;
+        }
+        return FGF_OK;
+    };
+    int rc;
+    if (up && (rc = strip(B.t0, B.t1, B.y0, B.t1, B.o_et))) return rc;
+    if (down && (rc = strip(B.b0, B.b1, B.b0, B.y1, B.o_eb))) return rc;
+    return FGF_OK;
+}
+
+// Halo of plane j for the overlapped exchange: own rows [y0, y0 + 2r' + 1) go up and arrive as
+// the upper neighbour's rows [y1', b1'); own rows [y1 - 2r' - 1, y1) go down.
+Halo band_ovl_halo(const BandPlan& B, char* ws, int j) {
+    const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;
+    Halo hl{};
+    const size_t w = B.w;
+    const int H2 = 2 * B.R + 1;
+    if (up) {
+        float* et = reinterpret_cast<float*>(ws + B.o_et) + (size_t)j * (B.t1 - B.t0) * w;
+        hl.n_up = (size_t)(B.y0 - B.t0) * w;
+        hl.send_up = et + (size_t)(B.y0 - B.t0) * w;            // own rows [y0, y0 + H2)
+        hl.recv_up = et;                                        // rows [t0, y0)
+        if (B.y0 - B.t0 != H2) hl.n_up = 0;                     // (validated by the plan)
+    }
+    if (down) {
+        float* eb = reinterpret_cast<float*>(ws + B.o_eb) + (size_t)j * (B.b1 - B.b0) * w;
+        hl.n_down = (size_t)(B.b1 - B.y1) * w;
+        hl.send_down = eb + (size_t)(B.y1 - H2 - B.b0) * w;     // own rows [y1 - H2, y1)
+        hl.recv_down = eb + (size_t)(B.y1 - B.b0) * w;          // rows [y1, b1)
+    }
+    return hl;
+}
+
+// Interior: the band's own rows as an image (the whole-image low-res chain, in place).
+int band_ovl_interior(const BandPlan& B, const float* I, const float* p, char* ws, cudaStream_t st) {
+    return run_lowres(I, p, reinterpret_cast<float*>(ws + B.o_int), 0, 1, B.pb, ws + B.o_slot, st);
+}
+
+// Edge chains (after the exchange): maps of the edge strips.
+int band_ovl_edges(const BandPlan& B, char* ws, bool self_guided, cudaStream_t st) {
+    const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;
+    auto chain = [&](const Plan& pe, size_t o_e, size_t o_w, size_t o_m) {
+        const float* ext = reinterpret_cast<const float*>(ws + o_e);
+        const size_t pl = pe.n;
+        return run_coefficients(ext, self_guided ? ext : ext + B.CI * pl,
+                                reinterpret_cast<float*>(ws + o_m), pe, ws + o_w,
+                                plan_ws(pe, false), st);
+    };
+    int rc;
+    if (up && (rc = chain(B.pe_t, B.o_et, B.o_etw, B.o_etm))) return rc;
+    if (down && (rc = chain(B.pe_b, B.o_eb, B.o_ebw, B.o_ebm))) return rc;
+    return FGF_OK;
+}
+
+// Assembly of the maps of rows [m0, m1): interior rows, then (edges = true) the edge rows.
+int band_ovl_assemble(const BandPlan& B, char* ws, bool edges, cudaStream_t st) {
+    const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;
+    const size_t w = B.w, hm = B.m1 - B.m0, nc = B.pb.NC;
+    float* fin = reinterpret_cast<float*>(ws + B.o_fin);
+    auto cp = [&](const float* src, size_t src_rows, int src_r0, int dst_r0, int n) -> int {
+        for (size_t m = 0; m < nc; ++m)
+            if (cudaMemcpyAsync(fin + (m * hm + (dst_r0 - B.m0)) * w,
+                                src + (m * src_rows + src_r0) * w, (size_t)n * w * sizeof(float),
+                                cudaMemcpyDeviceToDevice, st))
+                return FGF_ERR_CUDA;
+        return FGF_OK;
+    };
+    int rc;
+    if (!edges) return cp(reinterpret_cast<const float*>(ws + B.o_int), B.y1 - B.y0, 0, B.y0, B.y1 - B.y0);
+    const int R = B.R;
+    if (up &&
+        (rc = cp(reinterpret_cast<const float*>(ws + B.o_etm), B.t1 - B.t0, B.y0 - 1 - B.t0,
+                 B.y0 - 1, 2 * R + 1)))
+        return rc;
+    if (down &&
+        (rc = cp(reinterpret_cast<const float*>(ws + B.o_ebm), B.b1 - B.b0, B.y1 - 2 * R - B.b0,
+                 B.y1 - 2 * R, 2 * R + 1)))
+        return rc;
+    return FGF_OK;
+}
+
+// K4 on the own rows from the assembled maps.
+int band_ovl_output(const BandPlan& B, const float* I, float* q, char* ws, cudaStream_t st) {
+    Plan P{};
+    P.batch = 1; P.H = B.rows; P.W = B.W; P.CI = B.CI; P.CP = B.CP; P.NC = B.pb.NC;
+    P.h = B.m1 - B.m0; P.w = B.w; P.N = (size_t)B.rows * B.W; P.n = (size_t)P.h * B.w; P.TR = 32;
+    const Band band{B.H, B.h, B.row0, B.m0, B.m1 - B.m0};
+    return launch_output(I, reinterpret_cast<const float*>(ws + B.o_fin), q, 1, P, st, &band);
 }
 
 // Two-step: statistics + a, b on the extended I', p' rows (strip engine K1), then the own
@@ -172,11 +352,6 @@ int band_prepare(const BandPlan& B, const float* I, const float* p, char* ws, cu
     return FGF_OK;
 }
 
-// Halo geometry of plane j: the rows this rank sends up / down and receives from up / down.
-struct Halo {
-    float *send_up, *send_down, *recv_up, *recv_down;
-    size_t n_up, n_down;     // floats (0 when there is no neighbour on that side)
-};
 Halo band_halo(const BandPlan& B, char* ws, int j, int rank, int nranks) {
     float* ext = reinterpret_cast<float*>(ws + B.o_ext) + j * B.ext_plane;
     Halo hl{};

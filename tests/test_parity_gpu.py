@@ -343,3 +343,42 @@ def test_colour_stats_cta_widths_agree(monkeypatch, cfg):
     assert compare(I, p, q128, **prm) <= tol
     assert compare(I, p, q256, **prm) <= tol
     assert float((q128 - q256).abs().max()) <= tol
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_library_graph_cache(monkeypatch, cfg):
+    """Small calls repeated with the same arguments on a non-default stream are replayed from
+    the library's CUDA-graph cache (captured on the second occurrence): bit-identical q to the
+    eager path (FGF_GRAPHS=0), new input VALUES are seen by the replay, the reported launch
+    count is the graph's."""
+    H, W, B = (256, 256, 1) if cfg == 0 else ((540, 960, 1) if cfg == 1 else (270, 480, 2))
+    I, p = synth.make_batch(cfg, "cuda", batch=B, H=H, W=W)
+    prm = synth.params(cfg)
+    CI, CP = I.shape[1], p.shape[1]
+    nb = fgf.fgf_workspace_bytes(B, H, W, CI, CP, prm["r"], prm["s"])
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    args = (B, H, W, CI, CP, prm["r"], prm["eps"], prm["s"], prm["sub_mode"], ws, nb, st)
+    monkeypatch.setenv("FGF_GRAPHS", "0")
+    q_ref = torch.empty((B, CP, H, W), device="cuda")
+    fgf.fgf_filter_ws(I, p, q_ref, *args)
+    n_eager = fgf.fgf_last_launch_count()
+    monkeypatch.delenv("FGF_GRAPHS")
+    q = torch.empty_like(q_ref)
+    for _ in range(4):                    # eager, capture + replay, replay, replay
+        q.zero_()
+        st.synchronize()
+        fgf.fgf_filter_ws(I, p, q, *args)
+        assert fgf.fgf_last_launch_count() == n_eager
+        st.synchronize()
+        assert torch.equal(q, q_ref)
+    # new input values through the cached graph
+    I2 = (I * 0.5 + 0.25).contiguous()
+    I.copy_(I2)
+    if cfg == 0:
+        p = I
+    torch.cuda.synchronize()
+    fgf.fgf_filter_ws(I, p, q, *args)
+    st.synchronize()
+    assert compare(I, p, q, **prm) <= tol(prm["eps"])

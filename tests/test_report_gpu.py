@@ -73,7 +73,9 @@ def test_config_report(cfg, s_over, sample):
     q = torch.empty((B, CP, H, W), device="cuda")
     nb = fgf.fgf_workspace_bytes(B, H, W, CI, CP, r, s)
     ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-    st = torch.cuda.current_stream()
+    # a non-default stream: small repeated calls replay from the library's graph cache
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream()
 
     def call():
         fgf.fgf_filter_ws(I, p, q, B, H, W, CI, CP, r, eps, s, sub, ws, nb, st)
@@ -91,6 +93,12 @@ def test_config_report(cfg, s_over, sample):
         times.append(a.elapsed_time(b))
     t_med = statistics.median(times)
     launches = fgf.fgf_last_launch_count()
+    # per-kernel CUDA-event times of one more call (profiling runs the launches eagerly)
+    fgf.fgf_profile_enable(True)
+    call()
+    torch.cuda.synchronize()
+    kern = {k: round(v[0], 5) for k, v in fgf.fgf_profile_read().items() if v[1]}
+    fgf.fgf_profile_enable(False)
 
     # parity on the sampled images
     tol = 1e-4 if eps >= 1e-3 else 1e-3
@@ -132,8 +140,18 @@ def test_config_report(cfg, s_over, sample):
         "max_abs_dq": worst, "tol": tol, "pass": worst <= tol, "oracle_images": sample,
         "oracle_mpx_s": N / oracle_s / 1e6, "host_cores": os.cpu_count(),
         "sm_clock_mhz": _sm_clock(), "psnr_vs_s1_db": psnr,
-        "kernel_launches": launches,
+        "kernel_launches": launches, "kernel_ms": kern,
     }
+    # B_ncu: DRAM bytes of every kernel of one call from a committed ncu launch list
+    # (tools/ncu_bytes.py writes FGF_NCU_BYTES: {"<name>_s<s>": bytes})
+    nb_path = os.environ.get("FGF_NCU_BYTES")
+    if nb_path and os.path.exists(nb_path):
+        d = json.load(open(nb_path)).get(f"{c['name']}_s{s}")
+        if d:
+            rec["B_ncu"] = d["bytes"]
+            rec["ncu_kernel_ms"] = d["ms"]
+            rec["frac_ncu_meas"] = d["bytes"] / (t_med / 1e3) / (peak * 1e9)
+            rec["frac_ncu_8T"] = d["bytes"] / (t_med / 1e3) / 8e12
     out = os.environ.get("FGF_REPORT")
     if out:
         with open(out, "a") as f:
