@@ -70,9 +70,12 @@ inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
     const long long cols = (long long)best.strips * images;
     long long th = ((long long)h * cols + 2 * 3 * 148 - 1) / (2 * 3 * 148);
-    // (cap: half the image height, at least 256 rows -- config 4 s = 4: 512-row segments
-    // 3.90 -> 3.78 ms; s = 8: 256 (= h / 2) best; whole-image segments were slower)
-    const long long cap = std::max<long long>(256, (h + 1) / 2);
+    // (cap: half the image height, at least 256 and at most 512 rows -- config 4 s = 4:
+    // 512-row segments 3.90 -> 3.78 ms; s = 8: 256 (= h / 2) best; whole-image segments were
+    // slower.  The upper bound keeps stage B's fp32 running column sums (R17) to <= 512
+    // add / remove steps per segment, whatever the image height: ADVICE r1; an fp64 or
+    // periodically re-summed variant measured 3-6 % slower on config 4)
+    const long long cap = std::max<long long>(256, std::min<long long>(512, (h + 1) / 2));
     th = std::min<long long>(cap, std::max<long long>(th, std::max(8, 2 * R + 2)));
     if (const char* e = dev_env("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));

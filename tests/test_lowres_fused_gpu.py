@@ -124,3 +124,20 @@ def test_strip_engine_still_parity_green():
         q = fgf.filter(I, p, 8, 0.01, 4, 0)
         torch.cuda.synchronize()
     assert oracle_err(I, p, q, 8, 0.01, 4, 0) <= 1e-4
+
+
+def test_tall_image_default_segments():
+    """K13 on a 4000-row image: the default geometry caps segments at 512 rows, so
+    stage B's fp32 running column sums (R17) take at most 512 add / remove steps; the result
+    stays within the oracle tolerance at eps = 1e-3."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    I = torch.rand((1, 1, 4000, 96), device="cuda", generator=g)
+    p = (I + 0.2 * torch.rand((1, 1, 4000, 96), device="cuda", generator=g)).clamp(0, 1)
+    with env(FGF_ENGINE="k13"):
+        fgf.fgf_profile_enable(True)
+        q = fgf.filter(I, p, 3, 1e-3, 1, 0)
+        torch.cuda.synchronize()
+        prof = fgf.fgf_profile_read()
+        fgf.fgf_profile_enable(False)
+    assert prof["lowres_fused"][1] == 1, prof
+    assert oracle_err(I, p, q, 3, 1e-3, 1, 0) <= 1e-4
