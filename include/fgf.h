@@ -42,8 +42,19 @@
  * how a batch is split across calls or devices.
  *
  * PRECISION.  fp32 storage; box statistics, var/cov and the 3x3 solve in fp64; a, b stored
- * in fp32; the box of a, b accumulated in fp64 (colour guidance) or fp32 (gray guidance,
- * DESIGN.md R17); upsample + output in fp32.
+ * in fp32; the box of a, b accumulated in fp64 (colour guidance; gray guidance at s = 1 and
+ * for wide windows, engine K5) or fp32 (gray guidance in K13, R17, at most 512
+ * running steps per segment); upsample + output in fp32.
+ *
+ * ENGINES (one choice per call, fixed by the arguments): gray guidance at s = 1
+ * runs the exact guided filter (Alg. 1) as ONE kernel (K5) for r >= 4; gray guidance at s > 1
+ * runs K13 (r' <= 12) or K5 (wider r'), then K4; colour guidance runs K0/K1/K3 then K4.
+ *
+ * GRAPH CACHE.  fgf_filter_ws / fgf_filter_ex_ws calls of at most 32 Mi output pixels on a
+ * non-default stream are recorded on their first occurrence and, when the same arguments
+ * (pointers, sizes, parameters, workspace, stream) occur again, captured into a CUDA graph and
+ * replayed from then on (no per-launch host cost, no validation queries: the caller keeps the
+ * buffers valid, as for any call).  FGF_GRAPHS=0 in the environment turns this off.
  */
 #ifndef FGF_H
 #define FGF_H

@@ -43,6 +43,10 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
         // small launches (single images): shorter bands until ~2 waves of 4 CTAs per SM exist
         const long long ncb = (P.W + 256 * PX - 1) / (256 * PX);
         while (op.TR > 8 && ncb * ((P.H + op.TR - 1) / op.TR) * images < 2LL * 4 * 148) op.TR /= 2;
+        if (const char* e = dev_env("FGF_K4_TR")) {      // development knob: band height
+            const int tr = atoi(e);
+            if (tr >= 1 && tr <= op.TR) op.TR = tr;
+        }
         smem = (size_t)lowres_span(op.TR, op.Hg, op.hg) * NC * ncl * sizeof(float);
         if (smem > 200 * 1024) return FGF_ERR_UNSUPPORTED;
         // optional floor on the dynamic smem: caps K4 CTAs/SM so the low-res stream's CTAs

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
     // hb ring of this CTA: slot k, map m, output column t at ring[(k NAB + m) TW + t]
     float* const ring0 = P.ring + (size_t)blockIdx.x * RS * NAB * TW + tid;
     const int slotStride = NAB * TW;
-    float* const ringEnd = ring0 + (size_t)RS * slotStride;
+    const int ringLen = RS * slotStride;              // ring offsets (floats) wrap at ringLen
     auto ldE = [](const E* p) { return ElemT<E>::load(p); };
 
     for (int item = blockIdx.x; item < P.items; item += gridDim.x) {
@@ -251,13 +251,14 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
                 const bool oka = full || (colIn && y < yA1 && y + R < h);
                 const bool oks = full || (colIn && y < yA1 && y - R - 1 >= 0);
                 if constexpr (STAGE) {
-                    stage4((g * 2 + 0) * NIN, ai + g * row, oka);
-                    stage4((g * 2 + 1) * NIN, si + g * row, oks);
+                    stage4((g * 2 + 0) * NIN, ai, oka);
+                    stage4((g * 2 + 1) * NIN, si, oks);
 #pragma unroll
                     for (int c = 0; c < CP; ++c) {
-                        stage4((g * 2 + 0) * NIN + 1 + c, ap + c * cstr + g * row, oka);
-                        stage4((g * 2 + 1) * NIN + 1 + c, sp + c * cstr + g * row, oks);
+                        stage4((g * 2 + 0) * NIN + 1 + c, ap + c * cstr, oka);
+                        stage4((g * 2 + 1) * NIN + 1 + c, sp + c * cstr, oks);
                     }
+                    ai += row; ap += row; si += row; sp += row;
                 } else {
                     va[STAGE ? 0 : g][0] = oka ? ldE(ai + g * row) : 0.0f;
                     vs[STAGE ? 0 : g][0] = oks ? ldE(si + g * row) : 0.0f;
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
         double accB[NAB];
 #pragma unroll
         for (int m = 0; m < NAB; ++m) accB[m] = 0.0;
-        float* rslot = ring0;                              // ring slot of step ya
+        int rslot = 0;                                     // ring offset of step ya
         double* const va_t = VA + tid;                     // P0 snapshots of this column
         const double* const pa_t = VA + tid;               // P2: window ends tid - 1, tid + 2R
         double* const ab_t = AB + tid;                     // P2: a, b of column tid
@@ -320,21 +321,25 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             // guidance row of each output: issued now, used in P4
             float old[G][NAB];
             float Io[OUTQ ? G : 1];
+            // interior batches (warp-uniform): every step removes a ring row and emits an output
+            const bool fastS = nS == G && ya - RS >= yA0;
+            const bool fastO = nS == G && ya - R >= y0 && ya + G - 1 - R < y1;
             if (colO) {
-                float* rp = rslot;
+                int ro = rslot;
                 const E* ip = Iq + (ya - R) * row;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const int yy = ya + g;
-                    const bool sub = g < nS && yy - RS >= yA0;   // row yy - 2R - 1 was added
+                    const bool sub = fastS || (g < nS && yy - RS >= yA0);   // row yy - 2R - 1 was added
 #pragma unroll
-                    for (int m = 0; m < NAB; ++m) old[g][m] = sub ? rp[m * TW] : 0.0f;
+                    for (int m = 0; m < NAB; ++m) old[g][m] = sub ? ring0[ro + m * TW] : 0.0f;
                     if (OUTQ) {
                         const int yb = yy - R;
-                        Io[OUTQ ? g : 0] = (g < nS && yb >= y0 && yb < y1) ? ldE(ip + g * row) : 0.0f;
+                        Io[OUTQ ? g : 0] = (fastO || (g < nS && yb >= y0 && yb < y1)) ? ldE(ip) : 0.0f;
+                        ip += row;
                     }
-                    rp += slotStride;
-                    rp = rp == ringEnd ? ring0 : rp;
+                    ro += slotStride;
+                    ro = ro == ringLen ? 0 : ro;
                 }
             }
             __syncthreads();
@@ -382,32 +387,33 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             // ---- P4: horizontal box of a, b, vertical running window through the ring, output
             if (colO) {
                 const float ixB = invB[tid];
+                const float ixR = ixB * (float)invRow;
                 const bool first = tid == 0;
-                float* rp = rslot;
+                const bool fastA = nA == G;
+                int ro = rslot;
+                E* qrow = OUTQ ? static_cast<E*>(P.q) + (long long)img * CP * h * w + (long long)(ya - R) * w + xo
+                               : nullptr;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    if (g < nS) {
-                        if (g < nA) {
+                    if (fastO || g < nS) {
+                        if (fastA || g < nA) {
 #pragma unroll
                             for (int m = 0; m < NAB; ++m) {
                                 const double* q = pb_t + (g * NAB + m) * PW;
                                 const float hb = (float)(q[R2] - (first ? 0.0 : q[-1]));
-                                rp[m * TW] = hb;
+                                ring0[ro + m * TW] = hb;
                                 accB[m] += (double)hb;
                             }
                         }
 #pragma unroll
                         for (int m = 0; m < NAB; ++m) accB[m] -= (double)old[g][m];
                         const int yb = ya + g - R;
-                        if (yb >= y0 && yb < y1) {
-                            const float iy = (yb - R >= 0 && yb + R < h)
-                                                 ? (float)invRow
-                                                 : 1.0f / (float)wide_count(yb, h, R);
-                            const float inv = ixB * iy;
+                        if (fastO || (yb >= y0 && yb < y1)) {
+                            const float inv = (yb - R >= 0 && yb + R < h)
+                                                  ? ixR : ixB / (float)wide_count(yb, h, R);
                             if (OUTQ) {
                                 const float I = Io[OUTQ ? g : 0];
-                                E* qo = static_cast<E*>(P.q) + (long long)img * CP * h * w +
-                                        (long long)yb * w + xo;
+                                E* qo = qrow + (long long)g * w;
 #pragma unroll
                                 for (int c = 0; c < CP; ++c) {
                                     const float ma = fmaf(P.k1, (float)accB[2 * c] * inv,
@@ -428,15 +434,13 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
                             }
                         }
                     }
-                    rp += slotStride;
-                    rp = rp == ringEnd ? ring0 : rp;
+                    ro += slotStride;
+                    ro = ro == ringLen ? 0 : ro;
                 }
             }
-            // ring slot of the next batch's first step
-            for (int g = 0; g < G; ++g) {
-                rslot += slotStride;
-                rslot = rslot == ringEnd ? ring0 : rslot;
-            }
+            // ring offset of the next batch's first step
+            rslot += G * slotStride;
+            rslot = rslot >= ringLen ? rslot - ringLen : rslot;
         }
     }
 }
