@@ -52,7 +52,7 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
            "fgf_nccl_check", "fgf_band_geometry")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused",
-                "wide_fused")
+                "wide_fused", "tiny_fused")
 
 _P = ctypes.c_void_p
 _i, _d, _sz = ctypes.c_int, ctypes.c_double, ctypes.c_size_t

@@ -134,10 +134,15 @@ int choose_engine(const Plan& P) {
     const bool wide = wide_supports(P.CP, P.dtype) && wide_geom(g, P.h, P.w, P.R, P.CP, 1, P.s == 1);
     if (const char* e = dev_env("FGF_LOWRES"))
         if (strcmp(e, "strip") == 0) return ENG_STRIP;
+    const bool tiny = tiny_supports(P);
     if (const char* e = dev_env("FGF_ENGINE")) {
         if (strcmp(e, "strip") == 0) return ENG_STRIP;
         if (strcmp(e, "k13") == 0 && k13) return ENG_K13;
         if (strcmp(e, "wide") == 0 && wide) return ENG_WIDE;
+        if (strcmp(e, "tiny") == 0 && tiny) return ENG_TINY;
+        if (strcmp(e, "notiny") != 0 && tiny) return ENG_TINY;
+    } else if (tiny) {
+        return ENG_TINY;
     }
     if (P.s == 1 && wide) return ENG_WIDE;
     if (k13) return ENG_K13;
@@ -151,11 +156,11 @@ int choose_engine(const Plan& P) {
 //   K5:    [block-mean planes] [mean maps, unless it writes q itself (s = 1)] [hb rings]
 void plan_layout(Plan& P) {
     P.engine = choose_engine(P);
-    P.fused_out = P.engine == ENG_WIDE && P.s == 1;
+    P.fused_out = (P.engine == ENG_WIDE && P.s == 1) || P.engine == ENG_TINY;
     const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
     const bool planes = P.engine == ENG_STRIP ? (P.s > 1 || P.dtype != FGF_F32) : blk;
     const bool coef = P.engine == ENG_STRIP;
-    const bool mean = !P.fused_out;
+    const bool mean = !P.fused_out || P.engine == ENG_TINY;   // K6's maps-only fallback is K13
     const size_t per_img =
         (size_t)((planes ? P.CI + P.CP : 0) + (coef ? P.NC : 0) + (mean ? P.NC : 0)) * P.n *
         sizeof(float);
@@ -189,6 +194,7 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     // at s = 1), else K5 in its mean-maps mode.
     int eng = P.engine;
     if (P.fused_out && launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) eng = ENG_K13;
+    if (eng == ENG_TINY) return FGF_ERR_UNSUPPORTED;   // (K13 always takes K6's plans)
     // Gray guidance, block-mean samples (R4): K0 compacts I', p' into fp32 planes first.
     const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
     const float *Is = nullptr, *ps = nullptr;
@@ -321,6 +327,9 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
     if (!ws) return FGF_ERR_NULL;
     if (ws_bytes < plan_ws(P, true)) return FGF_ERR_NOMEM;
     char* base = static_cast<char*>(ws);
+    if (P.engine == ENG_TINY)   // small gray image: the whole filter in one kernel, no workspace
+        return launch_tiny(static_cast<const float*>(I), static_cast<const float*>(p),
+                           static_cast<float*>(q), P, st);
     if (P.fused_out) {
         // s = 1, gray guidance: the exact guided filter (Alg. 1) as one K5 launch over the
         // batch -- I and p read once, q written once.

@@ -29,7 +29,7 @@ constexpr size_t kChunkTargetBytes = 8ull << 30;  // low-res workspace bytes per
 
 // ---- optional per-launch event timing (fgf_profile_*)
 enum { KIND_SUB = 0, KIND_STATS = 1, KIND_MEAN = 2, KIND_OUT = 3, KIND_LOWRES = 4, KIND_WIDE = 5,
-       NKIND = 6 };
+       KIND_TINY = 6, NKIND = 7 };
 struct ProfRec {
     int kind;
     cudaEvent_t a, b;
@@ -61,7 +61,8 @@ extern Profiler g_prof;                   // fgf_api.cu
 const char* const kKindName[NKIND] = {"fgf K0 subsample", "fgf K1 statistics+coefficients",
                                       "fgf K3 box of a,b", "fgf K4 upsample+output",
                                       "fgf K13 fused low-res chain",
-                                      "fgf K5 radius-independent fused chain"};
+                                      "fgf K5 radius-independent fused chain",
+                                      "fgf K6 single-kernel small image"};
 
 // Around every launch: an NVTX range named after the kernel (timeline tools: nsys, ncu
 // --nvtx) and, when fgf_profile_enable(1) is on, a CUDA-event pair on the launching stream.
@@ -89,7 +90,7 @@ struct ProfScope {
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // Engine of steps 2-5 (and, for K5 at s = 1, of the whole filter), chosen once per plan.
-enum { ENG_STRIP = 0, ENG_K13 = 1, ENG_WIDE = 2 };
+enum { ENG_STRIP = 0, ENG_K13 = 1, ENG_WIDE = 2, ENG_TINY = 3 };
 
 // K5 geometry (fgf_k_wide.cu): strips of TW output columns, segments of TH rows, a persistent
 // grid of `grid` CTAs of NT threads, one hb ring of ring_bytes / grid per CTA.
@@ -173,6 +174,9 @@ bool wide_supports(int CP, int dtype);
 size_t wide_ring_reserve(int R, int CP);
 int launch_wide(const WideParams& wp, const WideGeom& g, int CP, int dtype, bool outq,
                 cudaStream_t st);
+// K6 (fgf_k_tiny.cu): the whole filter of small gray images in one kernel.
+bool tiny_supports(const Plan& P);
+int launch_tiny(const float* I, const float* p, float* q, const Plan& P, cudaStream_t st);
 // K13 (fgf_k_lowres.cu); dry = true: only report whether K13 serves this plan.
 int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaStream_t st,
                        bool dry = false);

@@ -88,12 +88,23 @@ size_t wide_ring_reserve(int R, int CP) {
                     sizeof(float));
 }
 
-template <int CP, bool OUTQ, typename E, int G = wide_g<CP>(), int MINB = kWideCtasPerSM>
+// Contiguous, 16-byte-aligned fp32 sample rows: TMA bulk copies can stage them.
+bool wide_bulk_ok(const WideParams& wp) {
+    // development knob FGF_WIDE_BULK=1: TMA bulk staging (measured slower than the per-thread
+    // cp.async staging: config 4 s = 1 13.85 vs 12.92 ms per 32 images, config 1 0.218 vs 0.205 ms)
+    if (!dev_env("FGF_WIDE_BULK")) return false;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(wp.srcI) | reinterpret_cast<uintptr_t>(wp.srcP);
+    return wp.col == 1 && (a & 15u) == 0 && wp.row % 4 == 0 && wp.imgI % 4 == 0 &&
+           wp.imgP % 4 == 0 && wp.planeP % 4 == 0 && wp.w % 4 == 0;
+}
+
+template <int CP, bool OUTQ, typename E, int G = wide_g<CP>(), int MINB = kWideCtasPerSM,
+          bool BULK = false>
 int launch_wide_t(const WideParams& wp0, const WideGeom& g, cudaStream_t st) {
-    auto kern = wide_gray_kernel<CP, G, OUTQ, E, MINB>;
+    auto kern = wide_gray_kernel<CP, G, OUTQ, E, MINB, BULK>;
     WideParams wp = wp0;
     wp.TW = g.TW; wp.TH = g.TH; wp.strips = g.strips; wp.segs = g.segs; wp.items = g.items;
-    wp.L = WideCfg<CP, G, sizeof(E) == 4>::layout(g.TW, g.R);
+    wp.L = WideCfg<CP, G, BULK ? 2 : (sizeof(E) == 4 ? 1 : 0)>::layout(g.TW, g.R);
     if (wp.L.total > 227 * 1024) return FGF_ERR_UNSUPPORTED;
     set_smem(kern, wp.L.total);
     // persistent grid: as many CTAs as fit on the GPU at once (at most the geometry's)
@@ -124,9 +135,14 @@ int launch_wide_cp(const WideParams& wp, const WideGeom& g, int CP, int dtype, c
     // (development knob) forces the 4-row / 8-row variant.
     int v = OUTQ ? 1 : 0;
     if (const char* e = dev_env("FGF_WIDE_V")) v = atoi(e) == 1 ? 1 : 0;
+    const bool bulk = wide_bulk_ok(wp);
     switch (CP) {
-        case 1: return v == 1 ? launch_wide_t<1, OUTQ, float, 8, 1>(wp, g, st)
-                              : launch_wide_t<1, OUTQ, float>(wp, g, st);
+        case 1:
+            if (v == 1)
+                return bulk ? launch_wide_t<1, OUTQ, float, 8, 1, true>(wp, g, st)
+                            : launch_wide_t<1, OUTQ, float, 8, 1>(wp, g, st);
+            return bulk ? launch_wide_t<1, OUTQ, float, 4, kWideCtasPerSM, true>(wp, g, st)
+                        : launch_wide_t<1, OUTQ, float>(wp, g, st);
     }
     return FGF_ERR_UNSUPPORTED;
 }

@@ -53,7 +53,7 @@ constexpr int kWideCtasPerSM = 2;
 
 struct WideLayout {
     int NCS, NCA;          // statistics columns TW + 4R, a, b columns TW + 2R
-    size_t oVA, oAB, oInvA, oInvB, oStage, total;
+    size_t oVA, oAB, oInvA, oInvB, oStage, oBar, total;
 };
 
 struct WideParams {
@@ -75,7 +75,12 @@ struct WideParams {
     WideLayout L;
 };
 
-template <int CP, int G, bool STAGE = true>
+constexpr int kWideBulkPitch = kWideMaxCols + 8;   // floats per bulk-staged row (16 B aligned)
+
+// STAGE: 0 = next batch's samples prefetched into registers (8/16-bit samples), 1 = by per-thread
+// cp.async into shared memory (fp32, strided samples), 2 = by TMA bulk copies of whole row
+// segments issued by one thread (fp32, contiguous 16-byte-aligned rows: s = 1 and K0 planes).
+template <int CP, int G, int STAGE = 1>
 struct WideCfg {
     static constexpr int NMAP = 2 + 2 * CP;   // I, II, p_c, Ip_c
     static constexpr int NAB = 2 * CP;        // a_c, b_c
@@ -91,7 +96,10 @@ struct WideCfg {
         L.oInvA = o; o = al(o + (size_t)kWidePitch * 8);
         L.oInvB = o; o = al(o + (size_t)kWidePitch * 4);
         // cp.async staging of the next batch's add / subtract sample rows (fp32 samples)
-        L.oStage = o; o = al(o + (STAGE ? (size_t)G * 2 * NIN * kWideMaxCols * 4 : 0));
+        L.oStage = o;
+        o = al(o + (STAGE == 2 ? (size_t)G * 2 * NIN * kWideBulkPitch * 4
+                               : STAGE == 1 ? (size_t)G * 2 * NIN * kWideMaxCols * 4 : 0));
+        L.oBar = o; o = al(o + 16);
         L.total = o;
         return L;
     }
@@ -136,19 +144,24 @@ __device__ __forceinline__ int wide_count(int i, int n, int R) {
 
 // grid: persistent (<= items CTAs, two per SM), block NT = round32(TW + 4R) <= 384, dynamic
 // smem L.total.
-template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM>
+template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM, bool BULK = false>
 __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParams P) {
-    // fp32 samples: the next batch's rows are prefetched by cp.async into shared memory (no
-    // registers held while in flight); 8/16-bit samples: into registers
+    // fp32 samples: the next batch's rows are prefetched into shared memory (no registers held
+    // while in flight) -- by TMA bulk copies of whole row segments when the rows are contiguous
+    // and aligned (BULK), else by per-thread cp.async; 8/16-bit samples: into registers
     constexpr bool STAGE = sizeof(E) == 4;
-    using C = WideCfg<CP, G, STAGE>;
+    constexpr int SMODE = BULK ? 2 : (STAGE ? 1 : 0);
+    static_assert(!BULK || sizeof(E) == 4, "bulk staging moves fp32 rows");
+    using C = WideCfg<CP, G, SMODE>;
     constexpr int NMAP = C::NMAP, NAB = C::NAB, NIN = 1 + CP, PW = kWidePitch;
     extern __shared__ __align__(16) unsigned char smem[];
     double* __restrict__ VA = reinterpret_cast<double*>(smem + P.L.oVA);     // [G][NMAP][PW]
     double* __restrict__ AB = reinterpret_cast<double*>(smem + P.L.oAB);     // [G][NAB][PW]
     double* __restrict__ invA = reinterpret_cast<double*>(smem + P.L.oInvA); // [NCA], 0 outside
     float* __restrict__ invB = reinterpret_cast<float*>(smem + P.L.oInvB);   // [TW]
-    float* __restrict__ stg = reinterpret_cast<float*>(smem + P.L.oStage);   // [G][2][NIN][384]
+    float* __restrict__ stg = reinterpret_cast<float*>(smem + P.L.oStage);   // [G][2][NIN][384 | 392]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.L.oBar);            // BULK: rows landed
+    uint32_t phase = 0;                                                      // BULK: parity
     const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NW = NT >> 5;
     const int h = P.h, w = P.w, R = P.R, TW = P.TW;
@@ -160,6 +173,10 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
     // zero pads once: prefix rows read [n, PW) as zeros and never write them
     for (int i = tid; i < G * NMAP * PW; i += NT) VA[i] = 0.0;
     for (int i = tid; i < G * NAB * PW; i += NT) AB[i] = 0.0;
+    if (BULK && tid == 0) {
+        mbar_init_cta(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     // hb ring of this CTA: slot k, map m, output column t at ring[(k NAB + m) TW + t]
     float* const ring0 = P.ring + (size_t)blockIdx.x * RS * NAB * TW + tid;
@@ -178,7 +195,12 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
         const int yA0 = max(0, y0 - R), yA1 = min(h, y1 + R);   // a, b rows [yA0, yA1)
         const int yEnd = y1 + R;                          // steps ya in [yA0, yEnd)
 
-        __syncthreads();   // the previous item's P2 / P4 have read invA / invB
+        __syncthreads();   // the previous item's P0 / P2 / P4 have read stg / invA / invB
+        if (BULK) {
+            // columns outside the image are never copied: they read these zeros
+            for (int i = tid; i < G * 2 * NIN * kWideBulkPitch; i += NT) stg[i] = 0.0f;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         for (int j = tid; j < NCA; j += NT) {
             const int ca = x0 - R + j;
             invA[j] = (ca >= 0 && ca < w) ? 1.0 / (double)wide_count(ca, w, R) : 0.0;
@@ -239,6 +261,48 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
                          ::"r"(d), "l"(ok ? src : colI), "r"(ok ? 4 : 0) : "memory");
         };
+        // BULK: one thread copies the batch's add / subtract sample-row segments (all planes)
+        // [ca, cb) of each row into the staging rows, completion on the mbarrier (tx bytes)
+        const int cs0a = (x0 - 2 * R) & ~3;                 // 16-byte-aligned segment origin
+        const int bca = max(0, cs0a), bcb = min(w, (x0 - 2 * R + NCS + 3) & ~3);
+        const int boff = (x0 - 2 * R) - cs0a;               // staging index of column x0 - 2R
+        auto bulk_batch = [&](int ya) {
+            const uint32_t nb = bcb > bca ? (uint32_t)(bcb - bca) * 4u : 0u;
+            int rows = 0;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int y = ya + g;
+                rows += (y < yA1 && y + R < h) + (y < yA1 && y - R - 1 >= 0);
+            }
+            const uint32_t tx = nb * (uint32_t)(rows * NIN);
+            const uint32_t b = smem_addr(bar);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(tx) : "memory");
+            if (nb == 0) return;
+            const float* baseI = static_cast<const float*>(P.srcI) + img * P.imgI + bca;
+            const float* baseP = static_cast<const float*>(P.srcP) + img * P.imgP + bca;
+            auto copy = [&](int slot, const float* src) {
+                const uint32_t d = smem_addr(stg + slot * kWideBulkPitch + (bca - cs0a));
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                    ::"r"(d), "l"(src), "r"(nb), "r"(b) : "memory");
+            };
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int y = ya + g;
+                if (y < yA1 && y + R < h) {
+                    copy((g * 2 + 0) * NIN, baseI + (long long)(y + R) * row);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        copy((g * 2 + 0) * NIN + 1 + c, baseP + c * cstr + (long long)(y + R) * row);
+                }
+                if (y < yA1 && y - R - 1 >= 0) {
+                    copy((g * 2 + 1) * NIN, baseI + (long long)(y - R - 1) * row);
+#pragma unroll
+                    for (int c = 0; c < CP; ++c)
+                        copy((g * 2 + 1) * NIN + 1 + c, baseP + c * cstr + (long long)(y - R - 1) * row);
+                }
+            }
+        };
         auto load_batch = [&](int ya) {
             const E* ai = colI + (ya + R) * row;
             const E* ap = colP + (ya + R) * row;
@@ -286,21 +350,44 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
         const double* const pb_t = AB + tid;               // P4: window ends tid - 1, tid + 2R
         const int R2 = 2 * R;
 
-        load_batch(yA0);
+        if (BULK) {
+            __syncthreads();                                // the zeroed staging rows are visible
+            if (tid == 0) bulk_batch(yA0);
+        } else {
+            load_batch(yA0);
+        }
         for (int ya = yA0; ya < yEnd; ya += G) {
             const int nA = max(0, min(G, yA1 - ya));       // a, b rows of this batch
             const int nS = min(G, yEnd - ya);              // steps of this batch
             // ---- P0: vertical windows of a, b rows [ya, ya + nA), snapshots
-            if constexpr (STAGE) asm volatile("cp.async.wait_group 0;" ::: "memory");
+            if (BULK) {
+                if (nA > 0) {
+                    mbar_wait_parity(bar, phase);
+                    phase ^= 1u;
+                }
+            } else if constexpr (STAGE) {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
             if (colS) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     if (g < nA) {
                         float xa[NIN], xs[NIN];
+                        if (BULK) {
+                            const int y = ya + g;
+                            const bool oka = colIn && y + R < h, oks = colIn && y - R - 1 >= 0;
+                            const float* bs = stg + boff + tid;
 #pragma unroll
-                        for (int k = 0; k < NIN; ++k) {
-                            xa[k] = STAGE ? stg_t[((g * 2 + 0) * NIN + k) * kWideMaxCols] : va[STAGE ? 0 : g][k];
-                            xs[k] = STAGE ? stg_t[((g * 2 + 1) * NIN + k) * kWideMaxCols] : vs[STAGE ? 0 : g][k];
+                            for (int k = 0; k < NIN; ++k) {
+                                xa[k] = oka ? bs[((g * 2 + 0) * NIN + k) * kWideBulkPitch] : 0.0f;
+                                xs[k] = oks ? bs[((g * 2 + 1) * NIN + k) * kWideBulkPitch] : 0.0f;
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < NIN; ++k) {
+                                xa[k] = STAGE ? stg_t[((g * 2 + 0) * NIN + k) * kWideMaxCols] : va[STAGE ? 0 : g][k];
+                                xs[k] = STAGE ? stg_t[((g * 2 + 1) * NIN + k) * kWideMaxCols] : vs[STAGE ? 0 : g][k];
+                            }
                         }
                         const double Ia = (double)xa[0], Is = (double)xs[0];
                         acc[0] += Ia - Is;
@@ -316,7 +403,8 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
                     }
                 }
             }
-            if (ya + G < yA1) load_batch(ya + G);
+            if (!BULK && ya + G < yA1) load_batch(ya + G);
+            if (BULK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // reads before the next copies
             // ring rows leaving the vertical windows of this batch's steps, and (s = 1) the
             // guidance row of each output: issued now, used in P4
             float old[G][NAB];
@@ -343,6 +431,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
                 }
             }
             __syncthreads();
+            if (BULK && tid == 0 && ya + G < yA1) bulk_batch(ya + G);   // in flight under P1-P4
             // ---- P1: prefix sums of the snapshotted rows
             for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row(VA + rs * PW, NCS, lane);
             __syncthreads();

@@ -32,8 +32,8 @@ def _cuda():
 def gpu_filter(I, p, r, eps, s, sub_mode):
     q = fgf.filter(I, p, r, eps, s, sub_mode)
     torch.cuda.synchronize()
-    # K13 (or K0/K1/K3) + K4, or K5 alone at s = 1, went through libfgf.so
-    assert fgf.fgf_last_launch_count() >= (1 if s == 1 and I.shape[1] == 1 else 2)
+    # K13 (or K0/K1/K3) + K4, or K5 / K6 alone, went through libfgf.so
+    assert fgf.fgf_last_launch_count() >= 1
     return q
 
 
@@ -382,3 +382,39 @@ def test_library_graph_cache(monkeypatch, cfg):
     fgf.fgf_filter_ws(I, p, q, *args)
     st.synchronize()
     assert compare(I, p, q, **prm) <= tol(prm["eps"])
+
+
+@pytest.mark.parametrize("B,H,W,r,s,sub,eps,selfg", [
+    (1, 256, 256, 8, 4, 0, 0.01, True),       # BASELINE.json config 0's geometry
+    (3, 203, 301, 7, 4, 0, 0.01, False),      # ragged, several images
+    (1, 251, 253, 16, 4, 1, 0.01, False),     # block mean, partial edge blocks (63 x 64)
+    (2, 64, 64, 8, 1, 0, 1e-6, False),        # s = 1 (64 x 64 low-res), eps class 1e-3
+    (1, 97, 370, 3, 3, 0, 0.02, False),       # odd s (33 x 124)
+    (1, 5, 7, 1, 2, 0, 0.01, False),          # tiny
+])
+def test_tiny_single_kernel(B, H, W, r, s, sub, eps, selfg):
+    """K6 (csrc/fgf_tiny.cuh): the whole filter of a small gray image (<= 4096 low-res samples,
+    r' <= 8) in ONE kernel -- vs the oracle, and vs K13 + K4 on the same inputs."""
+    import os
+    g = torch.Generator(device="cuda").manual_seed(H + W + r + s)
+    I = torch.rand((B, 1, H, W), device="cuda", generator=g)
+    p = I if selfg else torch.rand((B, 1, H, W), device="cuda", generator=g)
+    fgf.fgf_profile_enable(True)
+    q = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    prof = fgf.fgf_profile_read()
+    fgf.fgf_profile_enable(False)
+    assert {k: v[1] for k, v in prof.items() if v[1]} == {"tiny_fused": 1}, prof
+    assert compare(I, p, q, r, eps, s, sub) <= tol(eps)
+    old = {k: os.environ.get(k) for k in ("FGF_DEV", "FGF_ENGINE")}
+    os.environ.update(FGF_DEV="1", FGF_ENGINE="notiny")
+    try:
+        q2 = fgf.filter(I, p, r, eps, s, sub)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert float((q - q2).abs().max()) <= 2e-6

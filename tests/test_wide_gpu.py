@@ -83,9 +83,14 @@ def test_exact_guided_filter_one_kernel(B, H, W, r, eps):
     g = torch.Generator(device="cuda").manual_seed(H * 7 + W + r)
     I = torch.rand((B, 1, H, W), device="cuda", generator=g)
     p = torch.rand((B, 1, H, W), device="cuda", generator=g)
-    q, kinds = profiled(lambda: fgf.filter(I, p, r, eps, 1, 0))
+    with env(FGF_ENGINE="wide"):                    # (small images default to K6)
+        q, kinds = profiled(lambda: fgf.filter(I, p, r, eps, 1, 0))
     assert kinds == {"wide_fused": 1}, kinds        # Alg. 1 is ONE launch: q written directly
     assert oracle_err(I, p, q, r, eps, 1, 0) <= tol(eps)
+    with env(FGF_ENGINE="wide", FGF_WIDE_BULK=1):   # TMA bulk staging of the sample rows
+        qb = fgf.filter(I, p, r, eps, 1, 0)
+    torch.cuda.synchronize()
+    assert float((qb - q).abs().max()) == 0.0
 
 
 @pytest.mark.parametrize("V", ["0", "1"])

@@ -17,7 +17,9 @@ for line in out.splitlines():
         secs[-1].append(line)
 if not secs:
     sys.exit("no source page")
-sec = secs[min(which, len(secs) - 1)]
+if which >= len(secs):
+    sys.exit(1)            # no such kernel in the report (the caller's loop stops here)
+sec = secs[which]
 rows = list(csv.reader(sec[1:]))
 hdr, data = rows[0], rows[1:]
 ie = hdr.index("Instructions Executed")
