@@ -158,7 +158,9 @@ void plan_layout(Plan& P) {
     P.engine = choose_engine(P);
     P.fused_out = (P.engine == ENG_WIDE && P.s == 1) || P.engine == ENG_TINY;
     const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
-    const bool planes = P.engine == ENG_STRIP ? (P.s > 1 || P.dtype != FGF_F32) : blk;
+    // (development knob FGF_WIDE_COMPACT: K5 at s > 1 reads K0-compacted nearest samples)
+    const bool wcompact = P.engine == ENG_WIDE && P.s > 1 && dev_env("FGF_WIDE_COMPACT") != nullptr;
+    const bool planes = P.engine == ENG_STRIP ? (P.s > 1 || P.dtype != FGF_F32) : (blk || wcompact);
     const bool coef = P.engine == ENG_STRIP;
     const bool mean = !P.fused_out || P.engine == ENG_TINY;   // K6's maps-only fallback is K13
     const size_t per_img =
@@ -195,8 +197,10 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     int eng = P.engine;
     if (P.fused_out && launch_lowres_gray(LowresParams{}, nb, P, st, true) == FGF_OK) eng = ENG_K13;
     if (eng == ENG_TINY) return FGF_ERR_UNSUPPORTED;   // (K13 always takes K6's plans)
-    // Gray guidance, block-mean samples (R4): K0 compacts I', p' into fp32 planes first.
-    const bool blk = P.s > 1 && P.sub == FGF_SUB_BILINEAR;
+    // Gray guidance, block-mean samples (R4): K0 compacts I', p' into fp32 planes first (and,
+    // under the development knob FGF_WIDE_COMPACT, K5's nearest samples too).
+    const bool blk = (P.s > 1 && P.sub == FGF_SUB_BILINEAR) ||
+                     (eng == ENG_WIDE && P.s > 1 && P.ws_planes > 0 && dev_env("FGF_WIDE_COMPACT"));
     const float *Is = nullptr, *ps = nullptr;
     if (eng != ENG_STRIP && blk) {
         float* Isw = planes;

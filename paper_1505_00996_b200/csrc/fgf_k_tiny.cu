@@ -14,11 +14,11 @@ int launch_tiny(const float* I, const float* p, float* q, const Plan& P, cudaStr
     tp.I = I; tp.p = p; tp.q = q;
     tp.H = P.H; tp.W = P.W; tp.h = P.h; tp.w = P.w; tp.s = P.s; tp.sub = P.sub; tp.R = P.R;
     tp.eps = P.eps; tp.k1 = P.k1; tp.k0 = P.k0;
-    // output bands of ~16 rows per CTA (two 8-row groups of guidance loads; each CTA recomputes
-    // the tiny low-res chain, a few microseconds of on-chip work)
-    int rows = 16;
+    // output bands of ~4 rows per CTA (each CTA computes the low-res chain of the few rows its
+    // band needs; measured on config 0: 4 / 8 / 16 / 32-row bands 10.8 / 11.4 / 15.9 / 20.5 us)
+    int rows = 4;
     if (const char* e = dev_env("FGF_TINY_ROWS")) rows = std::max(1, atoi(e));   // development knob
-    tp.bands = std::max(1, std::min(128, (P.H + rows - 1) / rows));
+    tp.bands = std::max(1, std::min(296, (P.H + rows - 1) / rows));
     const size_t smem = tiny_smem((int)P.n);
     set_smem(tiny_gray_kernel, smem);
     dim3 grid(tp.bands, P.batch);
