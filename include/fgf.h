@@ -77,7 +77,7 @@ enum {
     FGF_ERR_CUDA = 6,        /* a CUDA call or kernel launch failed                        */
     FGF_ERR_NOMEM = 7,       /* workspace too small / device allocation failed             */
     FGF_ERR_NCCL = 8,        /* band path: NCCL missing, or a send/recv/group call failed   */
-    FGF_ERR_UNSUPPORTED = 9, /* r' > 240 with w > 512 (strip kernel limit)       */
+    FGF_ERR_UNSUPPORTED = 9, /* no engine serves the geometry (colour: r' > 240 with w > 512) */
     FGF_ERR_DEVICE = 10      /* a pointer is not device memory (device entry points) or is
                                 not host memory (fgf_filter_host)                           */
 };
@@ -105,7 +105,10 @@ enum {
 int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
                int C_p, int r, double eps, int s, int sub_mode);
 
-/* Bytes of device workspace fgf_filter_ws needs for these arguments (0 on invalid args). */
+/* Bytes of device workspace fgf_filter_ws needs for these arguments (0 on invalid args), the
+ * larger of the two subsampling modes.  It takes r, beyond SURVEY §8(b)'s six arguments,
+ * because the engine and so the workspace depend on r' (K5's hb rings grow with r'; K5 at
+ * s = 1 and K6 need no per-image maps at all). */
 size_t fgf_workspace_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s);
 
 /* As fgf_filter, with caller-owned DEVICE workspace (>= fgf_workspace_bytes, 256-byte

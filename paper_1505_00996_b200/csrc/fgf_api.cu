@@ -600,7 +600,7 @@ const char* fgf_status_str(int status) {
         case FGF_ERR_CUDA: return "CUDA error";
         case FGF_ERR_NOMEM: return "workspace too small or allocation failed";
         case FGF_ERR_NCCL: return "NCCL error";
-        case FGF_ERR_UNSUPPORTED: return "unsupported geometry (r' > 240 with w > 512)";
+        case FGF_ERR_UNSUPPORTED: return "unsupported geometry (no engine serves it)";
         case FGF_ERR_DEVICE: return "pointer is in the wrong memory space";
     }
     return "unknown status";
