@@ -8,7 +8,7 @@ PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 # one translation unit per kernel family, compiled in parallel (make -j), each in a single
 # ptxas pass: nvcc --split-compile made register allocation depend on the split count
-TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_wide fgf_k_tiny fgf_k_lowres fgf_k_lowres_v3 fgf_k_lowres_v3h \
+TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_wide fgf_k_tiny fgf_k_apps fgf_k_lowres fgf_k_lowres_v3 fgf_k_lowres_v3h \
        fgf_k_lowres_v3bf fgf_k_lowres_v3b
 OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h

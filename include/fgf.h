@@ -265,12 +265,30 @@ int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, i
                    double eps, int s, int sub_mode, double gain, void* workspace,
                    size_t ws_bytes, void* cuda_stream);
 
+/* Guidance of detail enhancement: the image itself (colour guidance for RGB, R20),
+ * or SPEC's shared gray guidance to_grayscale(img) = 0.299 R + 0.587 G + 0.114 B (S:48-51,
+ * S:297) with the three channels as the filtering input. */
+enum { FGF_GUIDE_SELF = 0, FGF_GUIDE_LUMA = 1 };
+
+/* fgf_enhance_ws with a choice of guidance.  FGF_GUIDE_SELF (or C = 1) is fgf_enhance_ws.
+ * FGF_GUIDE_LUMA with C = 3: a luminance kernel writes L into the workspace, the filter runs
+ * with I = L (C_I = 1) and p = the image (C_p = 3), and a blend kernel forms
+ * out = gain img + (1 - gain) q in place (three kernels' worth of extra traffic: the gain does
+ * not fold into the maps when the guidance is not the image).  Workspace:
+ * fgf_enhance_workspace_bytes (0 on invalid args).  Errors as fgf_enhance_ws; a bad guide is
+ * FGF_ERR_PARAM. */
+size_t fgf_enhance_workspace_bytes(int batch, int H, int W, int C, int r, int s, int guide);
+int fgf_enhance_ex_ws(const float* I, float* out, int batch, int H, int W, int C, int r,
+                      double eps, int s, int sub_mode, double gain, int guide, void* workspace,
+                      size_t ws_bytes, void* cuda_stream);
+
 /* Diagnostics (single-threaded use): per-kernel CUDA-event timing of the launches this
  * process enqueues.  fgf_profile_enable(1) clears old records and starts recording an event
  * pair around every kernel launch on its launching stream; fgf_profile_enable(0) stops.
  * fgf_profile_read() waits for the recorded events and writes, for each kernel kind
- * (0 = subsample K0, 1 = statistics + coefficients K1, 2 = box of a, b K3,
- * 3 = upsample + output K4, 4 = fused low-res chain K13 for gray guidance), the summed device milliseconds and the launch count, then
+ * (0 = subsample K0 (and the luminance kernel), 1 = statistics + coefficients K1, 2 = box of
+ * a, b K3, 3 = upsample + output K4 (and the enhance blend), 4 = fused low-res chain K13 for
+ * gray guidance, 5 = K5, 6 = K6), the summed device milliseconds and the launch count, then
  * clears the records.  Returns the number of kinds written (<= max_kinds) or -FGF_ERR_CUDA. */
 int fgf_profile_enable(int on);
 int fgf_profile_read(double* ms, int* launches, int max_kinds);

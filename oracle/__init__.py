@@ -55,6 +55,7 @@ def _load():
         lib.fgfo_upsample_output.argtypes = [F, D, D, i, i, i, i, i, i]
         lib.fgfo_filter.argtypes = [F, F, D, i, i, i, i, i, i, d, i, i]
         lib.fgfo_lowres_chain.argtypes = [D, D, i, i, i, i, i, i, d, D]
+        lib.fgfo_filter_f64.argtypes = [D, D, D, i, i, i, i, i, i, d, i, i]
         _lib = lib
     return _lib
 
@@ -186,14 +187,49 @@ def guided_filter(I, p, r: int, eps: float) -> np.ndarray:
     return fast_guided_filter(I, p, r, eps, 1, NEAREST)
 
 
-def enhance(I, gain: float, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
+def fast_guided_filter_f64(I, p, r: int, eps: float, s: int, sub_mode: int = NEAREST) -> np.ndarray:
+    """Alg. 2 on fp64 inputs (no rounding to fp32): I [B,C_I,H,W], p [B,C_p,H,W]."""
+    I = _f64(I)
+    p = _f64(p)
+    B, C_I, H, W = I.shape
+    C_p = p.shape[1]
+    if p.shape[0] != B or p.shape[2:] != (H, W):
+        raise ValueError("I and p shapes disagree")
+    q = np.empty((B, C_p, H, W), np.float64)
+    rc = _load().fgfo_filter_f64(_dptr(I), _dptr(p), _dptr(q), B, H, W, C_I, C_p, r, float(eps),
+                                 s, sub_mode)
+    if rc:
+        raise ValueError(f"oracle rejected arguments (rc={rc})")
+    return q
+
+
+def to_grayscale(img) -> np.ndarray:
+    """SPEC to_grayscale: luminance 0.299 R + 0.587 G + 0.114 B of a 3-channel image
+    [B,3,H,W] (identity for 1 channel), in double: [B,1,H,W]."""
+    x = np.asarray(img, dtype=np.float64)
+    if x.shape[1] == 1:
+        return x.copy()
+    if x.shape[1] != 3:
+        raise ValueError("to_grayscale takes 1 or 3 channels")
+    return (0.299 * x[:, 0] + 0.587 * x[:, 1] + 0.114 * x[:, 2])[:, None]
+
+
+def enhance(I, gain: float, r: int, eps: float, s: int, sub_mode: int = NEAREST,
+            guide: str = "self") -> np.ndarray:
     """Detail enhancement (PAPER.md Fig. 2 caption P:95-97, "enhanced images with x5 detail";
-    SPEC S:303-306 enhance): base = the self-guided filter of the image (I = p), then
+    SPEC S:303-306 enhance): base = the filter of the image (p = I) guided by the image itself
+    (guide = "self": colour guidance for RGB, R20) or by its luminance (guide =
+    "luma": SPEC's default shared gray guidance, I = to_grayscale(img)), then
     out = (I - base) * gain + base, in double, unclamped (S:266)."""
     I = _f32(I)
     if I.ndim == 2:
         I = I[None, None]
-    base = fast_guided_filter(I, I, r, eps, s, sub_mode)
+    if guide == "luma" and I.shape[1] == 3:
+        base = fast_guided_filter_f64(to_grayscale(I), I, r, eps, s, sub_mode)
+    elif guide in ("self", "luma"):
+        base = fast_guided_filter(I, I, r, eps, s, sub_mode)
+    else:
+        raise ValueError("guide must be 'self' or 'luma'")
     return (I.astype(np.float64) - base) * gain + base
 
 

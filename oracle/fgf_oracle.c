@@ -382,3 +382,40 @@ int fgfo_filter(const float* I, const float* p, double* q, int batch, int H, int
     free(mean_ab);
     return rc;
 }
+
+/* The whole Fast Guided Filter (Alg. 2) on fp64 inputs: I [batch][C_I][H][W] and
+ * p [batch][C_p][H][W] in double (e.g. a guidance computed in double, such as SPEC's
+ * to_grayscale luminance).  The same steps as fgfo_filter -- step 1 by
+ * fgfo_subsample, steps 2-5 by lowres_chain_one, steps 6-7 by fgfo_upsample and the product
+ * with the full-resolution I -- with no rounding of the inputs to fp32. */
+int fgfo_filter_f64(const double* I, const double* p, double* q, int batch, int H, int W,
+                    int C_I, int C_p, int r, double eps, int s, int sub_mode) {
+    int rc = check_args(batch, H, W, C_I, C_p, r, eps, s, sub_mode);
+    if (rc) return rc;
+    const int h = fgfo_lowres_dim(H, s), w = fgfo_lowres_dim(W, s);
+    const size_t N = (size_t)H * W, n = (size_t)h * w;
+    double* Is = (double*)malloc(sizeof(double) * n * C_I);
+    double* ps = (double*)malloc(sizeof(double) * n * C_p);
+    double* mean_ab = (double*)malloc(sizeof(double) * n * C_p * (C_I + 1));
+    double* up = (double*)malloc(sizeof(double) * N);
+    rc = (Is && ps && mean_ab && up) ? FGFO_OK : FGFO_ENOMEM;
+    for (int b = 0; b < batch && !rc; ++b) {
+        const double* Ib = I + (size_t)b * C_I * N;
+        const double* pb = p + (size_t)b * C_p * N;
+        double* qb = q + (size_t)b * C_p * N;
+        for (int j = 0; j < C_I; ++j) fgfo_subsample(Ib + (size_t)j * N, H, W, s, sub_mode, Is + (size_t)j * n);
+        for (int c = 0; c < C_p; ++c) fgfo_subsample(pb + (size_t)c * N, H, W, s, sub_mode, ps + (size_t)c * n);
+        rc = lowres_chain_one(Is, ps, h, w, C_I, C_p, fgfo_radius_lowres(r, s), eps, NULL, mean_ab);
+        for (int c = 0; c < C_p && !rc; ++c) {
+            double* qc = qb + (size_t)c * N;
+            fgfo_upsample(mean_ab + ((size_t)c * (C_I + 1) + C_I) * n, h, w, H, W, up);   /* mean_b */
+            for (size_t i = 0; i < N; ++i) qc[i] = up[i];
+            for (int j = 0; j < C_I; ++j) {
+                fgfo_upsample(mean_ab + ((size_t)c * (C_I + 1) + j) * n, h, w, H, W, up);
+                for (size_t i = 0; i < N; ++i) qc[i] = up[i] * Ib[(size_t)j * N + i] + qc[i];
+            }
+        }
+    }
+    free(Is); free(ps); free(mean_ab); free(up);
+    return rc;
+}

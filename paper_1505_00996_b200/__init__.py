@@ -38,6 +38,8 @@ FGF_BF16 = 2
 FGF_U8 = 3
 FGF_BAND_SINGLE = 0
 FGF_BAND_TWO_STEP = 1
+FGF_GUIDE_SELF = 0
+FGF_GUIDE_LUMA = 1
 FGF_SUB_NEAREST = 0
 FGF_SUB_BILINEAR = 1
 
@@ -50,7 +52,8 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_nccl_comm_init", "fgf_nccl_comm_destroy", "fgf_bands_loopback_workspace_bytes",
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
            "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
-           "fgf_nccl_check", "fgf_band_geometry")
+           "fgf_nccl_check", "fgf_band_geometry", "fgf_enhance_workspace_bytes",
+           "fgf_enhance_ex_ws")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused",
                 "wide_fused", "tiny_fused")
 
@@ -115,6 +118,10 @@ _lib.fgf_filter_joint_ws.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
 _lib.fgf_filter_joint_ws.restype = _i
 _lib.fgf_band_geometry.argtypes = [_i, _i, _i, _i, _i, _i, ctypes.POINTER(ctypes.c_int)]
 _lib.fgf_band_geometry.restype = _i
+_lib.fgf_enhance_workspace_bytes.argtypes = [_i] * 7
+_lib.fgf_enhance_workspace_bytes.restype = _sz
+_lib.fgf_enhance_ex_ws.argtypes = [_P, _P] + [_i] * 5 + [_d, _i, _i, _d, _i, _P, _sz, _P]
+_lib.fgf_enhance_ex_ws.restype = _i
 _lib.fgf_version.argtypes = []
 _lib.fgf_version.restype = ctypes.c_char_p
 
@@ -478,26 +485,42 @@ def upsample_output(I, mean_ab, s, stream=None):
     return q
 
 
+def fgf_enhance_workspace_bytes(batch, H, W, C, r, s, guide=FGF_GUIDE_SELF) -> int:
+    return _lib.fgf_enhance_workspace_bytes(batch, H, W, C, r, s, guide)
+
+
+def fgf_enhance_ex_ws(I, out, batch, H, W, C, r, eps, s, sub_mode, gain, guide, workspace,
+                      ws_bytes, stream=None, check=True):
+    rc = _lib.fgf_enhance_ex_ws(_addr(I), _addr(out), batch, H, W, C, r, float(eps), s,
+                                sub_mode, float(gain), guide, _addr(workspace), ws_bytes,
+                                _stream(stream))
+    if check:
+        _check(rc, "fgf_enhance_ex_ws")
+    return rc
+
+
 def enhance(I, gain=5.0, r=16, eps=0.01, s=4, sub_mode=FGF_SUB_NEAREST, out=None, stream=None,
-            workspace=None):
+            workspace=None, guide="self"):
     """Detail enhancement (Fig. 2; defaults = its r=16, eps=0.1^2, s=4, x5):
-    out = (I - q) gain + q with q the self-guided fast guided filter of I [B, C, H, W]."""
+    out = (I - q) gain + q with q the fast guided filter of I [B, C, H, W] guided by the image
+    itself (guide="self") or, for RGB, by its luminance (guide="luma", SPEC's default)."""
     import torch
     if I.dim() != 4 or not I.is_cuda or I.dtype != torch.float32 or not I.is_contiguous():
         raise ValueError("I must be a contiguous float32 CUDA tensor [B, C, H, W]")
+    gcode = {"self": FGF_GUIDE_SELF, "luma": FGF_GUIDE_LUMA}[guide]
     B, C, H, W = I.shape
     if out is None:
         out = torch.empty_like(I)
     else:
         _check_out(out, I.shape, I.dtype, I.device)
     ws = workspace or Workspace()
-    nbytes = fgf_workspace_bytes(B, H, W, C, C, r, s)
+    nbytes = fgf_enhance_workspace_bytes(B, H, W, C, r, s, gcode)
     if nbytes == 0:
-        _check(FGF_ERR_PARAM, "fgf_workspace_bytes")
+        _check(FGF_ERR_PARAM, "fgf_enhance_workspace_bytes")
     buf = ws.get(nbytes, I.device)
     st = _stream_of(I, stream)
     _keep(st, buf, out)
-    fgf_enhance_ws(I, out, B, H, W, C, r, eps, s, sub_mode, gain, buf, buf.numel(), st)
+    fgf_enhance_ex_ws(I, out, B, H, W, C, r, eps, s, sub_mode, gain, gcode, buf, buf.numel(), st)
     return out
 
 

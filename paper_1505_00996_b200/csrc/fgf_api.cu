@@ -1027,6 +1027,53 @@ int fgf_enhance_ws(const float* I, float* out, int batch, int H, int W, int C, i
     return run_all(I, I, out, P, workspace, ws_bytes, static_cast<cudaStream_t>(cuda_stream));
 }
 
+size_t fgf_enhance_workspace_bytes(int batch, int H, int W, int C, int r, int s, int guide) {
+    if (guide == FGF_GUIDE_LUMA && C == 3) {
+        // [luminance planes][the workspace of the gray-guided filter with 3 input channels]
+        Plan P0, P1;
+        if (make_plan(P0, batch, H, W, 1, 3, r, 1.0, s, FGF_SUB_NEAREST) ||
+            make_plan(P1, batch, H, W, 1, 3, r, 1.0, s, FGF_SUB_BILINEAR))
+            return 0;
+        return align_up((size_t)batch * H * W * sizeof(float)) +
+               std::max(plan_ws(P0, true), plan_ws(P1, true));
+    }
+    if (guide != FGF_GUIDE_SELF && guide != FGF_GUIDE_LUMA) return 0;
+    return fgf_workspace_bytes(batch, H, W, C, C, r, s);
+}
+
+int fgf_enhance_ex_ws(const float* I, float* out, int batch, int H, int W, int C, int r,
+                      double eps, int s, int sub_mode, double gain, int guide, void* workspace,
+                      size_t ws_bytes, void* cuda_stream) {
+    if (guide != FGF_GUIDE_SELF && guide != FGF_GUIDE_LUMA) return FGF_ERR_PARAM;
+    if (guide == FGF_GUIDE_SELF || C == 1)
+        return fgf_enhance_ws(I, out, batch, H, W, C, r, eps, s, sub_mode, gain, workspace,
+                              ws_bytes, cuda_stream);
+    g_last_launches = 0;
+    Plan P;   // SPEC's shared gray guidance: I = to_grayscale(img), p = img (3 channels)
+    int rc = make_plan(P, batch, H, W, 1, 3, r, eps, s, sub_mode);
+    if (rc) return rc;
+    if (!std::isfinite(gain) || gain < 0.0) return FGF_ERR_PARAM;
+    if (!I || !out || !workspace) return FGF_ERR_NULL;
+    if ((reinterpret_cast<uintptr_t>(I) | reinterpret_cast<uintptr_t>(out)) & 3u) return FGF_ERR_ALIGN;
+    const size_t img_bytes = (size_t)batch * 3 * P.N * sizeof(float);
+    if (overlaps(out, img_bytes, I, img_bytes)) return FGF_ERR_ALIAS;
+    if (!is_device_ptr(I) || !is_device_ptr(out) || !is_device_ptr(workspace)) return FGF_ERR_DEVICE;
+    const size_t o_lw = align_up((size_t)batch * P.N * sizeof(float));
+    if (ws_bytes < o_lw + plan_ws(P, true)) return FGF_ERR_NOMEM;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    float* L = static_cast<float*>(workspace);
+    if ((rc = launch_luma(I, L, batch, P.N, st))) return rc;
+    int launches = g_last_launches;
+    g_last_launches = 0;
+    if ((rc = run_all(L, I, out, P, static_cast<char*>(workspace) + o_lw, ws_bytes - o_lw, st)))
+        return rc;
+    launches += g_last_launches;
+    g_last_launches = 0;
+    rc = launch_blend(I, out, (size_t)batch * 3 * P.N, gain, st);
+    g_last_launches += launches;
+    return rc;
+}
+
 int fgf_filter(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
                int C_p, int r, double eps, int s, int sub_mode) {
     g_last_launches = 0;

@@ -174,6 +174,9 @@ bool wide_supports(int CP, int dtype);
 size_t wide_ring_reserve(int R, int CP);
 int launch_wide(const WideParams& wp, const WideGeom& g, int CP, int dtype, bool outq,
                 cudaStream_t st);
+// Application kernels (fgf_k_apps.cu): SPEC to_grayscale, and out = gain img + (1 - gain) q.
+int launch_luma(const float* img, float* L, int batch, size_t N, cudaStream_t st);
+int launch_blend(const float* img, float* q, size_t n, double gain, cudaStream_t st);
 // K6 (fgf_k_tiny.cu): the whole filter of small gray images in one kernel.
 bool tiny_supports(const Plan& P);
 int launch_tiny(const float* I, const float* p, float* q, const Plan& P, cudaStream_t st);

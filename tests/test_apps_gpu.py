@@ -98,3 +98,25 @@ def test_joint_with_subsampled_p_equals_filter():
     q2 = fgf.filter(I, p, 16, 0.01, 4, 0)
     torch.cuda.synchronize()
     assert float((q1 - q2).abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("H,W,r,eps,s,sub,gain", [
+    (540, 960, 16, 0.01, 4, 0, 5.0),      # Fig. 2 preset on an RGB image
+    (203, 301, 8, 0.02, 2, 1, 3.0),       # block mean, ragged
+    (128, 160, 6, 0.01, 1, 0, 2.0),       # s = 1
+])
+def test_enhance_luma_guidance_vs_oracle(H, W, r, eps, s, sub, gain):
+    """SPEC enhance with its default shared gray guidance: I = luminance
+    0.299 R + 0.587 G + 0.114 B, p = the RGB image (fgf_enhance_ex_ws,
+    FGF_GUIDE_LUMA) vs oracle.enhance(guide="luma") in fp64 end to end."""
+    g = torch.Generator(device="cuda").manual_seed(H + W + s)
+    I = torch.rand((2, 3, H, W), device="cuda", generator=g)
+    out = fgf.enhance(I, gain, r, eps, s, sub, guide="luma")
+    torch.cuda.synchronize()
+    ref = oracle.enhance(I.cpu().numpy(), gain, r, eps, s, sub, guide="luma")
+    err = float(np.abs(out.double().cpu().numpy() - ref).max())
+    assert err <= tol(eps, gain), err
+    # gain = 1: the image itself (to fp32 rounding of gain I + 0 q)
+    one = fgf.enhance(I, 1.0, r, eps, s, sub, guide="luma")
+    torch.cuda.synchronize()
+    assert torch.equal(one, I)

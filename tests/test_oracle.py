@@ -382,3 +382,56 @@ def test_joint_upsample_constant_input():
     p_low = np.full((1, 1, 10, 13), 0.625, np.float32)
     q = oracle.joint_upsample(I, p_low, 8, 1e-4, 4, 0)
     assert np.abs(q - 0.625).max() < 1e-9
+
+
+# ---------------------------------------------------------------- luminance guidance
+
+def test_to_grayscale_spec_examples():
+    """pixel (1, 0, 0) -> 0.299; a constant (c, c, c) -> c; 1 channel -> identity."""
+    px = np.array([1.0, 0.0, 0.0]).reshape(1, 3, 1, 1)
+    assert abs(float(oracle.to_grayscale(px)[0, 0, 0, 0]) - 0.299) < 1e-15
+    c = np.full((1, 3, 4, 5), 0.37)
+    assert np.abs(oracle.to_grayscale(c) - 0.37).max() < 1e-15
+    g = np.random.default_rng(0).random((2, 1, 3, 4))
+    assert np.array_equal(oracle.to_grayscale(g), g)
+
+
+def test_filter_f64_matches_fp32_entry_on_fp32_values():
+    """fgfo_filter_f64 follows the same steps as fgfo_filter: on inputs that are exactly fp32
+    values (widened exactly) the two agree to rounding of a reordered-free identical chain."""
+    rng = np.random.default_rng(61)
+    I = rng.random((2, 3, 29, 41)).astype(np.float32)
+    p = rng.random((2, 2, 29, 41)).astype(np.float32)
+    for s, sub in [(1, 0), (3, 0), (3, 1)]:
+        a = oracle.fast_guided_filter(I, p, 6, 0.01, s, sub)
+        b = oracle.fast_guided_filter_f64(I.astype(np.float64), p.astype(np.float64), 6, 0.01, s, sub)
+        assert np.abs(a - b).max() <= 1e-14
+
+
+def test_filter_f64_against_brute_force_composition():
+    """On a non-fp32 (double) guidance: Alg. 2 = brute-force composition of the pinned pieces
+    (subsample slicing, per-window ridge regression, interpolation matrices)."""
+    from tests import brute
+    rng = np.random.default_rng(62)
+    H, W, r, s, eps = 22, 27, 5, 2, 0.02
+    L = rng.random((1, 1, H, W)) / 3.0           # not representable in fp32
+    p = rng.random((1, 1, H, W))
+    q = oracle.fast_guided_filter_f64(L, p, r, eps, s, 0)
+    ref = brute.fast_guided_filter_brute(L[0, 0], p[0, 0], r, eps, s, 0)
+    assert np.abs(q[0, 0] - ref).max() <= 1e-12
+
+
+def test_enhance_luma_identities():
+    """SPEC enhance with its default shared gray guidance: gain = 1 returns
+    the image, gain = 0 the base layer; an image with R = G = B = g equals the gray
+    self-guided enhancement of g (its luminance is g)."""
+    rng = np.random.default_rng(63)
+    img = rng.random((1, 3, 33, 47)).astype(np.float32)
+    assert np.abs(oracle.enhance(img, 1.0, 8, 0.01, 4, 0, guide="luma") - img).max() <= 1e-12
+    base = oracle.fast_guided_filter_f64(oracle.to_grayscale(img), img, 8, 0.01, 4, 0)
+    assert np.abs(oracle.enhance(img, 0.0, 8, 0.01, 4, 0, guide="luma") - base).max() <= 1e-15
+    g = rng.random((1, 1, 33, 47)).astype(np.float32)
+    rgb = np.repeat(g, 3, axis=1)
+    e3 = oracle.enhance(rgb, 5.0, 8, 0.01, 4, 0, guide="luma")
+    e1 = oracle.enhance(g, 5.0, 8, 0.01, 4, 0)
+    assert np.abs(e3 - np.repeat(e1, 3, axis=1)).max() <= 1e-9
