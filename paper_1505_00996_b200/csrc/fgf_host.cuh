@@ -96,7 +96,7 @@ enum { ENG_STRIP = 0, ENG_K13 = 1, ENG_WIDE = 2, ENG_TINY = 3 };
 // grid of `grid` CTAs of NT threads, one hb ring of ring_bytes / grid per CTA.
 struct WideGeom {
     int TW = 0, NT = 0, strips = 0, segs = 0, TH = 0, items = 0, grid = 0, R = 0;
-    int KC = 1, slots = 0;       // statistics columns per thread; persistent CTA slots
+    int KC = 1, slots = 0, maxc = 0;   // columns per thread; persistent CTA slots; max TW + 4R
     size_t ring_bytes = 0;
 };
 

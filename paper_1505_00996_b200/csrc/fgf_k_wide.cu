@@ -46,7 +46,8 @@ bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, 
         // 4-row at KC = 2); the mean-maps mode 4-row batches, two CTAs per SM
         const int Gr = outq && CP == 1 ? (kc == 1 ? 8 : 4) : (CP == 1 ? 4 : (CP == 2 ? 2 : 1));
         const int slots = sm_count() * (outq && CP == 1 ? 1 : kWideCtasPerSM);
-        for (int TW = 32; TW + 4 * R <= kc * kWideMaxCols; TW += 32) {
+        const int maxc = kc == 1 && outq && CP == 1 ? wide_ntmax(1, 1) : kc * kWideMaxCols;
+        for (int TW = 32; TW + 4 * R <= maxc; TW += 32) {
             const int tw = std::min(TW, w);
             const int NT = ((tw + 4 * R + kc - 1) / kc + 31) / 32 * 32;
             if (kc == 2 && NT <= kWideMaxCols / 2) continue;   // fits one column per thread
@@ -61,7 +62,7 @@ bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, 
                 if (cost < best * 0.999) {
                     best = cost;
                     g.TW = tw; g.NT = NT; g.strips = strips; g.segs = segs; g.TH = TH;
-                    g.KC = kc; g.slots = slots;
+                    g.KC = kc; g.slots = slots; g.maxc = maxc;
                     g.items = (int)std::min<long long>(items, 1LL << 30);
                 }
                 if (items >= 64LL * slots) break;
@@ -74,7 +75,7 @@ bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, 
     // strips and segments on small images)
     if (const char* e = dev_env("FGF_WIDE_TW")) {
         const int tw = std::min(std::max(1, atoi(e)), w);
-        if (tw + 4 * R > g.KC * kWideMaxCols) return false;
+        if (tw + 4 * R > g.maxc) return false;
         g.TW = tw;
         g.NT = ((tw + 4 * R + g.KC - 1) / g.KC + 31) / 32 * 32;
         g.strips = (w + tw - 1) / tw;
@@ -97,7 +98,7 @@ size_t wide_ring_reserve(int R, int CP) {
     // two CTAs per SM of strips <= 384 - 4R, or one CTA per SM of strips <= 768 - 4R (KC = 2)
     const long long tw1 = kWideMaxCols - 4 * R, tw2 = 2 * kWideMaxCols - 4 * R;
     if (tw1 < 32) return 0;
-    const long long cols = std::max<long long>(kWideCtasPerSM * tw1, tw2);
+    const long long cols = std::max<long long>(kWideCtasPerSM * tw1, tw2);   // >= 416 - 4R too
     return align_up((size_t)sm_count() * cols * (2 * R + 1) * 2 * CP * sizeof(float));
 }
 
@@ -117,7 +118,8 @@ int launch_wide_t(const WideParams& wp0, const WideGeom& g, cudaStream_t st) {
     auto kern = wide_gray_kernel<CP, G, OUTQ, E, MINB, BULK, KC>;
     WideParams wp = wp0;
     wp.TW = g.TW; wp.TH = g.TH; wp.strips = g.strips; wp.segs = g.segs; wp.items = g.items;
-    wp.L = WideCfg<CP, G, BULK ? 2 : (sizeof(E) == 4 ? 1 : 0), KC>::layout(g.TW, g.R);
+    wp.L = WideCfg<CP, G, BULK ? 2 : (sizeof(E) == 4 ? 1 : 0), KC, wide_ntmax(MINB, KC)>::layout(g.TW, g.R);
+    if (g.NT > wide_ntmax(MINB, KC)) return FGF_ERR_UNSUPPORTED;   // (geometry of another variant)
     if (wp.L.total > 227 * 1024) return FGF_ERR_UNSUPPORTED;
     set_smem(kern, wp.L.total);
     // persistent grid: as many CTAs as fit on the GPU at once (at most the geometry's)

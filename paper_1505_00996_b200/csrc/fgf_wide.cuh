@@ -50,7 +50,11 @@ constexpr int kWideChMax = 13;          // prefix chunk per lane (KC = 1): rows 
 constexpr int kWidePitch = 32 * kWideChMax;   // fp64 row pitch of the snapshot / a, b rows (KC = 1)
 constexpr int kWideMaxCols = 384;       // threads per CTA (<= 384 statistics columns per KC)
 constexpr int kWideCtasPerSM = 2;
-constexpr int kWideBulkPitch = kWideMaxCols + 8;   // floats per bulk-staged row (16 B aligned)
+// threads per CTA of a variant (416 = one full prefix row was measured too: ptxas then caps the
+// one-CTA-per-SM variant at 128 registers and config 4 s = 1 took 13.5 vs 13.0 ms)
+__host__ __device__ constexpr int wide_ntmax(int MINB, int KC) {
+    return (void)MINB, (void)KC, kWideMaxCols;
+}
 
 // KC statistics columns per thread: rows of <= 32 CH columns, CH odd (conflict-free fp64 lanes)
 template <int KC>
@@ -86,8 +90,9 @@ struct WideParams {
 // STAGE: 0 = next batch's samples prefetched into registers (8/16-bit samples), 1 = by per-thread
 // cp.async into shared memory (fp32, strided samples), 2 = by TMA bulk copies of whole row
 // segments issued by one thread (fp32, contiguous 16-byte-aligned rows: s = 1 and K0 planes).
-template <int CP, int G, int STAGE = 1, int KC = 1>
+template <int CP, int G, int STAGE = 1, int KC = 1, int NTM = kWideMaxCols>
 struct WideCfg {
+    static constexpr int BULKP = NTM + 8;     // floats per bulk-staged row (16 B aligned)
     static constexpr int NMAP = 2 + 2 * CP;   // I, II, p_c, Ip_c
     static constexpr int NAB = 2 * CP;        // a_c, b_c
     static constexpr int NIN = 1 + CP;        // I, p_c
@@ -104,8 +109,8 @@ struct WideCfg {
         L.oInvB = o; o = al(o + (size_t)PW * 4);
         // staging of the next batch's add / subtract sample rows (fp32 samples)
         L.oStage = o;
-        o = al(o + (STAGE == 2 ? (size_t)G * 2 * NIN * kWideBulkPitch * 4
-                               : STAGE == 1 ? (size_t)G * 2 * NIN * KC * kWideMaxCols * 4 : 0));
+        o = al(o + (STAGE == 2 ? (size_t)G * 2 * NIN * BULKP * 4
+                               : STAGE == 1 ? (size_t)G * 2 * NIN * KC * NTM * 4 : 0));
         L.oBar = o; o = al(o + 16);
         L.total = o;
         return L;
@@ -155,7 +160,7 @@ __device__ __forceinline__ int wide_count(int i, int n, int R) {
 // threads, each owning KC statistics columns (tid + k NT), dynamic smem L.total.
 template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM, bool BULK = false,
           int KC = 1>
-__global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParams P) {
+__global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(WideParams P) {
     // fp32 samples: the next batch's rows are prefetched into shared memory (no registers held
     // while in flight) -- by TMA bulk copies of whole row segments when the rows are contiguous
     // and aligned (BULK), else by per-thread cp.async; 8/16-bit samples: into registers
@@ -163,10 +168,12 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
     constexpr int SMODE = BULK ? 2 : (STAGE ? 1 : 0);
     static_assert(!BULK || (sizeof(E) == 4 && KC == 1), "bulk staging moves fp32 rows, KC = 1");
     static_assert(STAGE || KC == 1, "8/16-bit samples: one column per thread");
-    using C = WideCfg<CP, G, SMODE, KC>;
+    constexpr int NTM = wide_ntmax(MINB, KC);
+    using C = WideCfg<CP, G, SMODE, KC, NTM>;
+    constexpr int kWideBulkPitch = C::BULKP;
     constexpr int NMAP = C::NMAP, NAB = C::NAB, NIN = 1 + CP, PW = C::PW;
     constexpr int CH = WidePitch<KC>::CH;
-    constexpr int SPR = KC * kWideMaxCols;                  // cp.async staging row pitch
+    constexpr int SPR = KC * NTM;                           // cp.async staging row pitch
     extern __shared__ __align__(16) unsigned char smem[];
     double* __restrict__ VA = reinterpret_cast<double*>(smem + P.L.oVA);     // [G][NMAP][PW]
     double* __restrict__ AB = reinterpret_cast<double*>(smem + P.L.oAB);     // [G][NAB][PW]
