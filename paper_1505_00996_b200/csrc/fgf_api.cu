@@ -338,8 +338,7 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
         // s = 1, gray guidance: the exact guided filter (Alg. 1) as one K5 launch over the
         // batch -- I and p read once, q written once.
         WideGeom g;
-        if (!wide_geom(g, P.h, P.w, P.R, P.CP, P.batch, true, P.dtype == FGF_F32) ||
-            g.ring_bytes > P.ws_ring)
+        if (!wide_geom(g, P.h, P.w, P.R, P.CP, P.batch, true) || g.ring_bytes > P.ws_ring)
             return FGF_ERR_UNSUPPORTED;
         WideParams wp{};
         wp.h = P.h; wp.w = P.w; wp.R = P.R; wp.eps = P.eps;
@@ -561,7 +560,7 @@ using namespace fgf;
 
 extern "C" {
 
-const char* fgf_version(void) { return "fgf-b200 0.1 (sm_100a)"; }
+const char* fgf_version(void) { return "fgf-b200 0.2 (sm_100a)"; }
 
 int fgf_last_launch_count(void) { return g_last_launches; }
 

@@ -96,7 +96,6 @@ enum { ENG_STRIP = 0, ENG_K13 = 1, ENG_WIDE = 2, ENG_TINY = 3 };
 // grid of `grid` CTAs of NT threads, one hb ring of ring_bytes / grid per CTA.
 struct WideGeom {
     int TW = 0, NT = 0, strips = 0, segs = 0, TH = 0, items = 0, grid = 0, R = 0;
-    int KC = 1, slots = 0, maxc = 0;   // columns per thread; persistent CTA slots; max TW + 4R
     size_t ring_bytes = 0;
 };
 
@@ -170,8 +169,7 @@ int launch_output(const void* I, const float* M, void* q, int images, const Plan
                   cudaStream_t st, const Band* band = nullptr);
 int lowres_span(int T, int n_dst, int n_src);
 // K5 (fgf_k_wide.cu): geometry for `images` images, and the launch (maps or, outq, q).
-bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq,
-               bool kc2_ok = false);
+bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq);
 bool wide_supports(int CP, int dtype);
 size_t wide_ring_reserve(int R, int CP);
 int launch_wide(const WideParams& wp, const WideGeom& g, int CP, int dtype, bool outq,

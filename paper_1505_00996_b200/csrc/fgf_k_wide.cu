@@ -29,55 +29,42 @@ int sm_count() {
 }  // namespace
 
 // Strip / segment geometry: minimise (waves of items over the persistent CTAs) x (work per
-// item ~ statistics columns x rows streamed), over strip widths TW with TW + 4R <= KC x 384
-// (KC statistics columns per thread; KC = 2 for the fused filter only: wider strips, less
-// halo, one CTA per SM).
-bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, bool kc2_ok) {
+// item ~ threads x rows streamed), with NT = round32(TW + 4R) <= 672 threads.
+bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq) {
     if (R < 4 || CP < 1 || CP > 4) return false;      // ring of 2R + 1 >= G rows
+    // persistent CTAs: the fused filter (s = 1) runs 8-row batches, one CTA per SM; the
+    // mean-maps mode 4-row batches, two CTAs per SM (measured on configs 1 and 4)
+    const int Gr = outq && CP == 1 ? 8 : (CP == 1 ? 4 : (CP == 2 ? 2 : 1));
+    const int slots = sm_count() * (outq && CP == 1 ? 1 : kWideCtasPerSM);
     double best = 1e300;
-    int kcForce = 0;
-    if (const char* e = dev_env("FGF_WIDE_KC")) kcForce = atoi(e);
-    for (int kc = 1; kc <= 2; ++kc) {
-        // KC = 2 only on request (FGF_WIDE_KC=2): measured slower than KC = 1 with 8-row
-        // batches (config 4 s = 1: 14.73 vs 13.06 ms per 32 images; config 1: 0.288 vs 0.212 ms)
-        if (kc == 2 && !(outq && CP == 1 && kc2_ok && kcForce == 2)) break;
-        if (kcForce && kc != kcForce) continue;
-        // persistent CTAs: the fused filter (s = 1) runs one CTA per SM (8-row batches at KC = 1,
-        // 4-row at KC = 2); the mean-maps mode 4-row batches, two CTAs per SM
-        const int Gr = outq && CP == 1 ? (kc == 1 ? 8 : 4) : (CP == 1 ? 4 : (CP == 2 ? 2 : 1));
-        const int slots = sm_count() * (outq && CP == 1 ? 1 : kWideCtasPerSM);
-        const int maxc = kc == 1 && outq && CP == 1 ? wide_ntmax(1, 1) : kc * kWideMaxCols;
-        for (int TW = 32; TW + 4 * R <= maxc; TW += 32) {
-            const int tw = std::min(TW, w);
-            const int NT = ((tw + 4 * R + kc - 1) / kc + 31) / 32 * 32;
-            if (kc == 2 && NT <= kWideMaxCols / 2) continue;   // fits one column per thread
-            const int strips = (w + tw - 1) / tw;
-            // segment counts: 1, 2, ... while a segment keeps >= 2R rows
-            for (int segs = 1; segs <= std::max(1, h / std::max(16, 2 * R)); ++segs) {
-                const int TH = (h + segs - 1) / segs;
-                const long long items = (long long)strips * segs * images;
-                const long long waves = (items + slots - 1) / slots;
-                const double per_item = (double)(tw + 4 * R) * (TH + 2 * R + Gr + R / 2.0);
-                const double cost = (double)waves * per_item;
-                if (cost < best * 0.999) {
-                    best = cost;
-                    g.TW = tw; g.NT = NT; g.strips = strips; g.segs = segs; g.TH = TH;
-                    g.KC = kc; g.slots = slots; g.maxc = maxc;
-                    g.items = (int)std::min<long long>(items, 1LL << 30);
-                }
-                if (items >= 64LL * slots) break;
+    for (int TW = 32; TW + 4 * R <= kWideMaxCols; TW += 32) {
+        const int tw = std::min(TW, w);
+        const int NT = (tw + 4 * R + 31) / 32 * 32;
+        const int strips = (w + tw - 1) / tw;
+        // segment counts: 1, 2, ... while a segment keeps >= 2R rows
+        for (int segs = 1; segs <= std::max(1, h / std::max(16, 2 * R)); ++segs) {
+            const int TH = (h + segs - 1) / segs;
+            const long long items = (long long)strips * segs * images;
+            const long long waves = (items + slots - 1) / slots;
+            const double per_item = (double)NT * (TH + 2 * R + Gr + R / 2.0);
+            const double cost = (double)waves * per_item;
+            if (cost < best * 0.999) {
+                best = cost;
+                g.TW = tw; g.NT = NT; g.strips = strips; g.segs = segs; g.TH = TH;
+                g.items = (int)std::min<long long>(items, 1LL << 30);
             }
-            if (TW >= w) break;
+            if (items >= 64LL * slots) break;
         }
+        if (TW >= w) break;
     }
     if (best >= 1e300) return false;
     // development knobs (FGF_DEV=1): force the strip width / segment count (tests cover several
     // strips and segments on small images)
     if (const char* e = dev_env("FGF_WIDE_TW")) {
         const int tw = std::min(std::max(1, atoi(e)), w);
-        if (tw + 4 * R > g.maxc) return false;
+        if (tw + 4 * R > kWideMaxCols) return false;
         g.TW = tw;
-        g.NT = ((tw + 4 * R + g.KC - 1) / g.KC + 31) / 32 * 32;
+        g.NT = (tw + 4 * R + 31) / 32 * 32;
         g.strips = (w + tw - 1) / tw;
     }
     if (const char* e = dev_env("FGF_WIDE_SEGS")) {
@@ -86,7 +73,7 @@ bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, 
         g.segs = (h + g.TH - 1) / g.TH;
     }
     g.items = (int)std::min<long long>((long long)g.strips * g.segs * images, 1LL << 30);
-    g.grid = std::min(g.items, g.slots);
+    g.grid = std::min(g.items, slots);
     if (const char* e = dev_env("FGF_WIDE_GRID")) g.grid = std::max(1, std::min(g.grid, atoi(e)));
     g.R = R;
     g.ring_bytes = align_up((size_t)g.grid * (2 * R + 1) * 2 * CP * g.TW * sizeof(float));
@@ -95,11 +82,10 @@ bool wide_geom(WideGeom& g, int h, int w, int R, int CP, int images, bool outq, 
 
 // Ring bytes that cover every geometry wide_geom can return for radius R (any image count).
 size_t wide_ring_reserve(int R, int CP) {
-    // two CTAs per SM of strips <= 384 - 4R, or one CTA per SM of strips <= 768 - 4R (KC = 2)
-    const long long tw1 = kWideMaxCols - 4 * R, tw2 = 2 * kWideMaxCols - 4 * R;
-    if (tw1 < 32) return 0;
-    const long long cols = std::max<long long>(kWideCtasPerSM * tw1, tw2);   // >= 416 - 4R too
-    return align_up((size_t)sm_count() * cols * (2 * R + 1) * 2 * CP * sizeof(float));
+    const int twmax = kWideMaxCols - 4 * R;
+    if (twmax < 32) return 0;
+    return align_up((size_t)sm_count() * kWideCtasPerSM * (2 * R + 1) * 2 * CP * twmax *
+                    sizeof(float));
 }
 
 // Contiguous, 16-byte-aligned fp32 sample rows: TMA bulk copies can stage them.
@@ -113,13 +99,12 @@ bool wide_bulk_ok(const WideParams& wp) {
 }
 
 template <int CP, bool OUTQ, typename E, int G = wide_g<CP>(), int MINB = kWideCtasPerSM,
-          bool BULK = false, int KC = 1>
+          bool BULK = false>
 int launch_wide_t(const WideParams& wp0, const WideGeom& g, cudaStream_t st) {
-    auto kern = wide_gray_kernel<CP, G, OUTQ, E, MINB, BULK, KC>;
+    auto kern = wide_gray_kernel<CP, G, OUTQ, E, MINB, BULK>;
     WideParams wp = wp0;
     wp.TW = g.TW; wp.TH = g.TH; wp.strips = g.strips; wp.segs = g.segs; wp.items = g.items;
-    wp.L = WideCfg<CP, G, BULK ? 2 : (sizeof(E) == 4 ? 1 : 0), KC, wide_ntmax(MINB, KC)>::layout(g.TW, g.R);
-    if (g.NT > wide_ntmax(MINB, KC)) return FGF_ERR_UNSUPPORTED;   // (geometry of another variant)
+    wp.L = WideCfg<CP, G, BULK ? 2 : (sizeof(E) == 4 ? 1 : 0)>::layout(g.TW, g.R);
     if (wp.L.total > 227 * 1024) return FGF_ERR_UNSUPPORTED;
     set_smem(kern, wp.L.total);
     // persistent grid: as many CTAs as fit on the GPU at once (at most the geometry's)
@@ -149,14 +134,11 @@ int launch_wide_cp(const WideParams& wp, const WideGeom& g, int CP, int dtype, c
     // the mean-maps mode in 4-row batches, two CTAs per SM (80 registers).  FGF_WIDE_V=0 / 1
     // (development knob) forces the 4-row / 8-row variant.
     int v = OUTQ ? 1 : 0;
-    if (const char* e = dev_env("FGF_WIDE_V")) v = atoi(e) == 1 ? 1 : 0;
+    if (const char* e = dev_env("FGF_WIDE_V")) v = atoi(e);   // 0, 1; 2: 6-row batches, one CTA/SM
     const bool bulk = wide_bulk_ok(wp);
-    if (g.KC == 2) {   // two statistics columns per thread (fused filter, fp32, C_p = 1)
-        if (!OUTQ || CP != 1) return FGF_ERR_UNSUPPORTED;
-        return launch_wide_t<1, OUTQ, float, 4, 1, false, 2>(wp, g, st);
-    }
     switch (CP) {
         case 1:
+            if (v == 2) return launch_wide_t<1, OUTQ, float, 6, 1>(wp, g, st);
             if (v == 1)
                 return bulk ? launch_wide_t<1, OUTQ, float, 8, 1, true>(wp, g, st)
                             : launch_wide_t<1, OUTQ, float, 8, 1>(wp, g, st);

@@ -46,22 +46,10 @@
 
 namespace fgf {
 
-constexpr int kWideChMax = 13;          // prefix chunk per lane (KC = 1): rows of <= 416 columns
-constexpr int kWidePitch = 32 * kWideChMax;   // fp64 row pitch of the snapshot / a, b rows (KC = 1)
-constexpr int kWideMaxCols = 384;       // threads per CTA (<= 384 statistics columns per KC)
+constexpr int kWideChMax = 13;          // prefix chunk per lane: rows of <= 32 * 13 = 416 columns
+constexpr int kWidePitch = 32 * kWideChMax;   // fp64 row pitch of the snapshot / a, b rows
+constexpr int kWideMaxCols = 384;       // threads per CTA = statistics columns TW + 4R (rounded)
 constexpr int kWideCtasPerSM = 2;
-// threads per CTA of a variant (416 = one full prefix row was measured too: ptxas then caps the
-// one-CTA-per-SM variant at 128 registers and config 4 s = 1 took 13.5 vs 13.0 ms)
-__host__ __device__ constexpr int wide_ntmax(int MINB, int KC) {
-    return (void)MINB, (void)KC, kWideMaxCols;
-}
-
-// KC statistics columns per thread: rows of <= 32 CH columns, CH odd (conflict-free fp64 lanes)
-template <int KC>
-struct WidePitch {
-    static constexpr int CH = KC == 1 ? 13 : 25;
-    static constexpr int PW = 32 * CH;
-};
 
 struct WideLayout {
     int NCS, NCA;          // statistics columns TW + 4R, a, b columns TW + 2R
@@ -87,53 +75,51 @@ struct WideParams {
     WideLayout L;
 };
 
+constexpr int kWideBulkPitch = kWideMaxCols + 8;   // floats per bulk-staged row (16 B aligned)
+
 // STAGE: 0 = next batch's samples prefetched into registers (8/16-bit samples), 1 = by per-thread
 // cp.async into shared memory (fp32, strided samples), 2 = by TMA bulk copies of whole row
 // segments issued by one thread (fp32, contiguous 16-byte-aligned rows: s = 1 and K0 planes).
-template <int CP, int G, int STAGE = 1, int KC = 1, int NTM = kWideMaxCols>
+template <int CP, int G, int STAGE = 1>
 struct WideCfg {
-    static constexpr int BULKP = NTM + 8;     // floats per bulk-staged row (16 B aligned)
     static constexpr int NMAP = 2 + 2 * CP;   // I, II, p_c, Ip_c
     static constexpr int NAB = 2 * CP;        // a_c, b_c
     static constexpr int NIN = 1 + CP;        // I, p_c
-    static constexpr int PW = WidePitch<KC>::PW;
     __host__ static WideLayout layout(int TW, int R) {
         WideLayout L;
         L.NCS = TW + 4 * R;
         L.NCA = TW + 2 * R;
         auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
         size_t o = 0;
-        L.oVA = o; o = al(o + (size_t)G * NMAP * PW * 8);
-        L.oAB = o; o = al(o + (size_t)G * NAB * PW * 8);
-        L.oInvA = o; o = al(o + (size_t)PW * 8);
-        L.oInvB = o; o = al(o + (size_t)PW * 4);
-        // staging of the next batch's add / subtract sample rows (fp32 samples)
+        L.oVA = o; o = al(o + (size_t)G * NMAP * kWidePitch * 8);
+        L.oAB = o; o = al(o + (size_t)G * NAB * kWidePitch * 8);
+        L.oInvA = o; o = al(o + (size_t)kWidePitch * 8);
+        L.oInvB = o; o = al(o + (size_t)kWidePitch * 4);
+        // cp.async staging of the next batch's add / subtract sample rows (fp32 samples)
         L.oStage = o;
-        o = al(o + (STAGE == 2 ? (size_t)G * 2 * NIN * BULKP * 4
-                               : STAGE == 1 ? (size_t)G * 2 * NIN * KC * NTM * 4 : 0));
+        o = al(o + (STAGE == 2 ? (size_t)G * 2 * NIN * kWideBulkPitch * 4
+                               : STAGE == 1 ? (size_t)G * 2 * NIN * kWideMaxCols * 4 : 0));
         L.oBar = o; o = al(o + 16);
         L.total = o;
         return L;
     }
 };
 
-// In-place inclusive fp64 prefix sum of row[0, n) (n <= 32 CH) by one warp: lane l owns the
-// contiguous chunk [CH l, CH l + CH) (odd length: the 16 lanes of a half-warp hit 16 distinct
-// fp64 banks); a warp shuffle scan of the chunk totals gives the offsets.  Entries in
-// [n, 32 CH) are zeros that are read but never written.  CH <= 13: the chunk is held in
-// registers; longer chunks are read twice (sum, then running sums).
-template <int CH>
+// In-place inclusive fp64 prefix sum of row[0, n) (n <= kWidePitch) by one warp: lane l owns
+// the contiguous chunk [13 l, 13 l + 13) (odd length: the 16 lanes of a half-warp hit 16
+// distinct fp64 banks), loaded into registers at once; a warp shuffle scan of the chunk
+// totals gives the offsets.  Entries in [n, kWidePitch) are zeros that are read but never
+// written.
 __device__ __forceinline__ void warp_prefix_row(double* __restrict__ row, int n, int lane) {
-    double* r = row + lane * CH;
-    constexpr bool REG = CH <= 13;
-    double v[REG ? CH : 1];
+    double* r = row + lane * kWideChMax;
+    double v[kWideChMax];
+#pragma unroll
+    for (int i = 0; i < kWideChMax; ++i) v[i] = r[i];
     double t0 = 0.0, t1 = 0.0;                 // two chains: half the dependent latency
 #pragma unroll
-    for (int i = 0; i < CH; ++i) {
-        const double x = r[i];
-        if (REG) v[REG ? i : 0] = x;
-        if (i & 1) t1 += x;
-        else t0 += x;
+    for (int i = 0; i < kWideChMax; i += 2) {
+        t0 += v[i];
+        if (i + 1 < kWideChMax) t1 += v[i + 1];
     }
     const double tot = t0 + t1;
     double x = tot;
@@ -143,10 +129,10 @@ __device__ __forceinline__ void warp_prefix_row(double* __restrict__ row, int n,
         if (lane >= d) x += y;
     }
     double run = x - tot;
-    const int e = n - lane * CH;               // valid entries of this chunk
+    const int e = n - lane * kWideChMax;       // valid entries of this chunk
 #pragma unroll
-    for (int i = 0; i < CH; ++i) {
-        run += REG ? v[REG ? i : 0] : r[i];
+    for (int i = 0; i < kWideChMax; ++i) {
+        run += v[i];
         if (i < e) r[i] = run;
     }
 }
@@ -156,30 +142,24 @@ __device__ __forceinline__ int wide_count(int i, int n, int R) {
     return min(n - 1, i + R) - max(0, i - R) + 1;
 }
 
-// grid: persistent (<= items CTAs; MINB per SM), block NT = round32(ceil((TW + 4R) / KC)) <= 384
-// threads, each owning KC statistics columns (tid + k NT), dynamic smem L.total.
-template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM, bool BULK = false,
-          int KC = 1>
-__global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(WideParams P) {
+// grid: persistent (<= items CTAs, two per SM), block NT = round32(TW + 4R) <= 384, dynamic
+// smem L.total.
+template <int CP, int G, bool OUTQ, typename E, int MINB = kWideCtasPerSM, bool BULK = false>
+__global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParams P) {
     // fp32 samples: the next batch's rows are prefetched into shared memory (no registers held
     // while in flight) -- by TMA bulk copies of whole row segments when the rows are contiguous
     // and aligned (BULK), else by per-thread cp.async; 8/16-bit samples: into registers
     constexpr bool STAGE = sizeof(E) == 4;
     constexpr int SMODE = BULK ? 2 : (STAGE ? 1 : 0);
-    static_assert(!BULK || (sizeof(E) == 4 && KC == 1), "bulk staging moves fp32 rows, KC = 1");
-    static_assert(STAGE || KC == 1, "8/16-bit samples: one column per thread");
-    constexpr int NTM = wide_ntmax(MINB, KC);
-    using C = WideCfg<CP, G, SMODE, KC, NTM>;
-    constexpr int kWideBulkPitch = C::BULKP;
-    constexpr int NMAP = C::NMAP, NAB = C::NAB, NIN = 1 + CP, PW = C::PW;
-    constexpr int CH = WidePitch<KC>::CH;
-    constexpr int SPR = KC * NTM;                           // cp.async staging row pitch
+    static_assert(!BULK || sizeof(E) == 4, "bulk staging moves fp32 rows");
+    using C = WideCfg<CP, G, SMODE>;
+    constexpr int NMAP = C::NMAP, NAB = C::NAB, NIN = 1 + CP, PW = kWidePitch;
     extern __shared__ __align__(16) unsigned char smem[];
     double* __restrict__ VA = reinterpret_cast<double*>(smem + P.L.oVA);     // [G][NMAP][PW]
     double* __restrict__ AB = reinterpret_cast<double*>(smem + P.L.oAB);     // [G][NAB][PW]
     double* __restrict__ invA = reinterpret_cast<double*>(smem + P.L.oInvA); // [NCA], 0 outside
     float* __restrict__ invB = reinterpret_cast<float*>(smem + P.L.oInvB);   // [TW]
-    float* __restrict__ stg = reinterpret_cast<float*>(smem + P.L.oStage);   // [G][2][NIN][SPR | 392]
+    float* __restrict__ stg = reinterpret_cast<float*>(smem + P.L.oStage);   // [G][2][NIN][384 | 392]
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.L.oBar);            // BULK: rows landed
     uint32_t phase = 0;                                                      // BULK: parity
     const int NT = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -199,7 +179,7 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
     }
 
     // hb ring of this CTA: slot k, map m, output column t at ring[(k NAB + m) TW + t]
-    float* const ring0 = P.ring + (size_t)blockIdx.x * RS * NAB * TW;
+    float* const ring0 = P.ring + (size_t)blockIdx.x * RS * NAB * TW + tid;
     const int slotStride = NAB * TW;
     const int ringLen = RS * slotStride;              // ring offsets (floats) wrap at ringLen
     auto ldE = [](const E* p) { return ElemT<E>::load(p); };
@@ -228,60 +208,59 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
         for (int t = tid; t < TW; t += NT)
             invB[t] = (float)(1.0 / (double)wide_count(min(x0 + t, w - 1), w, R));
 
-        // ---- this thread's statistics columns (P0): column tid + k NT, k < KC
-        bool colS[KC], colIn[KC];
-        const E* colI[KC];
-        const E* colP[KC];
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int tc = tid + k * NT;
-            const int cs = x0 - 2 * R + tc;
-            colS[k] = tc < NCS;
-            colIn[k] = colS[k] && cs >= 0 && cs < w;
-            colI[k] = static_cast<const E*>(P.srcI) + img * P.imgI + (long long)(colIn[k] ? cs : 0) * P.col;
-            colP[k] = static_cast<const E*>(P.srcP) + img * P.imgP + (long long)(colIn[k] ? cs : 0) * P.col;
-        }
+        // ---- this thread's statistics column (P0)
+        const int cs = x0 - 2 * R + tid;
+        const bool colS = tid < NCS;
+        const bool colIn = colS && cs >= 0 && cs < w;
+        const E* const colI = static_cast<const E*>(P.srcI) + img * P.imgI + (long long)(colIn ? cs : 0) * P.col;
+        const E* const colP = static_cast<const E*>(P.srcP) + img * P.imgP + (long long)(colIn ? cs : 0) * P.col;
         const long long cstr = P.planeP;
-        double acc[KC][NMAP];
+        double acc[NMAP];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
+        for (int m = 0; m < NMAP; ++m) acc[m] = 0.0;
+        if (colIn) {
+            // warm-up: the window of a, b row yA0 - 1: sample rows [yA0 - 1 - R, yA0 - 1 + R]
+            const int wa = max(0, yA0 - 1 - R), wb = min(h, yA0 + R);
+            const E* pi = colI + wa * row;
+            const E* pp = colP + wa * row;
+            constexpr int WB = 8;
+            for (int yy = wa; yy < wb; yy += WB) {
+                float v[WB][NIN];
 #pragma unroll
-            for (int m = 0; m < NMAP; ++m) acc[k][m] = 0.0;
-            if (colIn[k]) {
-                // warm-up: the window of a, b row yA0 - 1: sample rows [yA0 - 1 - R, yA0 - 1 + R]
-                const int wa = max(0, yA0 - 1 - R), wb = min(h, yA0 + R);
-                const E* pi = colI[k] + wa * row;
-                const E* pp = colP[k] + wa * row;
-                constexpr int WB = 8;
-                for (int yy = wa; yy < wb; yy += WB) {
-                    float v[WB][NIN];
+                for (int k = 0; k < WB; ++k) {
+                    if (yy + k < wb) {
+                        v[k][0] = ldE(pi + k * row);
 #pragma unroll
-                    for (int q = 0; q < WB; ++q) {
-                        if (yy + q < wb) {
-                            v[q][0] = ldE(pi + q * row);
-#pragma unroll
-                            for (int c = 0; c < CP; ++c) v[q][1 + c] = ldE(pp + c * cstr + q * row);
-                        }
+                        for (int c = 0; c < CP; ++c) v[k][1 + c] = ldE(pp + c * cstr + k * row);
                     }
-#pragma unroll
-                    for (int q = 0; q < WB; ++q) {
-                        if (yy + q < wb) {
-                            const double I = (double)v[q][0];
-                            acc[k][0] += I;
-                            acc[k][1] = fma(I, I, acc[k][1]);
-#pragma unroll
-                            for (int c = 0; c < CP; ++c) {
-                                const double pv = (double)v[q][1 + c];
-                                acc[k][2 + c] += pv;
-                                acc[k][2 + CP + c] = fma(I, pv, acc[k][2 + CP + c]);
-                            }
-                        }
-                    }
-                    pi += WB * row;
-                    pp += WB * row;
                 }
+#pragma unroll
+                for (int k = 0; k < WB; ++k) {
+                    if (yy + k < wb) {
+                        const double I = (double)v[k][0];
+                        acc[0] += I;
+                        acc[1] = fma(I, I, acc[1]);
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) {
+                            const double pv = (double)v[k][1 + c];
+                            acc[2 + c] += pv;
+                            acc[2 + CP + c] = fma(I, pv, acc[2 + CP + c]);
+                        }
+                    }
+                }
+                pi += WB * row;
+                pp += WB * row;
             }
         }
+        // add / subtract sample rows of a batch, prefetched one batch ahead; rows that must
+        // not contribute are zeros (which add exactly nothing)
+        float va[STAGE ? 1 : G][NIN], vs[STAGE ? 1 : G][NIN];
+        float* const stg_t = stg + tid;                   // [(g 2 + a) NIN + k] * 384
+        auto stage4 = [&](int slot, const E* src, bool ok) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(stg_t + slot * kWideMaxCols);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                         ::"r"(d), "l"(ok ? src : colI), "r"(ok ? 4 : 0) : "memory");
+        };
         // BULK: one thread copies the batch's add / subtract sample-row segments (all planes)
         // [ca, cb) of each row into the staging rows, completion on the mbarrier (tx bytes)
         const int cs0a = (x0 - 2 * R) & ~3;                 // 16-byte-aligned segment origin
@@ -324,65 +303,51 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
                 }
             }
         };
-        // add / subtract sample rows of a batch, prefetched one batch ahead; rows that must
-        // not contribute are zeros (which add exactly nothing)
-        float va[STAGE ? 1 : G][NIN], vs[STAGE ? 1 : G][NIN];
-        auto stage4 = [&](int slot, int k, const E* src, bool ok) {
-            const uint32_t d = (uint32_t)__cvta_generic_to_shared(stg + slot * SPR + tid + k * NT);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
-                         ::"r"(d), "l"(ok ? src : colI[k]), "r"(ok ? 4 : 0) : "memory");
-        };
         auto load_batch = [&](int ya) {
+            const E* ai = colI + (ya + R) * row;
+            const E* ap = colP + (ya + R) * row;
+            const E* si = colI + (ya - R - 1) * row;
+            const E* sp = colP + (ya - R - 1) * row;
+            const bool full = colIn && ya + G <= yA1 && ya - R - 1 >= 0 && ya + G - 1 + R < h;
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const E* ai = colI[k] + (ya + R) * row;
-                const E* ap = colP[k] + (ya + R) * row;
-                const E* si = colI[k] + (ya - R - 1) * row;
-                const E* sp = colP[k] + (ya - R - 1) * row;
-                const bool full = colIn[k] && ya + G <= yA1 && ya - R - 1 >= 0 && ya + G - 1 + R < h;
+            for (int g = 0; g < G; ++g) {
+                const int y = ya + g;
+                const bool oka = full || (colIn && y < yA1 && y + R < h);
+                const bool oks = full || (colIn && y < yA1 && y - R - 1 >= 0);
+                if constexpr (STAGE) {
+                    stage4((g * 2 + 0) * NIN, ai, oka);
+                    stage4((g * 2 + 1) * NIN, si, oks);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int y = ya + g;
-                    const bool oka = full || (colIn[k] && y < yA1 && y + R < h);
-                    const bool oks = full || (colIn[k] && y < yA1 && y - R - 1 >= 0);
-                    if constexpr (STAGE) {
-                        stage4((g * 2 + 0) * NIN, k, ai, oka);
-                        stage4((g * 2 + 1) * NIN, k, si, oks);
+                    for (int c = 0; c < CP; ++c) {
+                        stage4((g * 2 + 0) * NIN + 1 + c, ap + c * cstr, oka);
+                        stage4((g * 2 + 1) * NIN + 1 + c, sp + c * cstr, oks);
+                    }
+                    ai += row; ap += row; si += row; sp += row;
+                } else {
+                    va[STAGE ? 0 : g][0] = oka ? ldE(ai + g * row) : 0.0f;
+                    vs[STAGE ? 0 : g][0] = oks ? ldE(si + g * row) : 0.0f;
 #pragma unroll
-                        for (int c = 0; c < CP; ++c) {
-                            stage4((g * 2 + 0) * NIN + 1 + c, k, ap + c * cstr, oka);
-                            stage4((g * 2 + 1) * NIN + 1 + c, k, sp + c * cstr, oks);
-                        }
-                        ai += row; ap += row; si += row; sp += row;
-                    } else {
-                        va[STAGE ? 0 : g][0] = oka ? ldE(ai + g * row) : 0.0f;
-                        vs[STAGE ? 0 : g][0] = oks ? ldE(si + g * row) : 0.0f;
-#pragma unroll
-                        for (int c = 0; c < CP; ++c) {
-                            va[STAGE ? 0 : g][1 + c] = oka ? ldE(ap + c * cstr + g * row) : 0.0f;
-                            vs[STAGE ? 0 : g][1 + c] = oks ? ldE(sp + c * cstr + g * row) : 0.0f;
-                        }
+                    for (int c = 0; c < CP; ++c) {
+                        va[STAGE ? 0 : g][1 + c] = oka ? ldE(ap + c * cstr + g * row) : 0.0f;
+                        vs[STAGE ? 0 : g][1 + c] = oks ? ldE(sp + c * cstr + g * row) : 0.0f;
                     }
                 }
             }
             if constexpr (STAGE) asm volatile("cp.async.commit_group;" ::: "memory");
         };
 
-        // ---- this thread's output columns (P4): tid + k NT, k < KC
-        bool colO[KC];
-        const E* Iq[KC];
+        // ---- this thread's output column (P4)
+        const int xo = x0 + tid;
+        const bool colO = tid < TW && xo < w;
+        const E* const Iq = static_cast<const E*>(P.srcI) + img * P.imgI + xo;   // OUTQ: s = 1
+        double accB[NAB];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-            const int tc = tid + k * NT;
-            colO[k] = tc < TW && x0 + tc < w;
-            Iq[k] = static_cast<const E*>(P.srcI) + img * P.imgI + x0 + tc;   // OUTQ: s = 1
-        }
-        double accB[KC][NAB];
-#pragma unroll
-        for (int k = 0; k < KC; ++k)
-#pragma unroll
-            for (int m = 0; m < NAB; ++m) accB[k][m] = 0.0;
+        for (int m = 0; m < NAB; ++m) accB[m] = 0.0;
         int rslot = 0;                                     // ring offset of step ya
+        double* const va_t = VA + tid;                     // P0 snapshots of this column
+        const double* const pa_t = VA + tid;               // P2: window ends tid - 1, tid + 2R
+        double* const ab_t = AB + tid;                     // P2: a, b of column tid
+        const double* const pb_t = AB + tid;               // P4: window ends tid - 1, tid + 2R
         const int R2 = 2 * R;
 
         if (BULK) {
@@ -403,42 +368,38 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
             } else if constexpr (STAGE) {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                if (!colS[k]) continue;
-                const int tc = tid + k * NT;
+            if (colS) {
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     if (g < nA) {
                         float xa[NIN], xs[NIN];
                         if (BULK) {
                             const int y = ya + g;
-                            const bool oka = colIn[k] && y + R < h, oks = colIn[k] && y - R - 1 >= 0;
-                            const float* bs = stg + boff + tc;
+                            const bool oka = colIn && y + R < h, oks = colIn && y - R - 1 >= 0;
+                            const float* bs = stg + boff + tid;
 #pragma unroll
-                            for (int q = 0; q < NIN; ++q) {
-                                xa[q] = oka ? bs[((g * 2 + 0) * NIN + q) * kWideBulkPitch] : 0.0f;
-                                xs[q] = oks ? bs[((g * 2 + 1) * NIN + q) * kWideBulkPitch] : 0.0f;
+                            for (int k = 0; k < NIN; ++k) {
+                                xa[k] = oka ? bs[((g * 2 + 0) * NIN + k) * kWideBulkPitch] : 0.0f;
+                                xs[k] = oks ? bs[((g * 2 + 1) * NIN + k) * kWideBulkPitch] : 0.0f;
                             }
                         } else {
 #pragma unroll
-                            for (int q = 0; q < NIN; ++q) {
-                                xa[q] = STAGE ? stg[((g * 2 + 0) * NIN + q) * SPR + tc] : va[STAGE ? 0 : g][q];
-                                xs[q] = STAGE ? stg[((g * 2 + 1) * NIN + q) * SPR + tc] : vs[STAGE ? 0 : g][q];
+                            for (int k = 0; k < NIN; ++k) {
+                                xa[k] = STAGE ? stg_t[((g * 2 + 0) * NIN + k) * kWideMaxCols] : va[STAGE ? 0 : g][k];
+                                xs[k] = STAGE ? stg_t[((g * 2 + 1) * NIN + k) * kWideMaxCols] : vs[STAGE ? 0 : g][k];
                             }
                         }
                         const double Ia = (double)xa[0], Is = (double)xs[0];
-                        acc[k][0] += Ia - Is;
-                        acc[k][1] += fma(Ia, Ia, -(Is * Is));
+                        acc[0] += Ia - Is;
+                        acc[1] += fma(Ia, Ia, -(Is * Is));
 #pragma unroll
                         for (int c = 0; c < CP; ++c) {
                             const double pa = (double)xa[1 + c], ps = (double)xs[1 + c];
-                            acc[k][2 + c] += pa - ps;
-                            acc[k][2 + CP + c] += fma(Ia, pa, -(Is * ps));
+                            acc[2 + c] += pa - ps;
+                            acc[2 + CP + c] += fma(Ia, pa, -(Is * ps));
                         }
-                        double* v = VA + tc;
 #pragma unroll
-                        for (int m = 0; m < NMAP; ++m) v[(g * NMAP + m) * PW] = acc[k][m];
+                        for (int m = 0; m < NMAP; ++m) va_t[(g * NMAP + m) * PW] = acc[m];
                     }
                 }
             }
@@ -446,26 +407,23 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
             if (BULK) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // reads before the next copies
             // ring rows leaving the vertical windows of this batch's steps, and (s = 1) the
             // guidance row of each output: issued now, used in P4
+            float old[G][NAB];
+            float Io[OUTQ ? G : 1];
             // interior batches (warp-uniform): every step removes a ring row and emits an output
             const bool fastS = nS == G && ya - RS >= yA0;
             const bool fastO = nS == G && ya - R >= y0 && ya + G - 1 - R < y1;
-            float old[G][KC][NAB];
-            float Io[OUTQ ? G : 1][KC];
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                if (!colO[k]) continue;
-                const int tc = tid + k * NT;
+            if (colO) {
                 int ro = rslot;
-                const E* ip = Iq[k] + (ya - R) * row;
+                const E* ip = Iq + (ya - R) * row;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const int yy = ya + g;
                     const bool sub = fastS || (g < nS && yy - RS >= yA0);   // row yy - 2R - 1 was added
 #pragma unroll
-                    for (int m = 0; m < NAB; ++m) old[g][k][m] = sub ? ring0[ro + m * TW + tc] : 0.0f;
+                    for (int m = 0; m < NAB; ++m) old[g][m] = sub ? ring0[ro + m * TW] : 0.0f;
                     if (OUTQ) {
                         const int yb = yy - R;
-                        Io[OUTQ ? g : 0][k] = (fastO || (g < nS && yb >= y0 && yb < y1)) ? ldE(ip) : 0.0f;
+                        Io[OUTQ ? g : 0] = (fastO || (g < nS && yb >= y0 && yb < y1)) ? ldE(ip) : 0.0f;
                         ip += row;
                     }
                     ro += slotStride;
@@ -475,17 +433,12 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
             __syncthreads();
             if (BULK && tid == 0 && ya + G < yA1) bulk_batch(ya + G);   // in flight under P1-P4
             // ---- P1: prefix sums of the snapshotted rows
-            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row<CH>(VA + rs * PW, NCS, lane);
+            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row(VA + rs * PW, NCS, lane);
             __syncthreads();
             // ---- P2: window sums, coefficient epilogue -> a, b (fp64 rows for P3)
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int tc = tid + k * NT;
-                if (tc >= NCA) continue;
-                const double ix = invA[tc];
-                const bool first = tc == 0;
-                const double* pr = VA + tc;
-                double* ab = AB + tc;
+            if (tid < NCA) {
+                const double ix = invA[tid];
+                const bool first = tid == 0;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     if (g < nA) {
@@ -496,7 +449,7 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
                         double S[NMAP];
 #pragma unroll
                         for (int m = 0; m < NMAP; ++m) {
-                            const double* q = pr + (g * NMAP + m) * PW;
+                            const double* q = pa_t + (g * NMAP + m) * PW;
                             S[m] = q[R2] - (first ? 0.0 : q[-1]);
                         }
                         const double mI = S[0] * inv;
@@ -510,29 +463,24 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
                             const double mp = S[2 + c] * inv;
                             const double cov = fma(-mI, mp, S[2 + CP + c] * inv);   // cov_Ip
                             const float a = (float)cov * rden;                    // Eq.2
-                            ab[(g * NAB + 2 * c) * PW] = (double)a;
-                            ab[(g * NAB + 2 * c + 1) * PW] = (double)fmaf(-a, mIf, (float)mp);   // Eq.3
+                            ab_t[(g * NAB + 2 * c) * PW] = (double)a;
+                            ab_t[(g * NAB + 2 * c + 1) * PW] = (double)fmaf(-a, mIf, (float)mp);   // Eq.3
                         }
                     }
                 }
             }
             __syncthreads();
             // ---- P3: prefix sums of the a, b rows
-            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row<CH>(AB + rs * PW, NCA, lane);
+            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row(AB + rs * PW, NCA, lane);
             __syncthreads();
             // ---- P4: horizontal box of a, b, vertical running window through the ring, output
-            const bool fastA = nA == G;
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                if (!colO[k]) continue;
-                const int tc = tid + k * NT;
-                const float ixB = invB[tc];
+            if (colO) {
+                const float ixB = invB[tid];
                 const float ixR = ixB * (float)invRow;
-                const bool first = tc == 0;
-                const double* pb = AB + tc;
+                const bool first = tid == 0;
+                const bool fastA = nA == G;
                 int ro = rslot;
-                E* qrow = OUTQ ? static_cast<E*>(P.q) + (long long)img * CP * h * w +
-                                     (long long)(ya - R) * w + x0 + tc
+                E* qrow = OUTQ ? static_cast<E*>(P.q) + (long long)img * CP * h * w + (long long)(ya - R) * w + xo
                                : nullptr;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -540,26 +488,26 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
                         if (fastA || g < nA) {
 #pragma unroll
                             for (int m = 0; m < NAB; ++m) {
-                                const double* q = pb + (g * NAB + m) * PW;
+                                const double* q = pb_t + (g * NAB + m) * PW;
                                 const float hb = (float)(q[R2] - (first ? 0.0 : q[-1]));
-                                ring0[ro + m * TW + tc] = hb;
-                                accB[k][m] += (double)hb;
+                                ring0[ro + m * TW] = hb;
+                                accB[m] += (double)hb;
                             }
                         }
 #pragma unroll
-                        for (int m = 0; m < NAB; ++m) accB[k][m] -= (double)old[g][k][m];
+                        for (int m = 0; m < NAB; ++m) accB[m] -= (double)old[g][m];
                         const int yb = ya + g - R;
                         if (fastO || (yb >= y0 && yb < y1)) {
                             const float inv = (yb - R >= 0 && yb + R < h)
                                                   ? ixR : ixB / (float)wide_count(yb, h, R);
                             if (OUTQ) {
-                                const float I = Io[OUTQ ? g : 0][k];
+                                const float I = Io[OUTQ ? g : 0];
                                 E* qo = qrow + (long long)g * w;
 #pragma unroll
                                 for (int c = 0; c < CP; ++c) {
-                                    const float ma = fmaf(P.k1, (float)accB[k][2 * c] * inv,
+                                    const float ma = fmaf(P.k1, (float)accB[2 * c] * inv,
                                                           c == 0 ? P.k0 : 0.0f);
-                                    const float mb = P.k1 * ((float)accB[k][2 * c + 1] * inv);
+                                    const float mb = P.k1 * ((float)accB[2 * c + 1] * inv);
                                     const float qv = fmaf(ma, I, mb);           // Eq.4
                                     const unsigned bits = ElemT<E>::bits(qv);
                                     E* qc = qo + (long long)c * h * w;
@@ -568,10 +516,10 @@ __global__ void __launch_bounds__(wide_ntmax(MINB, KC), MINB) wide_gray_kernel(W
                                     else *reinterpret_cast<unsigned char*>(qc) = (unsigned char)bits;
                                 }
                             } else {
-                                float* d = P.dst + ((size_t)img * NAB * h + yb) * w + x0 + tc;
+                                float* d = P.dst + ((size_t)img * NAB * h + yb) * w + xo;
 #pragma unroll
                                 for (int m = 0; m < NAB; ++m)
-                                    d[(size_t)m * h * w] = fmaf(P.k1, (float)accB[k][m] * inv, m == 0 ? P.k0 : 0.0f);
+                                    d[(size_t)m * h * w] = fmaf(P.k1, (float)accB[m] * inv, m == 0 ? P.k0 : 0.0f);
                             }
                         }
                     }

@@ -93,7 +93,7 @@ def test_exact_guided_filter_one_kernel(B, H, W, r, eps):
     assert float((qb - q).abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("V", ["0", "1", "kc2"])
+@pytest.mark.parametrize("V", ["0", "1", "2"])
 @pytest.mark.parametrize("TW,SEGS,GRID", [(32, 7, None), (96, 3, 2), (200, 1, 1), (64, 40, 5),
                                           (301, 2, 3)])
 def test_exact_guided_filter_geometries(TW, SEGS, GRID, V):
@@ -105,8 +105,7 @@ def test_exact_guided_filter_geometries(TW, SEGS, GRID, V):
     I, p = synth.make_batch(1, "cuda", batch=2, H=203, W=301)
     r, eps = 9, 0.01
     q0 = fgf.filter(I, p, r, eps, 1, 0)
-    kc = {"FGF_WIDE_KC": 2} if V == "kc2" else {"FGF_WIDE_V": V}   # kc2: 2 columns per thread
-    with env(FGF_WIDE_TW=TW, FGF_WIDE_SEGS=SEGS, FGF_WIDE_GRID=GRID, **kc):
+    with env(FGF_WIDE_TW=TW, FGF_WIDE_SEGS=SEGS, FGF_WIDE_GRID=GRID, FGF_WIDE_V=V):
         q1 = fgf.filter(I, p, r, eps, 1, 0)
     torch.cuda.synchronize()
     assert float((q0 - q1).abs().max()) <= 2e-6

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/r2
+O=gpurun_out/r2/bench30.jsonl; rm -f $O
+B="--steps 10 --warmup 3 --no-e2e --no-cpu-baseline"
+for v in 0 1 2 3 0; do echo "v $v" >> gpurun_out/r2/bench30.err
+  FGF_DEV=1 FGF_WIDE_V=$v timeout 300 python bench.py --config 4 --s 2 --batch 64 $B >> $O 2>> gpurun_out/r2/bench30.err
+done
