@@ -253,7 +253,14 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     if (P.nt == 0) return FGF_ERR_UNSUPPORTED;
 
     StripParams sp{};
-    if (P.s > 1 || P.dtype != FGF_F32) {
+    // (development knob FGF_STRIP_INPLACE: nearest fp32 samples read in place by K1, no K0)
+    const bool inplace = P.s > 1 && P.sub == FGF_SUB_NEAREST && P.dtype == FGF_F32 &&
+                         dev_env("FGF_STRIP_INPLACE") != nullptr;
+    if (inplace) {
+        sp.srcI = static_cast<const float*>(Ib); sp.imgI = (long long)P.CI * P.N; sp.planeI = (int)P.N;
+        sp.srcP = static_cast<const float*>(pb); sp.imgP = (long long)P.CP * P.N; sp.planeP = (int)P.N;
+        sp.row = P.s * P.W; sp.col = P.s;
+    } else if (P.s > 1 || P.dtype != FGF_F32) {
         // Step 1 as its own pass (R3 nearest / R4 block mean) into compact fp32 low-res planes
         // (s = 1 with reduced-precision inputs: the conversion to fp32).
         float* Is = planes;
