@@ -522,15 +522,38 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
     # the whole batch when host RAM allows (pinned I, p and q take per_img per image; keep
     # half of the available memory free), else the largest batch that fits
     Be = int(max(1, min(B, (avail // max(1, world)) // 2 // per_img)))
-    Id, pd = synth.make_batch(args.config, torch.device("cuda", local), batch=Be, first=rank * B)
+    dev = torch.device("cuda", local)
+
+    def agree(x, op):   # one value for every rank (the host batch must match across ranks)
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=op)
+        return int(t.item())
+
+    Be = agree(Be, dist.ReduceOp.MIN if world > 1 else None)
+
     def pinned(t):   # one pinned host copy (no pageable intermediate)
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         return h
-    Ih = pinned(Id)
-    ph = Ih if args.config == 0 else pinned(pd)
-    del Id, pd
-    qh = torch.empty((Be, CP, H, W), dtype=torch.float32).pin_memory()
+    while True:   # pinning can fail below the free-memory estimate: halve the batch and retry
+        ok = 1
+        try:
+            Id, pd = synth.make_batch(args.config, dev, batch=Be, first=rank * B)
+            Ih = pinned(Id)
+            ph = Ih if args.config == 0 else pinned(pd)
+            del Id, pd
+            qh = torch.empty((Be, CP, H, W), dtype=torch.float32, pin_memory=True)
+        except (RuntimeError, MemoryError):
+            ok = 0
+            Ih = ph = qh = Id = pd = None
+            torch.cuda.empty_cache()
+        if agree(ok, dist.ReduceOp.MIN if world > 1 else None) == 1:
+            break
+        if Be == 1:
+            raise RuntimeError("e2e: no pinned host batch could be allocated")
+        Be = max(1, Be // 2)
 
     def step():
         fgf.fgf_filter_host(Ih, ph, qh, Be, H, W, CI, CP, prm["r"], prm["eps"], prm["s"],
