@@ -169,19 +169,22 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
 /* Row-band geometry of rank `rank` of `nranks` for one H x W image (the same
  * rule fgf_filter_band and fgf_filter_bands_loopback use): rank k owns low-res rows
  * [k h / n, (k + 1) h / n) of h = ceil(H/s) (R6) and so full-resolution rows on multiples of s.
- * Host only (no GPU, no launch).  out[10] = {h, w, r', halo = 2r' + 1, own low-res rows y0, y1,
- * own full-res rows Y0, Y1, extended low-res rows e0, e1 of the single exchange}.
- * FGF_ERR_PARAM when a band of several holds fewer than 2r' + 1 low-res rows. */
+ * Host only (no GPU, no launch).  out[10] = {h, w, r', halo = 2r' + 1 + x, own low-res rows y0,
+ * y1, own full-res rows Y0, Y1, extended low-res rows e0, e1 of the single exchange}; x = 1 when
+ * h s != H (the map scale h / H then exceeds 1 / s and a band's last rows upsample from up to
+ * low-res row y1 + 1), else 0.  FGF_ERR_PARAM when a band of several holds fewer than halo
+ * low-res rows. */
 int fgf_band_geometry(int H, int W, int r, int s, int nranks, int rank, int* out);
 
 /* ---------------------------------------------------------------------------------------
  * One image split into row bands across ranks (BASELINE.json config 4b).
  * Rank `rank` of `nranks` owns full-resolution rows [row0, row0 + rows) of an image of
  * H_total x W (row0 a multiple of s; rows a multiple of s unless the band ends at H_total);
- * with more than one rank every band must span at least 2r'+1 low-res rows.  I_band: DEVICE
+ * with more than one rank every band must span at least halo = 2r'+1+x low-res rows
+ * (fgf_band_geometry).  I_band: DEVICE
  * [C_I][rows][W], p_band: [C_p][rows][W] (may equal I_band when C_I = C_p = 1), q_band:
  * [C_p][rows][W], all holding exactly the band's rows.  The call subsamples its rows, sends
- * 2r'+1 low-res rows of I', p' to rank-1 / rank+1 and receives theirs (ncclSend / ncclRecv in
+ * halo low-res rows of I', p' to rank-1 / rank+1 and receives theirs (ncclSend / ncclRecv in
  * one group on nccl_comm, enqueued on cuda_stream; one exchange, the single-step variant of
  * DESIGN.md §7), runs the low-res chain on the extended band with global window clipping
  * (R1) and writes q for its own rows with the global upsampling map (R5): the result equals
@@ -194,9 +197,10 @@ size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I,
                                 int s, int nranks);
 /* Halo exchange modes of the band path. */
 enum {
-    FGF_BAND_SINGLE = 0,   /* one exchange: 2r'+1 rows of I', p' (the default of fgf_filter_band) */
-    FGF_BAND_TWO_STEP = 1  /* r' rows of I', p', then ceil(r/s)+1 = r'+1 rows of a, b (BASELINE.json's
-                              halo); the statistics of the halo rows are not recomputed */
+    FGF_BAND_SINGLE = 0,   /* one exchange: 2r'+1+x rows of I', p' (the default of fgf_filter_band) */
+    FGF_BAND_TWO_STEP = 1  /* r' rows of I', p', then ceil(r/s)+1 = r'+1 (+x) rows of a, b
+                              (BASELINE.json's halo); the statistics of the halo rows are not
+                              recomputed */
 };
 /* fgf_filter_band with an explicit exchange mode (FGF_ERR_PARAM for an unknown mode).  Every
  * rank must use the same mode; the workspace query covers both. */

@@ -705,7 +705,9 @@ int fgf_band_geometry(int H, int W, int r, int s, int nranks, int rank, int* out
     if (H < 1 || W < 1) return FGF_ERR_SHAPE;
     if (r < 1 || s < 1 || nranks < 1 || rank < 0 || rank >= nranks) return FGF_ERR_PARAM;
     const int h = lowres_dim(H, s), w = lowres_dim(W, s), R = radius_lowres(r, s);
-    const int halo = 2 * R + 1;
+    // 2r'+1 rows, plus one when h s != H (the map scale h / H > 1 / s: a band's last rows
+    // upsample from up to low-res row y1 + 1; fgf_band.cuh)
+    const int halo = 2 * R + 1 + ((long long)h * s != H ? 1 : 0);
     // every band must hold a whole single-exchange halo, unless it is alone
     for (int k = 0; k < nranks && nranks > 1; ++k)
         if ((int)((long long)(k + 1) * h / nranks) - (int)((long long)k * h / nranks) < halo)
@@ -720,14 +722,17 @@ int fgf_band_geometry(int H, int W, int r, int s, int nranks, int rank, int* out
 size_t fgf_band_workspace_bytes(int H_total, int W, int row0, int rows, int C_I, int C_p, int r,
                                 int s, int nranks) {
     // The larger of the exchange modes this band admits (two-step accepts narrower bands:
-    // r'+1 low-res rows instead of 2r'+1); 0 only when neither mode accepts the band.
+    // r'+1 low-res rows instead of 2r'+1) and of the two subsampling modes (the band's own
+    // chain may need the I', p' planes under the block mean); 0 only when no mode accepts the
+    // band.
     size_t best = 0;
-    for (int mode : {FGF_BAND_SINGLE, FGF_BAND_TWO_STEP}) {
-        BandPlan B;
-        if (band_plan(B, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, FGF_SUB_NEAREST, nranks,
-                      false, mode) == FGF_OK)
-            best = std::max(best, B.ws_total);
-    }
+    for (int mode : {FGF_BAND_SINGLE, FGF_BAND_TWO_STEP})
+        for (int sub : {FGF_SUB_NEAREST, FGF_SUB_BILINEAR}) {
+            BandPlan B;
+            if (band_plan(B, H_total, W, row0, rows, C_I, C_p, r, 1.0, s, sub, nranks, false,
+                          mode) == FGF_OK)
+                best = std::max(best, B.ws_total);
+        }
     return best;
 }
 

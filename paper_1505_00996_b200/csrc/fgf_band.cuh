@@ -3,10 +3,12 @@
 //
 // Rank k owns full-resolution rows [row0, row0 + rows) (row0 a multiple of s; the last band
 // ends at H), i.e. low-res rows [y0, y1) = [row0/s, ceil((row0+rows)/s)) of the h = ceil(H/s)
-// low-res rows.  Its rows upsample from low-res rows y0-1 .. y1 (R5); their mean_a, mean_b
-// need a, b r' rows further and those need I', p' r' rows further again, so ONE exchange of
-// HALO = 2r'+1 low-res rows of I' and p' with each neighbour makes everything after it local
-// (the single-step variant of SURVEY §8(e)).  Windows clip at the global bounds because the
+// low-res rows.  Its rows upsample from low-res rows y0-1 .. y1 (R5) -- or y1 + 1 when H is not
+// a multiple of s: the map scale h / H then exceeds 1 / s, and the last rows of a band reach
+// up to one row further (below y1 + 1/2, so the row after y1 is the last one: x = 1 extra row,
+// 0 when h s = H); their mean_a, mean_b need a, b r' rows further and those need I', p' r' rows
+// further again, so ONE exchange of HALO = 2r'+1+x low-res rows of I' and p' with each
+// neighbour makes everything after it local (the single-step variant of SURVEY §8(e)).  Windows clip at the global bounds because the
 // extended band [e0, e1) = [y0 - HALO, y1 + HALO) is clipped to [0, h): at interior band
 // edges the clipped windows only reach a, b rows this rank never uses.
 //
@@ -16,8 +18,8 @@
 //
 // Two-step mode (FGF_BAND_TWO_STEP, SURVEY §8(e)'s first form, BASELINE.json's "halo of
 // ceil(r/s)+1 low-res rows"): exchange A sends r' rows of I', p'; the statistics and a, b of
-// the OWN rows follow; exchange B sends r'+1 rows of a, b; the box of a, b then covers the
-// own rows +-1 and K4 runs as above.  Two NCCL latencies instead of one, fewer bytes for
+// the OWN rows follow; exchange B sends r'+1+x rows of a, b; the box of a, b then covers the
+// own rows -1 .. +1+x and K4 runs as above.  Two NCCL latencies instead of one, fewer bytes for
 // colour guidance.
 //
 // The NCCL library is loaded at run time (dlopen "libnccl.so.2": the one torch already
@@ -71,10 +73,11 @@ const Nccl* nccl() {
 struct BandPlan {
     int mode;                // FGF_BAND_SINGLE / FGF_BAND_TWO_STEP
     int H, W, h, w, s, sub, R, halo;
+    int x;                   // 1 when h s != H: the own rows upsample from up to row y1 + 1
     int row0, rows;          // own full-res rows
     int y0, y1;              // own low-res rows
     int e0, e1;              // extended low-res rows of I', p' after (the first) exchange
-    int f0, f1;              // two-step: rows of a, b after exchange B ([y0-r'-1, y1+r'+1))
+    int f0, f1;              // two-step: rows of a, b after exchange B ([y0-r'-1-x, y1+r'+1+x))
     int CI, CP, NPL;         // planes exchanged: C_I (+ C_p unless self-guided)
     int r_full;              // r (full resolution)
     size_t ext_plane;        // floats per extended plane: (e1 - e0) * w
@@ -86,7 +89,7 @@ struct BandPlan {
     // overlapped single exchange (band_plan_overlap): the interior is the band's own image
     bool ovl = false;
     Plan pb;                 // the band's rows as an image (full resolution, s, r)
-    int m0, m1;              // rows of the assembled mean maps: [y0 - 1, y1 + 1) clipped
+    int m0, m1;              // rows of the assembled mean maps: [y0 - 1, y1 + 1 + x) clipped
     int t0, t1, b0, b1;      // top / bottom edge strips of low-res rows (halo + 4r' own rows)
     Plan pe_t, pe_b;         // s = 1 plans of the edge strips (radius r')
     size_t o_slot, o_int, o_et, o_etw, o_etm, o_eb, o_ebw, o_ebm, o_fin;
@@ -112,19 +115,21 @@ int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int
     B.h = lowres_dim(H, s);
     B.w = lowres_dim(W, s);
     B.R = radius_lowres(r, s);
-    // single: 2r'+1 rows of I', p'; two-step: r' rows of I', p' (exchange A), then r'+1 rows
-    // of a, b (exchange B)
-    B.halo = mode == FGF_BAND_SINGLE ? 2 * B.R + 1 : B.R;
+    // single: 2r'+1+x rows of I', p'; two-step: r' rows of I', p' (exchange A), then r'+1+x
+    // rows of a, b (exchange B).  Both directions exchange the same depth (one extra row above
+    // when x = 1, unused), so every halo message has one size on both sides.
+    B.x = (long long)B.h * s != H ? 1 : 0;
+    B.halo = mode == FGF_BAND_SINGLE ? 2 * B.R + 1 + B.x : B.R;
     B.row0 = row0; B.rows = rows;
     B.y0 = row0 / s;
     B.y1 = lowres_dim(row0 + rows, s);
     // every band (so every neighbour) must hold a whole halo, unless it is alone
-    const int need = mode == FGF_BAND_SINGLE ? B.halo : B.R + 1;
+    const int need = mode == FGF_BAND_SINGLE ? B.halo : B.R + 1 + B.x;
     if (nranks > 1 && B.y1 - B.y0 < need) return FGF_ERR_PARAM;
     B.e0 = std::max(0, B.y0 - B.halo);
     B.e1 = std::min(B.h, B.y1 + B.halo);
-    B.f0 = std::max(0, B.y0 - B.R - 1);
-    B.f1 = std::min(B.h, B.y1 + B.R + 1);
+    B.f0 = std::max(0, B.y0 - B.R - 1 - B.x);
+    B.f1 = std::min(B.h, B.y1 + B.R + 1 + B.x);
     B.NPL = self_guided ? CI : CI + CP;
     B.ext_plane = (size_t)(B.e1 - B.e0) * B.w;
     B.ab_plane = (size_t)(B.f1 - B.f0) * B.w;
@@ -164,10 +169,10 @@ int band_plan(BandPlan& B, int H, int W, int row0, int rows, int CI, int CP, int
 //     read in place, any engine) -> interior maps, exact on rows [y0 + 2r', y1 - 2r') (and on
 //     every row at a global image border); meanwhile on the library's comm stream:
 //   comm stream: K0 compacts the 4r' own rows next to each inner band edge into an edge strip,
-//     whose first / last 2r' + 1 rows are the halo the neighbour needs; NCCL send / recv of
-//     those rows straight into the neighbours' edge strips; the low-res chain of each edge
-//     strip gives the maps of rows [y0 - 1, y0 + 2r') and [y1 - 2r', y1 + 1);
-//   caller's stream (after both): the maps are assembled on rows [y0 - 1, y1 + 1) and K4
+//     whose first / last 2r' + 1 + x rows are the halo the neighbour needs; NCCL send / recv
+//     of those rows straight into the neighbours' edge strips; the low-res chain of each edge
+//     strip gives the maps of rows [y0 - 1, y0 + 2r') and [y1 - 2r', y1 + 1 + x);
+//   caller's stream (after both): the maps are assembled on rows [y0 - 1, y1 + 1 + x) and K4
 //   writes the own rows.  The exchange runs under the interior chain; with one rank the path
 //   is exactly the whole-image filter.
 int band_plan_overlap(BandPlan& B, bool self_guided, double eps) {
@@ -178,12 +183,13 @@ int band_plan_overlap(BandPlan& B, bool self_guided, double eps) {
     int rc = make_plan(B.pb, 1, B.rows, B.W, B.CI, B.CP, B.r_full, eps, B.s, B.sub);
     if (rc) return rc;
     if (B.pb.h != hb || B.pb.w != B.w || B.pb.R != R) return FGF_ERR_UNSUPPORTED;
+    // (halo = 2r'+1+x <= 4r' rows: the rows sent lie inside the edge strips' own rows)
     B.m0 = up ? B.y0 - 1 : B.y0;
-    B.m1 = down ? B.y1 + 1 : B.y1;
-    B.t0 = std::max(0, B.y0 - 2 * R - 1);
+    B.m1 = down ? std::min(B.h, B.y1 + 1 + B.x) : B.y1;
+    B.t0 = std::max(0, B.y0 - B.halo);
     B.t1 = B.y0 + 4 * R;
     B.b0 = B.y1 - 4 * R;
-    B.b1 = std::min(B.h, B.y1 + 2 * R + 1);
+    B.b1 = std::min(B.h, B.y1 + B.halo);
     if ((rc = make_plan(B.pe_t, 1, B.t1 - B.t0, B.w, B.CI, B.CP, R, eps, 1, FGF_SUB_NEAREST)))
         return rc;
     if ((rc = make_plan(B.pe_b, 1, B.b1 - B.b0, B.w, B.CI, B.CP, R, eps, 1, FGF_SUB_NEAREST)))
@@ -231,13 +237,13 @@ int band_ovl_prepare(const BandPlan& B, const float* I, const float* p, char* ws
     return FGF_OK;
 }
 
-// Halo of plane j for the overlapped exchange: own rows [y0, y0 + 2r' + 1) go up and arrive as
-// the upper neighbour's rows [y1', b1'); own rows [y1 - 2r' - 1, y1) go down.
+// Halo of plane j for the overlapped exchange: own rows [y0, y0 + halo) go up and arrive as
+// the upper neighbour's rows [y1', b1'); own rows [y1 - halo, y1) go down (halo = 2r'+1+x).
 Halo band_ovl_halo(const BandPlan& B, char* ws, int j) {
     const bool up = B.row0 > 0, down = B.row0 + B.rows < B.H;
     Halo hl{};
     const size_t w = B.w;
-    const int H2 = 2 * B.R + 1;
+    const int H2 = B.halo;
     if (up) {
         float* et = reinterpret_cast<float*>(ws + B.o_et) + (size_t)j * (B.t1 - B.t0) * w;
         hl.n_up = (size_t)(B.y0 - B.t0) * w;
@@ -297,7 +303,7 @@ int band_ovl_assemble(const BandPlan& B, char* ws, bool edges, cudaStream_t st) 
         return rc;
     if (down &&
         (rc = cp(reinterpret_cast<const float*>(ws + B.o_ebm), B.b1 - B.b0, B.y1 - 2 * R - B.b0,
-                 B.y1 - 2 * R, 2 * R + 1)))
+                 B.y1 - 2 * R, B.m1 - (B.y1 - 2 * R))))
         return rc;
     return FGF_OK;
 }
@@ -369,7 +375,7 @@ Halo band_halo(const BandPlan& B, char* ws, int j, int rank, int nranks) {
     return hl;
 }
 
-// Two-step exchange B geometry of a, b plane m: r'+1 own rows each way, into [f0, y0), [y1, f1).
+// Two-step exchange B geometry of a, b plane m: r'+1+x own rows each way, into [f0, y0), [y1, f1).
 Halo band_halo_ab(const BandPlan& B, char* ws, int m, int rank, int nranks) {
     float* ab = reinterpret_cast<float*>(ws + B.o_ab) + m * B.ab_plane;
     Halo hl{};

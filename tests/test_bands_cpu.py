@@ -24,14 +24,17 @@ def _free_port():
 
 
 @pytest.mark.parametrize("H,W,r,s,world", [(64, 48, 4, 2, 2), (100, 40, 8, 4, 3), (4096, 64, 32, 4, 8),
-                                           (16384, 16, 32, 4, 8)])
+                                           (16384, 16, 32, 4, 8), (101, 40, 8, 4, 3),
+                                           (253, 364, 4, 4, 6)])
 def test_band_plan_tiles_the_image(H, W, r, s, world):
     plans = [bands.plan_band(H, W, r, s, world, k) for k in range(world)]
     assert plans[0].Y0 == 0 and plans[-1].Y1 == H
     for a, b in zip(plans, plans[1:]):
         assert a.Y1 == b.Y0 and a.y1 == b.y0 and b.Y0 % s == 0
     for pl in plans:
-        assert pl.halo == 2 * pl.R + 1 == 2 * oracle.radius_lowres(r, s) + 1
+        # one extra row when h s != H: the map scale h / H > 1 / s reaches low-res row y1 + 1
+        x = int(pl.h * s != H)
+        assert pl.halo == 2 * pl.R + 1 + x == 2 * oracle.radius_lowres(r, s) + 1 + x
         assert pl.e0 == max(0, pl.y0 - pl.halo) and pl.e1 == min(pl.h, pl.y1 + pl.halo)
 
 
@@ -45,16 +48,32 @@ def _image(H, W, C, seed):
     return torch.rand((1, C, H, W), generator=g, dtype=torch.float32)
 
 
-@pytest.mark.parametrize("C_I,sub", [(1, 0), (3, 1)])
-def test_local_band_simulation_matches_whole_image(C_I, sub):
+@pytest.mark.parametrize("C_I,sub,H", [(1, 0, 90), (3, 1, 90), (1, 0, 89), (3, 1, 88)])
+def test_local_band_simulation_matches_whole_image(C_I, sub, H):
+    """H = 89, 88: not multiples of s, so the last rows of a band upsample from the low-res row
+    after the band (the halo grows by one row; found by the GPU band fuzz)."""
     from tests.band_oracle_backend import OracleBackend
-    H, W, r, s, eps = 90, 52, 6, 3, 0.01
+    W, r, s, eps = 52, 6, 3, 0.01
     I = _image(H, W, C_I, 1)
     p = _image(H, W, 2, 2)
     ref = oracle.fast_guided_filter(I.numpy(), p.numpy(), r, eps, s, sub)
     for world in (2, 3):
         q = bands.filter_bands_local(I, p, r, eps, s, sub, world, backend=OracleBackend())
         assert float(np.abs(q.numpy() - ref).max()) < 1e-6
+
+
+@pytest.mark.parametrize("sub", [0, 1])
+def test_local_bands_when_H_is_not_a_multiple_of_s(sub):
+    """H = 4 h - 3 at s = 4: the map scale h / H exceeds 1 / s by the most, and the last rows of
+    the bands ending below ~5/6 of the image upsample from the low-res row after the band --
+    the halo carries one more row (found by the GPU band fuzz, seed 153)."""
+    from tests.band_oracle_backend import OracleBackend
+    H, W, r, s, eps, world = 253, 60, 4, 4, 1e-3, 8
+    I = _image(H, W, 1, 3)
+    p = _image(H, W, 2, 4)
+    ref = oracle.fast_guided_filter(I.numpy(), p.numpy(), r, eps, s, sub)
+    q = bands.filter_bands_local(I, p, r, eps, s, sub, world, backend=OracleBackend())
+    assert float(np.abs(q.numpy() - ref).max()) < 1e-6
 
 
 def _worker(rank, world, port, H, W, r, s, eps, sub, out_path):
@@ -76,9 +95,9 @@ def _worker(rank, world, port, H, W, r, s, eps, sub, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_band_exchange_matches_whole_image(tmp_path, world):
-    H, W, r, s, eps, sub = 96, 40, 6, 2, 0.02, 0
+@pytest.mark.parametrize("world,H", [(2, 96), (3, 96), (3, 95)])
+def test_gloo_band_exchange_matches_whole_image(tmp_path, world, H):
+    W, r, s, eps, sub = 40, 6, 2, 0.02, 0
     out = str(tmp_path / "q.npy")
     mp.spawn(_worker, args=(world, _free_port(), H, W, r, s, eps, sub, out), nprocs=world,
              join=True)

@@ -178,3 +178,35 @@ def test_c_band_loopback_two_step_narrow_bands():
                                        torch.cuda.current_stream(), mode=fgf.FGF_BAND_SINGLE,
                                        check=False)
     assert rc == fgf.FGF_ERR_PARAM
+
+
+@pytest.mark.parametrize("sub", [0, 1])
+def test_c_band_block_mean_workspace(sub):
+    """Found by the band fuzz (seed 11): with the block mean (R4) a band's own chain needs the
+    compact I', p' planes, which the workspace query sized for the nearest mode only (NOMEM).
+    The query now covers both subsampling modes, as fgf_workspace_bytes does."""
+    H, W, CI, CP, r, s, nranks = 560, 119, 1, 2, 14, 4, 4
+    g = torch.Generator(device="cuda").manual_seed(11)
+    I = torch.rand((1, CI, H, W), device="cuda", generator=g)
+    p = torch.rand((1, CP, H, W), device="cuda", generator=g)
+    q = _loopback(I, p, r, 1e-3, s, sub, nranks, fgf.FGF_BAND_SINGLE)
+    q_whole = fgf.filter(I, p, r, 1e-3, s, sub)
+    torch.cuda.synchronize()
+    assert float((q - q_whole).abs().max()) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("H,s,sub,nranks", [(253, 4, 1, 6), (253, 4, 0, 8), (1021, 8, 0, 5),
+                                            (2045, 4, 1, 3)])
+def test_c_band_height_not_a_multiple_of_s(H, s, sub, nranks, mode):
+    """Found by the band fuzz (seed 153): when h s != H the map scale h / H exceeds 1 / s and
+    the last rows of a band upsample from the low-res row after the band, so the halo carries
+    one more row (fgf_band.cuh).  Before the fix row 211 of this 253-row image was off by 2e-3."""
+    W, r, eps = 364, 2 * s, 1e-3
+    g = torch.Generator(device="cuda").manual_seed(H + nranks)
+    I = torch.rand((1, 1, H, W), device="cuda", generator=g)
+    p = torch.rand((1, 2, H, W), device="cuda", generator=g)
+    q = _loopback(I, p, r, eps, s, sub, nranks, mode)
+    q_whole = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    assert float((q - q_whole).abs().max()) <= 1e-5

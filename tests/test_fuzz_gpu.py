@@ -78,3 +78,43 @@ def test_fuzz_against_oracle(seed):
         err = np.abs(got - ref)
         assert (err <= bound).all(), (seed, B, H, W, CI, CP, r, eps, s, sub, dtype,
                                       float(err.max()))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FGF_FUZZ_BAND_SEEDS", "40"))))
+def test_fuzz_band_loopback(seed):
+    """Random row-band splits through the C band path (fgf_filter_bands_loopback: the same
+    plans, phases and halo geometry as fgf_filter_band over NCCL) -- overlapped single
+    exchange where the bands are tall enough, compacting single or two-step exchange otherwise
+    -- against the whole-image filter (same kernels: <= 1e-5) and the oracle."""
+    rng = np.random.default_rng(5000 + seed)
+    CI = int(rng.choice([1, 3]))
+    CP = int(rng.integers(1, 4))
+    s = int(rng.choice([1, 2, 3, 4]))
+    r = int(rng.integers(2, 40))
+    R = max(1, (2 * r + s) // (2 * s))
+    mode = int(rng.integers(0, 2))
+    nranks = int(rng.integers(2, 7))
+    need = (2 * R + 2) if mode == 0 else (R + 2)
+    h = int(rng.integers(nranks * need, nranks * need + 200))
+    H = min(h * s - int(rng.integers(0, s)), 2400)
+    h = -(-H // s)
+    need -= int(h * s == H)            # the halo's extra row only when h s != H
+    if any((k + 1) * h // nranks - k * h // nranks < need for k in range(nranks)):
+        pytest.skip("bands thinner than the exchange depth")
+    W = int(rng.integers(max(s + 1, 8), 700))
+    sub = int(rng.integers(0, 2))
+    eps = float(rng.choice([1e-4, 1e-3, 0.01]))
+    g = torch.Generator(device="cuda").manual_seed(6000 + seed)
+    I = torch.rand((1, CI, H, W), device="cuda", generator=g)
+    p = torch.rand((1, CP, H, W), device="cuda", generator=g)
+    nb = fgf.fgf_bands_loopback_workspace_bytes(H, W, CI, CP, r, s, nranks)
+    assert nb > 0, (H, W, CI, CP, r, s, nranks)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    q = torch.empty((1, CP, H, W), device="cuda")
+    fgf.fgf_filter_bands_loopback(I, p, q, H, W, CI, CP, r, eps, s, sub, nranks, ws, nb,
+                                  torch.cuda.current_stream(), mode=mode)
+    q_whole = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    assert float((q - q_whole).abs().max()) <= 1e-5, (seed, H, W, CI, CP, r, s, sub, mode, nranks)
+    ref = oracle.fast_guided_filter(I.cpu().numpy(), p.cpu().numpy(), r, eps, s, sub)
+    assert float(np.abs(q.double().cpu().numpy() - ref).max()) <= 1e-4
