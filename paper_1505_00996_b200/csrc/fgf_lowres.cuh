@@ -55,8 +55,18 @@ struct LowresParams {
     int TW, TH;            // output columns per strip, output rows per segment
     double eps;
     float k1, k0;          // written maps: k1 mean_a + k0 (map 0), k1 mean (others); 1, 0 = plain
+    int bulk_out;          // 1: the staged output rows go out as TMA bulk copies (host-checked:
+                           // w, TW and the Os pitches multiples of 4 floats, dst 16-byte aligned)
     LowresLayout L;        // LowresCfg<...>::layout(blockDim.x, TW, TH, R), set by the host
 };
+
+// Bulk shared -> global copy of `bytes` (multiple of 16, both addresses 16-byte aligned) by
+// the async proxy; completion tracked per issuing thread by bulk groups.
+__device__ __forceinline__ void lr_bulk_store(float* gdst, const float* ssrc, unsigned bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(gdst), "r"(s), "r"(bytes) : "memory");
+}
 
 template <int CP, int G, int KA, int KB, bool RING = true>
 struct LowresCfg {
@@ -433,9 +443,23 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
                 }
             }
         }
+        if (P.bulk_out) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // Os -> async proxy
         __syncthreads();
-        // coalesced store of the outputs staged in Os
-        if (hbN > 0 && tid < TW && x0 + tid < w) {
+        // store of the outputs staged in Os: one TMA bulk copy per row and map (issued by one
+        // thread; Os is not rewritten before the copies have read it, see the end of X), or
+        // coalesced per-thread stores
+        if (P.bulk_out) {
+            if (tid == 0 && hbN > 0) {
+                const unsigned bytes = (unsigned)min(TW, w - x0) * 4u;
+                for (int g = 0; g < hbN; ++g) {
+#pragma unroll
+                    for (int m = 0; m < NAB; ++m)
+                        lr_bulk_store(dstimg + (size_t)m * n + (size_t)(hbY + g) * w + x0,
+                                      Os + (size_t)g * L.ROS + m * L.PB, bytes);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else if (hbN > 0 && tid < TW && x0 + tid < w) {
             float* d[NAB];
 #pragma unroll
             for (int m = 0; m < NAB; ++m) d[m] = dstimg + (size_t)m * n + (size_t)hbY * w + x0 + tid;
@@ -523,8 +547,11 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
             column_A(yA, nA);
             load_batch(yA + nA);
         }
+        // the bulk copies of the previous outputs have read Os before the next Y phase rewrites it
+        if (P.bulk_out && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
     }
+    if (P.bulk_out && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace fgf

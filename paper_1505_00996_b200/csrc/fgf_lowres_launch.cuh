@@ -66,6 +66,14 @@ inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
         if (NT < 64) break;
     }
     if (best.NT == 0) return false;
+    // 4-column multiples when the rows allow it: 16-byte aligned strips for the bulk stores
+    if (w % 4 == 0 && best.TW % 4 != 0) {
+        const int TW4 = (best.TW + 3) & ~3;
+        if ((TW4 + 4 * R + 31) / 32 * 32 == best.NT) {
+            best.TW = TW4;
+            best.strips = (w + TW4 - 1) / TW4;
+        }
+    }
     // Segment height: long segments amortise the 2r'+1 warm-up rows (up to h / 2 rows); small
     // batches (single images) get shorter segments so that ~2 waves of 3 CTAs per SM exist.
     const long long cols = (long long)best.strips * images;
@@ -96,6 +104,10 @@ int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, co
     auto kern = lowres_gray_kernel<CP, G, KA, KB, RING, MAXT, MINB, E>;
     LowresParams lpl = lp;
     lpl.L = LowresCfg<CP, G, KA, KB, RING>::layout(g.NT, lp.TW, lp.TH, P.R);
+    // TMA bulk stores of the staged output rows: every row segment and Os row 16-byte aligned
+    lpl.bulk_out = P.w % 4 == 0 && lp.TW % 4 == 0 && lpl.L.PB % 4 == 0 && lpl.L.ROS % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(lp.dst) & 15u) == 0 &&
+                   dev_env("FGF_LR_NOBULK") == nullptr;
     size_t smem = g.smem;
     // optional floor on the dynamic smem: caps K13 CTAs per SM so that the output pass of the
     // previous chunk can be co-resident (overlap experiment knob)
