@@ -110,30 +110,56 @@ struct WideCfg {
 // distinct fp64 banks), loaded into registers at once; a warp shuffle scan of the chunk
 // totals gives the offsets.  Entries in [n, kWidePitch) are zeros that are read but never
 // written.
+// SPLIT = true: the chunk's own prefix is formed first, as two half-chunk chains joined by one
+// add (dependent depth 7, not 13), under the latency of the shuffle scan, and the scanned
+// offset is then added to every entry independently (mean-maps mode, 2 CTAs / SM: config 4
+// s = 2 31.7 -> 30.0 ms); false: totals first, then one running chain (the fused s = 1 mode,
+// one CTA / SM: 12.97 vs 13.14 ms with SPLIT).
+template <bool SPLIT>
 __device__ __forceinline__ void warp_prefix_row(double* __restrict__ row, int n, int lane) {
     double* r = row + lane * kWideChMax;
     double v[kWideChMax];
 #pragma unroll
     for (int i = 0; i < kWideChMax; ++i) v[i] = r[i];
-    double t0 = 0.0, t1 = 0.0;                 // two chains: half the dependent latency
-#pragma unroll
-    for (int i = 0; i < kWideChMax; i += 2) {
-        t0 += v[i];
-        if (i + 1 < kWideChMax) t1 += v[i + 1];
-    }
-    const double tot = t0 + t1;
-    double x = tot;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += y;
-    }
-    double run = x - tot;
     const int e = n - lane * kWideChMax;       // valid entries of this chunk
+    if constexpr (SPLIT) {
+        constexpr int H1 = (kWideChMax + 1) / 2;   // half-chunks [0, H1), [H1, 13)
 #pragma unroll
-    for (int i = 0; i < kWideChMax; ++i) {
-        run += v[i];
-        if (i < e) r[i] = run;
+        for (int i = 1; i < kWideChMax; ++i)
+            if (i != H1) v[i] += v[i - 1];         // two independent chains
+#pragma unroll
+        for (int i = H1; i < kWideChMax; ++i) v[i] += v[H1 - 1];
+        const double tot = v[kWideChMax - 1];
+        double x = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        const double off = x - tot;            // exclusive scan of the chunk totals
+#pragma unroll
+        for (int i = 0; i < kWideChMax; ++i)
+            if (i < e) r[i] = off + v[i];
+    } else {
+        double t0 = 0.0, t1 = 0.0;             // two chains: half the dependent latency
+#pragma unroll
+        for (int i = 0; i < kWideChMax; i += 2) {
+            t0 += v[i];
+            if (i + 1 < kWideChMax) t1 += v[i + 1];
+        }
+        const double tot = t0 + t1;
+        double x = tot;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        double run = x - tot;
+#pragma unroll
+        for (int i = 0; i < kWideChMax; ++i) {
+            run += v[i];
+            if (i < e) r[i] = run;
+        }
     }
 }
 
@@ -433,7 +459,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             __syncthreads();
             if (BULK && tid == 0 && ya + G < yA1) bulk_batch(ya + G);   // in flight under P1-P4
             // ---- P1: prefix sums of the snapshotted rows
-            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row(VA + rs * PW, NCS, lane);
+            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row<!OUTQ>(VA + rs * PW, NCS, lane);
             __syncthreads();
             // ---- P2: window sums, coefficient epilogue -> a, b (fp64 rows for P3)
             if (tid < NCA) {
@@ -471,7 +497,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             }
             __syncthreads();
             // ---- P3: prefix sums of the a, b rows
-            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row(AB + rs * PW, NCA, lane);
+            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row<!OUTQ>(AB + rs * PW, NCA, lane);
             __syncthreads();
             // ---- P4: horizontal box of a, b, vertical running window through the ring, output
             if (colO) {
