@@ -115,52 +115,86 @@ struct WideCfg {
 // offset is then added to every entry independently (mean-maps mode, 2 CTAs / SM: config 4
 // s = 2 31.7 -> 30.0 ms); false: totals first, then one running chain (the fused s = 1 mode,
 // one CTA / SM: 12.97 vs 13.14 ms with SPLIT).
-template <bool SPLIT>
-__device__ __forceinline__ void warp_prefix_row(double* __restrict__ row, int n, int lane) {
-    double* r = row + lane * kWideChMax;
-    double v[kWideChMax];
+template <bool SPLIT, int NR = 1>
+__device__ __forceinline__ void warp_prefix_rows(double* __restrict__ row0, int stride, int n,
+                                                 int lane) {
+    // NR rows (row0 + k stride) scanned together: independent chains interleaved (ILP NR)
+    double v[NR][kWideChMax];
 #pragma unroll
-    for (int i = 0; i < kWideChMax; ++i) v[i] = r[i];
+    for (int k = 0; k < NR; ++k) {
+        const double* r = row0 + (size_t)k * stride + lane * kWideChMax;
+#pragma unroll
+        for (int i = 0; i < kWideChMax; ++i) v[k][i] = r[i];
+    }
     const int e = n - lane * kWideChMax;       // valid entries of this chunk
+    double tot[NR], base[NR];
     if constexpr (SPLIT) {
         constexpr int H1 = (kWideChMax + 1) / 2;   // half-chunks [0, H1), [H1, 13)
 #pragma unroll
         for (int i = 1; i < kWideChMax; ++i)
-            if (i != H1) v[i] += v[i - 1];         // two independent chains
 #pragma unroll
-        for (int i = H1; i < kWideChMax; ++i) v[i] += v[H1 - 1];
-        const double tot = v[kWideChMax - 1];
-        double x = tot;
+            for (int k = 0; k < NR; ++k)
+                if (i != H1) v[k][i] += v[k][i - 1];   // two independent chains per row
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        const double off = x - tot;            // exclusive scan of the chunk totals
+        for (int i = H1; i < kWideChMax; ++i)
 #pragma unroll
-        for (int i = 0; i < kWideChMax; ++i)
-            if (i < e) r[i] = off + v[i];
+            for (int k = 0; k < NR; ++k) v[k][i] += v[k][H1 - 1];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) tot[k] = v[k][kWideChMax - 1];
     } else {
-        double t0 = 0.0, t1 = 0.0;             // two chains: half the dependent latency
 #pragma unroll
-        for (int i = 0; i < kWideChMax; i += 2) {
-            t0 += v[i];
-            if (i + 1 < kWideChMax) t1 += v[i + 1];
-        }
-        const double tot = t0 + t1;
-        double x = tot;
+        for (int k = 0; k < NR; ++k) {
+            double t0 = 0.0, t1 = 0.0;             // two chains: half the dependent latency
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, x, d);
-            if (lane >= d) x += y;
-        }
-        double run = x - tot;
-#pragma unroll
-        for (int i = 0; i < kWideChMax; ++i) {
-            run += v[i];
-            if (i < e) r[i] = run;
+            for (int i = 0; i < kWideChMax; i += 2) {
+                t0 += v[k][i];
+                if (i + 1 < kWideChMax) t1 += v[k][i + 1];
+            }
+            tot[k] = t0 + t1;
         }
     }
+    double x[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) x[k] = tot[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+            const double y = __shfl_up_sync(0xffffffffu, x[k], d);
+            if (lane >= d) x[k] += y;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NR; ++k) base[k] = x[k] - tot[k];   // exclusive scan of the totals
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        double* r = row0 + (size_t)k * stride + lane * kWideChMax;
+        if constexpr (SPLIT) {
+#pragma unroll
+            for (int i = 0; i < kWideChMax; ++i)
+                if (i < e) r[i] = base[k] + v[k][i];
+        } else {
+            double run = base[k];
+#pragma unroll
+            for (int i = 0; i < kWideChMax; ++i) {
+                run += v[k][i];
+                if (i < e) r[i] = run;
+            }
+        }
+    }
+}
+
+// nrows rows (row0 + rs PW) over the NW warps of the CTA: pairs of rows per warp while two
+// are left for it (P2 = true), then single rows.
+template <bool SPLIT, bool P2>
+__device__ __forceinline__ void warp_prefix_all(double* __restrict__ row0, int nrows, int n,
+                                                int warp, int NW, int lane) {
+    int rs = warp;
+    if constexpr (P2) {
+        for (; rs + NW < nrows; rs += 2 * NW)
+            warp_prefix_rows<SPLIT, 2>(row0 + (size_t)rs * kWidePitch, NW * kWidePitch, n, lane);
+    }
+    for (; rs < nrows; rs += NW) warp_prefix_rows<SPLIT, 1>(row0 + (size_t)rs * kWidePitch, 0, n, lane);
 }
 
 // Number of indices of [i - R, i + R] inside [0, n).
@@ -459,7 +493,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             __syncthreads();
             if (BULK && tid == 0 && ya + G < yA1) bulk_batch(ya + G);   // in flight under P1-P4
             // ---- P1: prefix sums of the snapshotted rows
-            for (int rs = warp; rs < nA * NMAP; rs += NW) warp_prefix_row<!OUTQ>(VA + rs * PW, NCS, lane);
+            warp_prefix_all<!OUTQ, OUTQ>(VA, nA * NMAP, NCS, warp, NW, lane);
             __syncthreads();
             // ---- P2: window sums, coefficient epilogue -> a, b (fp64 rows for P3)
             if (tid < NCA) {
@@ -497,7 +531,7 @@ __global__ void __launch_bounds__(kWideMaxCols, MINB) wide_gray_kernel(WideParam
             }
             __syncthreads();
             // ---- P3: prefix sums of the a, b rows
-            for (int rs = warp; rs < nA * NAB; rs += NW) warp_prefix_row<!OUTQ>(AB + rs * PW, NCA, lane);
+            warp_prefix_all<!OUTQ, OUTQ>(AB, nA * NAB, NCA, warp, NW, lane);
             __syncthreads();
             // ---- P4: horizontal box of a, b, vertical running window through the ring, output
             if (colO) {

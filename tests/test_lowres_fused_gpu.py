@@ -141,3 +141,38 @@ def test_tall_image_default_segments():
         fgf.fgf_profile_enable(False)
     assert prof["lowres_fused"][1] == 1, prof
     assert oracle_err(I, p, q, 3, 1e-3, 1, 0) <= 1e-4
+
+
+# (B, H, W, r, s, TH): w % 4 == 0 (bulk stores), w % 4 != 0 and TW rounded to 4 columns
+BULK_CASES = [
+    (2, 1024, 1024, 32, 4, None),     # config-4 geometry: TW 128, every row segment 512 B
+    (1, 2160, 3840, 16, 4, None),     # config 1: w = 960, TW rounded 138 -> 140
+    (1, 203, 1204, 9, 4, 8),          # w = 301: per-thread stores (no bulk)
+    (3, 97, 388, 5, 1, 5),            # s = 1, several segments, ragged last strip
+]
+
+
+@pytest.mark.parametrize("case", BULK_CASES)
+def test_bulk_output_stores_bit_identical(case):
+    """K13's staged output rows leave by TMA bulk copies when the rows are 16-byte aligned;
+    the per-thread store path (FGF_LR_NOBULK) must give the same maps bit for bit (same
+    strips: the geometry does not depend on the store path)."""
+    B, H, W, r, s, TH = case
+    g = torch.Generator(device="cuda").manual_seed(101 + H)
+    I = torch.rand((B, 1, H, W), device="cuda", generator=g)
+    p = torch.rand((B, 1, H, W), device="cuda", generator=g)
+    with env(FGF_LR_TH=TH, FGF_ENGINE="k13", FGF_LR_NOBULK=None):
+        fgf.fgf_profile_enable(True)
+        m1 = fgf.coefficients(I, p, r, 0.01, s, 0)
+        torch.cuda.synchronize()
+        prof = fgf.fgf_profile_read()
+        fgf.fgf_profile_enable(False)
+    with env(FGF_LR_TH=TH, FGF_ENGINE="k13", FGF_LR_NOBULK="1"):
+        m2 = fgf.coefficients(I, p, r, 0.01, s, 0)
+        torch.cuda.synchronize()
+    assert prof["lowres_fused"][1] == 1, prof
+    assert torch.equal(m1, m2)
+    if (W + s - 1) // s <= 1024 and B * H * W <= 1 << 21:
+        q = fgf.filter(I, p, r, 0.01, s, 0)
+        torch.cuda.synchronize()
+        assert oracle_err(I, p, q, r, 0.01, s, 0) <= 1e-4
