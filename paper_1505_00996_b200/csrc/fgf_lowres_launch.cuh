@@ -84,7 +84,24 @@ inline bool lowres_geom(LrGeom& g, int h, int w, int R, int images) {
     // add / remove steps per segment, whatever the image height: ADVICE r1; an fp64 or
     // periodically re-summed variant measured 3-6 % slower on config 4)
     const long long cap = std::max<long long>(256, std::min<long long>(512, (h + 1) / 2));
-    th = std::min<long long>(cap, std::max<long long>(th, std::max(8, 2 * R + 2)));
+    const long long thmin = std::max(8, 2 * R + 2);
+    th = std::min<long long>(cap, std::max<long long>(th, thmin));
+    // Small batches (fewer strip columns than CTA slots, 3 per SM): the segment count that
+    // minimises waves x rows streamed per CTA (TH + ~4r' + 3 warm-up rows) -- a launch just
+    // over a whole number of waves pays a nearly empty one (one 16384^2 image, 32 strips:
+    // TH 296 = 448 CTAs 0.734 ms, TH 342 = 384 CTAs 0.652 ms, the ~2-wave rule's 148 0.682 ms)
+    constexpr long long kSlots = 3LL * 148;
+    if (cols < kSlots) {
+        double best_cost = 1e300;
+        for (long long segs = 1; segs <= h; ++segs) {
+            const long long T = (h + segs - 1) / segs;
+            if (T < thmin) break;
+            if (T > cap) continue;
+            const long long items = cols * ((h + T - 1) / T);
+            const double cost = (double)((items + kSlots - 1) / kSlots) * (double)(T + 4 * R + 3);
+            if (cost < best_cost * 0.999) { best_cost = cost; th = T; }
+        }
+    }
     if (const char* e = dev_env("FGF_LR_TH")) th = atoi(e);
     best.TH = (int)std::max<long long>(1, std::min<long long>(th, h));
     if (const char* e = dev_env("FGF_LR_V")) {
