@@ -7,8 +7,10 @@ namespace fgf {
 template <int CP>
 int launch_lowres_gray_t(const LowresParams& lp0, int images, const Plan& P, cudaStream_t st,
                          bool dry) {
+    // geometry from the whole call's batch, not the pipeline chunk's: every chunk of a call
+    // then runs the same segments, so a chunked call equals the one-chunk call bit for bit
     LrGeom g;
-    if (!lowres_geom<CP>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
+    if (!lowres_geom<CP>(g, P.h, P.w, P.R, std::max(images, P.batch))) return FGF_ERR_UNSUPPORTED;
     if (dry) return FGF_OK;
     LowresParams lp = lp0;
     lp.TW = g.TW;
@@ -57,7 +59,7 @@ int launch_lowres_gray(const LowresParams& lp, int images, const Plan& P, cudaSt
             if (P.dtype != FGF_F32 && dry) {
                 // only variants 3 and 0 exist for reduced-precision inputs
                 LrGeom g;
-                if (!lowres_geom<1>(g, P.h, P.w, P.R, images)) return FGF_ERR_UNSUPPORTED;
+                if (!lowres_geom<1>(g, P.h, P.w, P.R, std::max(images, P.batch))) return FGF_ERR_UNSUPPORTED;
                 return (g.V == 3 || g.V == 0) ? FGF_OK : FGF_ERR_UNSUPPORTED;
             }
             return launch_lowres_gray_t<1>(lp, images, P, st, dry);

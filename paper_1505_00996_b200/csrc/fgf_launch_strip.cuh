@@ -28,6 +28,9 @@ int launch_strip_g(const StripParams& sp0, int images, const Plan& P, cudaStream
     long long thmax = P.R >= 16 ? 256 : 64;
     if (const char* e = dev_env("FGF_STRIP_THMAX")) thmax = atoi(e);
     int TH = (int)std::min<long long>(thmax, th);
+    // balanced segments: the same segment count with equal heights, no short last segment
+    // (config 3: 64 + 64 + 64 + 64 + 14 -> 5 x 54 rows, 1.982 -> 1.961 ms)
+    TH = (P.h + (P.h + TH - 1) / TH - 1) / ((P.h + TH - 1) / TH);
     TH = (TH + C::G - 1) / C::G * C::G;
     sp.TH = TH;
     sp.TW = P.TW;
