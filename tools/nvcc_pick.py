@@ -66,8 +66,9 @@ def main():
                 obj = os.path.join(tmp, f"try{t}.o")
                 procs.append((t, obj, subprocess.Popen(cmd + ["-o", obj], env=env)))
                 t += 1
-            for k, obj, pr in procs:
-                if pr.wait() != 0:
+            codes = [(k, obj, pr.wait()) for k, obj, pr in procs]   # all finished first
+            for k, obj, rc in codes:
+                if rc != 0:
                     sys.exit(f"nvcc_pick: compile {k} failed")
                 n = uniform_count(obj, a.kernel)
                 print(f"nvcc_pick: try {k}: {n} uniform instructions in {a.kernel[:48]}...", file=sys.stderr)
