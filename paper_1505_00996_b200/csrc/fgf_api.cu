@@ -362,7 +362,13 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
         int rc = run_lowres(I, p, reinterpret_cast<float*>(base + mean_off(P)), 0, P.batch, P,
                             base, st);
         if (rc) return rc;
-        return launch_output(I, reinterpret_cast<float*>(base + mean_off(P)), q, P.batch, P, st);
+        // small launches (<= 16 Mi low-res samples, K13 in about one wave): K4 as a
+        // programmatic dependent of K13, so its map-independent prologue and first guidance
+        // rows overlap K13's tail (FGF_NO_PDL=1: a plain launch)
+        Plan Po = P;
+        Po.pdl_out = P.engine == ENG_K13 && (size_t)P.batch * P.n <= (16u << 20) &&
+                     dev_env("FGF_NO_PDL") == nullptr;
+        return launch_output(I, reinterpret_cast<float*>(base + mean_off(P)), q, P.batch, Po, st);
     }
     std::lock_guard<std::mutex> lk(g_pipe_mu);
     Pipe* pp = nullptr;

@@ -115,6 +115,7 @@ struct Plan {
     // engine and workspace carve-up per pipeline slot (bytes), from plan_layout()
     int engine = ENG_STRIP;
     bool fused_out = false;       // K5 at s = 1: one kernel writes q (no mean maps, no K4)
+    bool pdl_out = false;         // K4 launched as a programmatic dependent of K13 (run_all)
     size_t ws_planes, ws_coef, ws_mean, ws_ring, ws_slot;
     int nslots;
 };

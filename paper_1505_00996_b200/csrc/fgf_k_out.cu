@@ -62,7 +62,21 @@ int launch_output_px(const OutParams& op0, int images, const Plan& P, cudaStream
                 auto kern = output_async_kernel<CI, CP, PX, E>;
                 set_smem(kern, asm_);
                 ProfScope ps(KIND_OUT, st);
-                kern<<<grid, 256, asm_, st>>>(op);
+                if (op.pdl) {
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = grid;
+                    cfg.blockDim = dim3(256);
+                    cfg.dynamicSmemBytes = asm_;
+                    cfg.stream = st;
+                    cudaLaunchAttribute at[1];
+                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[0].val.programmaticStreamSerializationAllowed = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 1;
+                    if (cudaLaunchKernelEx(&cfg, kern, op) != cudaSuccess) return FGF_ERR_CUDA;
+                } else {
+                    kern<<<grid, 256, asm_, st>>>(op);
+                }
                 ++g_last_launches;
                 return last_error();
             }
@@ -149,7 +163,7 @@ int launch_output_t(const OutParams& op, int images, const Plan& P, cudaStream_t
 int launch_output(const void* I, const float* M, void* q, int images, const Plan& P,
                   cudaStream_t st, const Band* band) {
     const Band b = band ? *band : Band{P.H, P.h, 0, 0, P.h};
-    OutParams op{I, M, q, P.H, P.W, b.hm, P.w, b.Hg, b.hg, b.Yoff, b.yoff, P.TR};
+    OutParams op{I, M, q, P.H, P.W, b.hm, P.w, b.Hg, b.hg, b.Yoff, b.yoff, P.TR, P.pdl_out ? 1 : 0};
     if (P.dtype != FGF_F32) {
         // reduced-precision I/O: gray -> gray, colour -> colour, colour guide -> one channel
         const int key = P.CI * 10 + P.CP;

@@ -655,6 +655,9 @@ struct OutParams {
     int Hg, hg;            // global full-res / low-res heights (the vertical map, R5)
     int Yoff, yoff;        // global row of local row 0 of I/q, and of the maps buffer
     int TR;                // full-resolution rows walked by each thread
+    int pdl;               // 1: launched as a programmatic dependent of the kernel writing M --
+                           // the guidance rows are prefetched before griddepcontrol.wait, the
+                           // maps staged after it (output_async_kernel)
 };
 
 // R5: source coordinate of destination index d, resize n_src -> n_dst, exactly in
@@ -956,16 +959,29 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
     src_coord(min(W, X0 + 256 * PX) - 1, w, W, xd, xhi, fd);
     xlo &= ~3;
     const int nrl = yhi - ylo + 1, ncl = (xhi + 1 - xlo + 3) & ~3;
-    stage_rect<NC, 256>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, tid);   // commit group 0
-    cp_async_commit();
     // Issue the first U rows (one commit group per row, empty groups keep the count uniform).
+    auto issue_rows = [&] {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        if (act && u < nrows)
+        for (int u = 0; u < U; ++u) {
+            if (act && u < nrows)
 #pragma unroll
-            for (int j = 0; j < CI; ++j)
-                cp_async_px<V::BYTES>(&ring[(u * CI + j) * 256 + tid], Ip + j * N + (size_t)u * W);
+                for (int j = 0; j < CI; ++j)
+                    cp_async_px<V::BYTES>(&ring[(u * CI + j) * 256 + tid], Ip + j * N + (size_t)u * W);
+            cp_async_commit();
+        }
+    };
+    if (P.pdl) {
+        // programmatic dependent of the low-res chain: everything that does not read the
+        // maps (row table, coordinates, the first U guidance rows) overlaps its tail; the
+        // maps are staged once it has completed
+        issue_rows();
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        stage_rect<NC, 256>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, tid);
         cp_async_commit();
+    } else {
+        stage_rect<NC, 256>(Ms, Mb, n, w, ylo, nrl, xlo, ncl, tid);   // commit group 0
+        cp_async_commit();
+        issue_rows();
     }
     int oa[PX], ob[PX];
     float fx[PX];
@@ -975,7 +991,9 @@ __global__ void __launch_bounds__(256, (AsyncCfg<CI, CP, PX, E>::MINB)) output_a
         oa[i] -= xlo;
         ob[i] -= xlo;
     }
-    cp_async_wait<U>();                             // the rectangle (group 0) has landed
+    // the rectangle has landed: group 0, or (pdl) the last group
+    if (P.pdl) cp_async_wait<0>();
+    else cp_async_wait<U>();
     __syncthreads();
 
     int cy = -2, cy1 = -2;

@@ -142,6 +142,10 @@ __global__ void __launch_bounds__(MAXT, MINB) lowres_gray_kernel(LowresParams P)
     using C = LowresCfg<CP, G, KA, KB, RING>;
     constexpr int NIN = C::NIN, NMAP = C::NMAP, NAB = C::NAB;
     extern __shared__ __align__(16) unsigned char smem[];
+    // a programmatic dependent (K4 launched with programmatic stream serialisation) may start
+    // its map-independent prologue once every CTA of this grid is running; it waits for this
+    // grid's completion (griddepcontrol.wait) before reading the maps.  No-op otherwise.
+    asm volatile("griddepcontrol.launch_dependents;");
     const int NT = blockDim.x, tid = threadIdx.x;
     const int h = P.h, w = P.w, R = P.R, TW = P.TW;
     const LowresLayout& L = P.L;
