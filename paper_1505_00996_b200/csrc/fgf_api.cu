@@ -366,7 +366,11 @@ int run_all(const void* I, const void* p, void* q, const Plan& P, void* ws, size
         // programmatic dependent of K13, so its map-independent prologue and first guidance
         // rows overlap K13's tail (FGF_NO_PDL=1: a plain launch)
         Plan Po = P;
-        Po.pdl_out = P.engine == ENG_K13 && (size_t)P.batch * P.n <= (16u << 20) &&
+        // (the colour chain only for single-frame sizes: config 2 135.5 -> 133.3 us, while 64
+        // frames of config 3 measured 1.983 -> 2.000 ms)
+        const size_t lr = (size_t)P.batch * P.n;
+        Po.pdl_out = ((P.engine == ENG_K13 && lr <= (16u << 20)) ||
+                      (P.engine == ENG_STRIP && lr <= (1u << 20))) &&
                      dev_env("FGF_NO_PDL") == nullptr;
         return launch_output(I, reinterpret_cast<float*>(base + mean_off(P)), q, P.batch, Po, st);
     }

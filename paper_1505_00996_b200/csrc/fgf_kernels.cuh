@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(NT, (StripConfig<MODE, CI, CP, NT, G_, MINB_>:
     constexpr int G = C::G;
     constexpr int K = C::K;
     extern __shared__ double smem_d[];
+    // box of a, b: a programmatic dependent (K4, run_all) may start its map-independent
+    // prologue once every CTA of this grid is running (no-op otherwise)
+    if (MODE == MODE_MEAN) asm volatile("griddepcontrol.launch_dependents;");
     const int VP = P.VP;
     double* Vs = smem_d;                                                  // [G][NMAP][VP]
     float* Os = reinterpret_cast<float*>(Vs + (size_t)G * NMAP * VP);      // [G][NOUT][NT]
