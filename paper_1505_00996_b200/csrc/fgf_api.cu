@@ -205,9 +205,12 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
     if (eng != ENG_STRIP && blk) {
         float* Isw = planes;
         float* psw = planes + (size_t)nb * P.n;
-        if ((rc = launch_subsample(Ib, Isw, nb, P, st))) return rc;
-        if (p_is_I) psw = Isw;
-        else if ((rc = launch_subsample(pb, psw, nb * P.CP, P, st))) return rc;
+        if (p_is_I) {
+            if ((rc = launch_subsample(Ib, Isw, nb, P, st))) return rc;
+            psw = Isw;
+        } else if ((rc = launch_subsample2(Ib, nb, pb, nb * P.CP, Isw, P, st))) {
+            return rc;                    // I' then p' planes, psw = Isw + nb n
+        }
         Is = Isw;
         ps = psw;
     }
@@ -265,9 +268,12 @@ int run_lowres(const void* I, const void* p, float* mean, int b0, int nb, const 
         // (s = 1 with reduced-precision inputs: the conversion to fp32).
         float* Is = planes;
         float* ps = planes + (size_t)nb * P.CI * P.n;
-        if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
-        if (p_is_I) ps = Is;
-        else if ((rc = launch_subsample(pb, ps, nb * P.CP, P, st))) return rc;
+        if (p_is_I) {
+            if ((rc = launch_subsample(Ib, Is, nb * P.CI, P, st))) return rc;
+            ps = Is;
+        } else if ((rc = launch_subsample2(Ib, nb * P.CI, pb, nb * P.CP, Is, P, st))) {
+            return rc;                    // I' then p' planes, ps = Is + nb C_I n
+        }
         sp.srcI = Is; sp.imgI = (long long)P.CI * P.n; sp.planeI = (int)P.n;
         sp.srcP = ps; sp.imgP = (p_is_I ? 1LL : (long long)P.CP) * P.n; sp.planeP = (int)P.n;
         sp.row = P.w; sp.col = 1;

@@ -160,6 +160,9 @@ struct Band {
 // ---- launcher entry points (each returns an FGF_* status; launches go on stream st)
 // K0 (fgf_k_mean.cu): step 1 into compact fp32 low-res planes.
 int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cudaStream_t st);
+// ... planes from src then planes2 from src2 in one launch, into consecutive dst planes
+int launch_subsample2(const void* src, int planes, const void* src2, int planes2, float* dst,
+                      const Plan& P, cudaStream_t st);
 // K1 / K3 strip engine (fgf_k_stats.cu: MODE_STATS, fgf_k_mean.cu: MODE_MEAN).
 template <int MODE>
 int launch_strip(const StripParams& sp, int images, const Plan& P, cudaStream_t st);

@@ -117,7 +117,17 @@ struct SubParams {
     float* dst;             // [plane][h][w]
     int H, W, h, w, s;
     int rows_per_cta;       // low-res rows per CTA (grid-y covers h / rows_per_cta)
+    const void* src2;       // planes >= nsplit come from src2 (one launch for I and p)
+    int nsplit;
 };
+
+// Source plane `plane` of a K0 launch (two inputs in one grid: src, then src2).
+template <typename E>
+__device__ __forceinline__ const E* sub_src(const SubParams& P, size_t plane) {
+    const size_t HW = (size_t)P.H * P.W;
+    return plane < (size_t)P.nsplit ? static_cast<const E*>(P.src) + plane * HW
+                                    : static_cast<const E*>(P.src2) + (plane - P.nsplit) * HW;
+}
 
 // R4: mean of the clipped s x s block, summed in fp64.  One thread per
 // low-res column, several low-res rows per CTA for memory-level parallelism.
@@ -127,7 +137,7 @@ __global__ void __launch_bounds__(256) subsample_block_kernel(SubParams P) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= P.w) return;
     const size_t plane = blockIdx.z;
-    const E* src = static_cast<const E*>(P.src) + plane * (size_t)P.H * P.W;
+    const E* src = sub_src<E>(P, plane);
     float* dst = P.dst + plane * (size_t)P.h * P.w;
     const int y0 = blockIdx.y * P.rows_per_cta;
     const int y1 = min(P.h, y0 + P.rows_per_cta);
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(256) subsample_nearest_kernel(SubParams P) {
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= P.w) return;
     const size_t plane = blockIdx.z;
-    const E* src = static_cast<const E*>(P.src) + plane * (size_t)P.H * P.W + (size_t)x * P.s;
+    const E* src = sub_src<E>(P, plane) + (size_t)x * P.s;
     float* dst = P.dst + plane * (size_t)P.h * P.w + x;
     const int y0 = blockIdx.y * RPC;
     float v[RPC];
