@@ -13,8 +13,11 @@ TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_wide fgf_k_tiny fgf_k_apps
 OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
 ORACLE := oracle/libfgf_oracle.so
+# test infrastructure: NCCL point-to-point stand-in for multi-process band tests on one GPU
+SHIM := tests/libnccl_shim.so
+CUDA_HOME ?= /usr/local/cuda
 
-all: $(LIB) $(ORACLE)
+all: $(LIB) $(ORACLE) $(SHIM)
 
 # K13 compiled through nvcc's split-compile path: there its loop and ring indices stay on the
 # uniform datapath (550 uniform instructions vs 68), measured 4.14 -> 4.03 ms on config 4; the
@@ -49,7 +52,10 @@ $(LIB): $(OBJS)
 $(ORACLE): oracle/fgf_oracle.c
 	gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC -o $@ $< -lm
 
+$(SHIM): tests/nccl_shim.cpp
+	g++ -O2 -std=c++17 -shared -fPIC -I$(CUDA_HOME)/include -o $@ $< -L$(CUDA_HOME)/lib64 -lcudart
+
 clean:
-	rm -f $(LIB) $(ORACLE)
+	rm -f $(LIB) $(ORACLE) $(SHIM)
 
 .PHONY: all clean

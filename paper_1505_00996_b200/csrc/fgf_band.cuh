@@ -51,7 +51,11 @@ const Nccl* nccl() {
     std::lock_guard<std::mutex> lk(g_nccl_mu);
     if (!g_nccl.tried) {
         g_nccl.tried = true;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // FGF_NCCL_LIB (a development knob, honoured only with FGF_DEV=1): another library
+        // with NCCL's point-to-point ABI -- tests/nccl_shim.cpp, which runs the multi-rank
+        // band path as several processes on one GPU
+        const char* lib = dev_env("FGF_NCCL_LIB");
+        void* h = dlopen(lib && *lib ? lib : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (h) {
             g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
             g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
