@@ -8,7 +8,7 @@ PKG := paper_1505_00996_b200
 LIB := $(PKG)/libfgf.so
 # one translation unit per kernel family, compiled in parallel (make -j), each in a single
 # ptxas pass: nvcc --split-compile made register allocation depend on the split count
-TUS := fgf_api fgf_k_stats fgf_k_mean fgf_k_out fgf_k_wide fgf_k_tiny fgf_k_apps fgf_k_lowres fgf_k_lowres_v3 fgf_k_lowres_v3h \
+TUS := fgf_api fgf_k_mean fgf_k_out fgf_k_wide fgf_k_tiny fgf_k_apps fgf_k_lowres fgf_k_lowres_v3 fgf_k_lowres_v3h \
        fgf_k_lowres_v3bf fgf_k_lowres_v3b
 OBJS := $(patsubst %,build/%.o,$(TUS))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/fgf.h
@@ -36,10 +36,15 @@ K13_fgf_k_lowres_v3 := $(call K13_SYM,f)
 K13_fgf_k_lowres_v3h := $(call K13_SYM,6__half)
 K13_fgf_k_lowres_v3bf := $(call K13_SYM,13__nv_bfloat16)
 K13_fgf_k_lowres_v3b := $(call K13_SYM,h)
+ELEM_fgf_k_lowres_v3 := float
+ELEM_fgf_k_lowres_v3h := __half
+ELEM_fgf_k_lowres_v3bf := __nv_bfloat16
+ELEM_fgf_k_lowres_v3b := uint8_t
 PICKED := fgf_k_lowres_v3 fgf_k_lowres_v3h fgf_k_lowres_v3bf fgf_k_lowres_v3b
-$(patsubst %,build/%.o,$(PICKED)): build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile tools/nvcc_pick.py
+# one source, fgf_k_lowres_v3.cu, compiled once per sample type
+$(patsubst %,build/%.o,$(PICKED)): build/%.o: $(PKG)/csrc/fgf_k_lowres_v3.cu $(HDRS) Makefile tools/nvcc_pick.py
 	@mkdir -p build
-	python3 tools/nvcc_pick.py --out $@ --kernel $(K13_$*) -- $(NVCC) $(NVFLAGS) --split-compile=2 -c $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+	python3 tools/nvcc_pick.py --out $@ --kernel $(K13_$*) -- $(NVCC) $(NVFLAGS) --split-compile=2 '-DFGF_V3_ELEM=$(ELEM_$*)' -c $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 
 build/%.o: $(PKG)/csrc/%.cu $(HDRS) Makefile
 	@mkdir -p build

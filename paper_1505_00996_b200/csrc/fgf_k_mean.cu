@@ -1,4 +1,5 @@
-// fgf_k_mean.cu -- K0: subsampling (Alg. 2 step 1) and K3: box of a, b
+// fgf_k_mean.cu -- the strip engine's launches: K0, subsampling (Alg. 2 step 1, PAPER.md
+// P:70-73), K1, box statistics + coefficients a, b (steps 2-4), and K3, box of a, b
 // (step 5).
 #include "fgf_launch_strip.cuh"
 
@@ -40,6 +41,7 @@ int launch_subsample(const void* src, float* dst, int planes, const Plan& P, cud
     return launch_subsample2(src, planes, nullptr, 0, dst, P, st);
 }
 
+template int launch_strip<MODE_STATS>(const StripParams&, int, const Plan&, cudaStream_t);
 template int launch_strip<MODE_MEAN>(const StripParams&, int, const Plan&, cudaStream_t);
 
 }  // namespace fgf

@@ -139,7 +139,7 @@ int launch_lowres_gray_g(const LowresParams& lp, const LrGeom& g, int images, co
 
 // The default variant (G 4, K 9/17, no sample ring, <= 160 threads x 3 CTAs/SM) for samples of
 // type E; each element type is instantiated in a translation unit of its own
-// (fgf_k_lowres_v3*.cu, built through tools/nvcc_pick.py).
+// (fgf_k_lowres_v3.cu compiled once per type, through tools/nvcc_pick.py).
 template <typename E>
 int launch_lowres_v3(const LowresParams& lp, const LrGeom& g, int images, const Plan& P,
                      cudaStream_t st);
