@@ -65,15 +65,19 @@ def _run_ranks(nranks, C_I, C_p, H, W, r, eps, s, sub, mode, seed, self_g, tmp_p
 
 
 @pytest.mark.parametrize("mode", [fgf.FGF_BAND_SINGLE, fgf.FGF_BAND_TWO_STEP])
-@pytest.mark.parametrize("nranks,C_I,C_p,s,sub,self_g", [(2, 1, 1, 4, 0, False),
-                                                        (4, 1, 1, 4, 0, True),
-                                                        (3, 3, 1, 2, 1, False),
-                                                        (3, 3, 3, 4, 0, False)])
-def test_band_processes_match_loopback_and_oracle(nranks, C_I, C_p, s, sub, self_g, mode,
+@pytest.mark.parametrize("nranks,C_I,C_p,s,sub,self_g,H,W", [(2, 1, 1, 4, 0, False, 1200, 1032),
+                                                            (4, 1, 1, 4, 0, True, 1200, 1032),
+                                                            (3, 3, 1, 2, 1, False, 1200, 1032),
+                                                            (3, 3, 3, 4, 0, False, 1200, 1032),
+                                                            (8, 1, 1, 4, 0, False, 4096, 1536),
+                                                            (5, 1, 2, 1, 0, False, 1001, 517)])
+def test_band_processes_match_loopback_and_oracle(nranks, C_I, C_p, s, sub, self_g, H, W, mode,
                                                   tmp_path):
+    """(8 ranks, r = 32, s = 4: config 4b's split and window on a 4096-row image; 5 ranks at
+    s = 1 with ragged bands and two p channels)"""
     if not os.path.exists(SHIM):
         pytest.fail("tests/libnccl_shim.so missing: run make")
-    H, W, r, eps, seed = 1200, 1032, 32, 0.01, 41 + nranks
+    r, eps, seed = 32, 0.01, 41 + nranks
     q = _run_ranks(nranks, C_I, C_p, H, W, r, eps, s, sub, mode, seed, self_g, tmp_path)
     g = torch.Generator(device="cuda").manual_seed(seed)
     I = torch.rand((1, C_I, H, W), device="cuda", generator=g)
