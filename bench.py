@@ -285,7 +285,10 @@ def main():
         torch.cuda.synchronize()
         graph.replay()
         torch.cuda.synchronize()
-        step = lambda st=stream: graph.replay()   # noqa: E731
+        def step(st=stream):
+            # replay on the timed stream (CUDAGraph.replay launches on the current stream)
+            with torch.cuda.stream(st):
+                graph.replay()
 
     props = torch.cuda.get_device_properties(dev)
     gpu_id = "GPU-" + str(props.uuid) if getattr(props, "uuid", None) else str(local)
