@@ -373,11 +373,16 @@ def main():
         + B * 4 * NC * n
     alg = {"upsample_output": B * (esize * CI * N + esize * CP * N + 4 * NC * n),
            "lowres_fused": lowres_bytes,
-           "wide_fused": (B * esize * N * (planes_in + CP)) if s == 1 else lowres_bytes}
+           "wide_fused": (B * esize * N * (planes_in + CP)) if s == 1 else lowres_bytes,
+           # K6 (whole filter of a small image in one kernel): read I once (its sample rows
+           # are part of it), the sample rows of p (all of p for block means), write q
+           "tiny_fused": B * esize * N * (CI + CP + (0 if args.config == 0 else
+                                                     (CP / s if sub == 0 else CP)))}
     names = {"upsample_output": "output_kernel (K4: bilinear upsample + q = A.I + B)",
              "lowres_fused": "lowres_gray_kernel (K13: fused low-res chain)",
              "wide_fused": ("wide_gray_kernel (K5: exact guided filter, Alg. 1, one kernel)"
-                            if s == 1 else "wide_gray_kernel (K5: wide-window low-res chain)")}
+                            if s == 1 else "wide_gray_kernel (K5: wide-window low-res chain)"),
+             "tiny_fused": "tiny_gray_kernel (K6: whole filter of a small image, one kernel)"}
     dom = max((k for k in prof if prof[k][1] and k in alg), key=lambda k: prof[k][0], default=None)
     roofline = None
     if dom is not None:
