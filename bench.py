@@ -579,11 +579,18 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
     if world > 1:
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     dt = float(dt.item())
-    h2d = Be * 4 * N * (CI + (0 if args.config == 0 else CP))
+    # bytes the call copies (the library's own rule: with nearest samples only the sample rows
+    # of p are read from the host buffer, include/fgf.h)
+    h2d = fgf.fgf_filter_host_input_bytes(Be, H, W, CI, CP, prm["r"], prm["s"], prm["sub_mode"],
+                                        args.config == 0)
+    h2d_dense = Be * 4 * N * (CI + (0 if args.config == 0 else CP))
     d2h = Be * 4 * N * CP
     return {"value": world * Be * N * steps / dt / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "batch_per_gpu": Be, "steps": steps,
-            "api": "fgf_filter_host (C ABI, pinned host buffers, H2D/compute/D2H overlapped)"}
+            "d2h_bytes_per_step": d2h, "h2d_bytes_dense_inputs": h2d_dense,
+            "batch_per_gpu": Be, "steps": steps,
+            "api": "fgf_filter_host (C ABI, pinned host buffers, H2D/compute/D2H overlapped; "
+                   "nearest samples: I whole + the sample rows of p cross the link, the rows "
+                   "Alg. 2 reads)"}
 
 
 if __name__ == "__main__":

@@ -120,9 +120,16 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
 /* As fgf_filter on HOST buffers (pinned memory gives overlapped transfers; pageable works
  * but serialises).  Streams each image through the device: host->device copy of I, p,
  * the filter, device->host copy of q, overlapped across images on separate streams.
- * Synchronous.  device: CUDA device ordinal to run on. */
+ * Synchronous.  device: CUDA device ordinal to run on.
+ * With FGF_SUB_NEAREST and s > 1 the method reads p only at its sample sites p[y s][x s]
+ * (the output step P:84-86 uses I alone at full resolution), so only rows y s of p are
+ * copied to the device (rows of >= 2 KB; the other rows of the host buffer are not read).
+ * fgf_filter_host_input_bytes: the host->device bytes one such call copies (0 on invalid
+ * arguments; self_guided != 0: p is the same buffer as I). */
 int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
                     int C_p, int r, double eps, int s, int sub_mode, int device);
+size_t fgf_filter_host_input_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s,
+                                 int sub_mode, int self_guided);
 
 /* Stages 1-5 only: writes the low-res mean maps mean_ab (DEVICE)
  * [batch][C_p][C_I+1][h][w] fp32 -- for p channel c, components j < C_I are mean_a_{c,j}

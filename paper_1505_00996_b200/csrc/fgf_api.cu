@@ -1247,6 +1247,23 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
     return launch_output(I, mean_ab, q, batch, P, static_cast<cudaStream_t>(cuda_stream), &band);
 }
 
+// fgf_filter_host copies only the sample rows of p when the subsampling is nearest (s > 1) and
+// the rows are long enough (>= 2 KB) for the copy engine's 2-D transfers to run at link rate.
+static bool host_p_sample_rows(const Plan& P) {
+    return P.s > 1 && P.sub == FGF_SUB_NEAREST && (size_t)P.W * 4 >= 2048;
+}
+
+size_t fgf_filter_host_input_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s,
+                                 int sub_mode, int self_guided) {
+    Plan P;
+    if (make_plan(P, batch, H, W, C_I, C_p, r, 0.01, s, sub_mode)) return 0;
+    const bool self = self_guided && C_I == 1 && C_p == 1;
+    size_t b = (size_t)batch * C_I * P.N * 4;
+    if (!self)
+        b += (size_t)batch * C_p * 4 * (host_p_sample_rows(P) ? (size_t)P.h * P.W : P.N);
+    return b;
+}
+
 int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
                     int C_p, int r, double eps, int s, int sub_mode, int device) {
     g_last_launches = 0;
@@ -1329,9 +1346,28 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
         if (cudaMemcpyAsync(dI, I + (size_t)b0 * C_I * P.N, (size_t)nb * C_I * P.N * 4,
                             cudaMemcpyHostToDevice, hp.s_h2d))
             return drain(FGF_ERR_CUDA);
-        if (!self && cudaMemcpyAsync(dp, p + (size_t)b0 * C_p * P.N, (size_t)nb * C_p * P.N * 4,
-                                     cudaMemcpyHostToDevice, hp.s_h2d))
-            return drain(FGF_ERR_CUDA);
+        if (!self && !host_p_sample_rows(P)) {
+            if (cudaMemcpyAsync(dp, p + (size_t)b0 * C_p * P.N, (size_t)nb * C_p * P.N * 4,
+                                cudaMemcpyHostToDevice, hp.s_h2d))
+                return drain(FGF_ERR_CUDA);
+        } else if (!self) {
+            // Nearest samples (R3): Alg. 2 reads p only at p[y s][x s] (q = mean_a I +
+            // mean_b needs I alone at full resolution), and every engine addresses p
+            // through the row stride s W -- only rows y s cross the host link.  The device
+            // plane keeps its full geometry; its other rows are never read.
+            const size_t pitch = (size_t)s * W * 4, width = (size_t)W * 4;
+            const float* ph = p + (size_t)b0 * C_p * P.N;
+            if (H % s == 0) {   // one pitch across the chunk's planes
+                if (cudaMemcpy2DAsync(dp, pitch, ph, pitch, width, (size_t)nb * C_p * P.h,
+                                      cudaMemcpyHostToDevice, hp.s_h2d))
+                    return drain(FGF_ERR_CUDA);
+            } else {
+                for (int j = 0; j < nb * C_p; ++j)
+                    if (cudaMemcpy2DAsync(dp + (size_t)j * P.N, pitch, ph + (size_t)j * P.N, pitch,
+                                          width, P.h, cudaMemcpyHostToDevice, hp.s_h2d))
+                        return drain(FGF_ERR_CUDA);
+            }
+        }
         if (cudaEventRecord(hp.ev_in[slot], hp.s_h2d) ||
             cudaStreamWaitEvent(hp.s_comp, hp.ev_in[slot], 0))
             return drain(FGF_ERR_CUDA);

@@ -223,6 +223,39 @@ def test_host_entry_point_matches_device():
     assert torch.equal(qh2, qd.cpu())
 
 
+@pytest.mark.parametrize("B,C_I,C_p,H,W,r,s", [
+    (3, 1, 1, 540, 960, 16, 4),      # H % s == 0: one 2-D copy per chunk
+    (2, 1, 2, 541, 962, 8, 4),       # ragged H: one 2-D copy per plane; two p channels
+    (2, 3, 1, 300, 1024, 12, 3),     # colour guidance (strip engine), odd s
+    (1, 1, 1, 2050, 8192, 64, 2),    # r' = 32: K5 reading the samples in place; several chunks' worth
+])
+def test_host_entry_point_reads_only_sample_rows_of_p(B, C_I, C_p, H, W, r, s):
+    """With nearest samples Alg. 2 reads p only at p[y s][x s]:
+    fgf_filter_host copies only rows y s of p.  NaN in every other row of the host buffer
+    must not reach q, which equals the device path on the clean p bit for bit; the byte count
+    the library reports follows the same rule."""
+    g = torch.Generator(device="cuda").manual_seed(H + W + s)
+    I = torch.rand((B, C_I, H, W), device="cuda", generator=g)
+    p = torch.rand((B, C_p, H, W), device="cuda", generator=g)
+    qd = gpu_filter(I, p, r, 0.01, s, 0)
+    ph = p.cpu()
+    mask = torch.ones(H, dtype=torch.bool)
+    mask[::s] = False
+    ph[:, :, mask, :] = float("nan")
+    Ih, ph = I.cpu().pin_memory(), ph.pin_memory()
+    qh = torch.empty(qd.shape, dtype=torch.float32).pin_memory()
+    fgf.fgf_filter_host(Ih, ph, qh, B, H, W, C_I, C_p, r, 0.01, s, 0, 0)
+    assert torch.isfinite(qh).all()
+    assert torch.equal(qh, qd.cpu())
+    h = -(-H // s)
+    assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, s, 0) == 4 * B * (C_I * H * W + C_p * h * W)
+    # block means read all of p; so do s = 1, and narrow rows (< 2 KB) take the dense copy
+    assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, s, 1) == 4 * B * (C_I + C_p) * H * W
+    assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, 1, 0) == 4 * B * (C_I + C_p) * H * W
+    assert fgf.fgf_filter_host_input_bytes(1, 64, 64, 1, 1, 8, 4, 0) == 4 * 2 * 64 * 64
+    assert fgf.fgf_filter_host_input_bytes(1, 64, 64, 1, 1, 8, 4, 0, True) == 4 * 64 * 64
+
+
 def test_default_stream_entry_point():
     I, p = synth.make_batch(0, "cuda")
     q = torch.empty_like(I)
