@@ -417,8 +417,8 @@ def main():
 
     # ---------------- e2e: host buffers through fgf_filter_host (H2D + filter + D2H inside).
     e2e = None
-    if not args.no_e2e and args.dtype == "f32":   # fgf_filter_host takes fp32 buffers
-        e2e = run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B)
+    if not args.no_e2e:
+        e2e = run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B, tdt, code, esize)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -516,13 +516,13 @@ def band_main(args, fgf, torch, dist, world, rank, local, dev, barrier):
         dist.destroy_process_group()
 
 
-def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
+def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B, tdt, code, esize):
     """Same metric through fgf_filter_host: each step copies the step's inputs from pinned
     host memory to the device and q back.  The host batch is bounded by host RAM."""
     import synth
     H, W, CI, CP = c["H"], c["W"], c["C_I"], c["C_p"]
     N = H * W
-    per_img = 4 * N * (CI + (0 if args.config == 0 else CP) + CP)
+    per_img = esize * N * (CI + (0 if args.config == 0 else CP) + CP)
     try:
         avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
     except Exception:
@@ -549,10 +549,15 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
         ok = 1
         try:
             Id, pd = synth.make_batch(args.config, dev, batch=Be, first=rank * B)
+            if args.dtype == "u8":     # 8-bit codes k / 255 (R19)
+                Id = torch.round(Id.clamp(0, 1) * 255.0).to(torch.uint8)
+                pd = torch.round(pd.clamp(0, 1) * 255.0).to(torch.uint8)
+            elif args.dtype != "f32":
+                Id, pd = Id.to(tdt), pd.to(tdt)
             Ih = pinned(Id)
             ph = Ih if args.config == 0 else pinned(pd)
             del Id, pd
-            qh = torch.empty((Be, CP, H, W), dtype=torch.float32, pin_memory=True)
+            qh = torch.empty((Be, CP, H, W), dtype=tdt, pin_memory=True)
         except (RuntimeError, MemoryError):
             ok = 0
             Ih = ph = qh = Id = pd = None
@@ -564,8 +569,8 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
         Be = max(1, Be // 2)
 
     def step():
-        fgf.fgf_filter_host(Ih, ph, qh, Be, H, W, CI, CP, prm["r"], prm["eps"], prm["s"],
-                            prm["sub_mode"], local)
+        fgf.fgf_filter_host_ex(Ih, ph, qh, Be, H, W, CI, CP, prm["r"], prm["eps"], prm["s"],
+                               prm["sub_mode"], code, local)
 
     step()
     steps = args.e2e_steps or max(2, min(args.steps, 5))
@@ -582,13 +587,13 @@ def run_e2e(fgf, torch, dist, world, rank, local, args, c, prm, B):
     # bytes the call copies (the library's own rule: with nearest samples only the sample rows
     # of p are read from the host buffer, include/fgf.h)
     h2d = fgf.fgf_filter_host_input_bytes(Be, H, W, CI, CP, prm["r"], prm["s"], prm["sub_mode"],
-                                        args.config == 0)
-    h2d_dense = Be * 4 * N * (CI + (0 if args.config == 0 else CP))
-    d2h = Be * 4 * N * CP
+                                          code, args.config == 0)
+    h2d_dense = Be * esize * N * (CI + (0 if args.config == 0 else CP))
+    d2h = Be * esize * N * CP
     return {"value": world * Be * N * steps / dt / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "h2d_bytes_dense_inputs": h2d_dense,
             "batch_per_gpu": Be, "steps": steps,
-            "api": "fgf_filter_host (C ABI, pinned host buffers, H2D/compute/D2H overlapped; "
+            "api": "fgf_filter_host_ex (C ABI; fgf_filter_host is its fp32 form; pinned host buffers, H2D/compute/D2H overlapped; "
                    "nearest samples: I whole + the sample rows of p cross the link, the rows "
                    "Alg. 2 reads)"}
 

@@ -124,12 +124,17 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
  * With FGF_SUB_NEAREST and s > 1 the method reads p only at its sample sites p[y s][x s]
  * (the output step P:84-86 uses I alone at full resolution), so only rows y s of p are
  * copied to the device (rows of >= 2 KB; the other rows of the host buffer are not read).
+ * fgf_filter_host_ex: the same on host buffers of element type dtype (FGF_F32 / FGF_F16 /
+ * FGF_BF16 / FGF_U8, the channel combinations of fgf_filter_ex_ws): camera frames stay 8-bit
+ * across the host link, 1 + 1/s + 1 bytes per pixel instead of 9 (gray, nearest samples).
  * fgf_filter_host_input_bytes: the host->device bytes one such call copies (0 on invalid
  * arguments; self_guided != 0: p is the same buffer as I). */
 int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
                     int C_p, int r, double eps, int s, int sub_mode, int device);
+int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, int W, int C_I,
+                       int C_p, int r, double eps, int s, int sub_mode, int dtype, int device);
 size_t fgf_filter_host_input_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s,
-                                 int sub_mode, int self_guided);
+                                   int sub_mode, int dtype, int self_guided);
 
 /* Stages 1-5 only: writes the low-res mean maps mean_ab (DEVICE)
  * [batch][C_p][C_I+1][h][w] fp32 -- for p channel c, components j < C_I are mean_a_{c,j}

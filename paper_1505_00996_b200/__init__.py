@@ -53,7 +53,8 @@ EXPORTS = ("fgf_filter", "fgf_workspace_bytes", "fgf_filter_ws", "fgf_filter_hos
            "fgf_filter_bands_loopback", "fgf_workspace_bytes_ex", "fgf_filter_ex_ws",
            "fgf_filter_band_ex", "fgf_joint_workspace_bytes", "fgf_filter_joint_ws",
            "fgf_nccl_check", "fgf_band_geometry", "fgf_enhance_workspace_bytes",
-           "fgf_enhance_ex_ws", "fgf_filter_host_input_bytes")
+           "fgf_enhance_ex_ws", "fgf_filter_host_input_bytes",
+           "fgf_filter_host_ex")
 KERNEL_KINDS = ("subsample", "stats_coef", "box_ab", "upsample_output", "lowres_fused",
                 "wide_fused", "tiny_fused")
 
@@ -66,7 +67,9 @@ _lib.fgf_filter_ws.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
 _lib.fgf_filter_ws.restype = _i
 _lib.fgf_filter_host.argtypes = [_P, _P, _P] + _GEOM + [_i]
 _lib.fgf_filter_host.restype = _i
-_lib.fgf_filter_host_input_bytes.argtypes = [_i] * 9
+_lib.fgf_filter_host_input_bytes.argtypes = [_i] * 10
+_lib.fgf_filter_host_ex.argtypes = [_P, _P, _P] + _GEOM + [_i, _i]
+_lib.fgf_filter_host_ex.restype = _i
 _lib.fgf_filter_host_input_bytes.restype = _sz
 _lib.fgf_coefficients.argtypes = [_P, _P, _P] + _GEOM + [_P, _sz, _P]
 _lib.fgf_coefficients.restype = _i
@@ -217,9 +220,18 @@ def fgf_filter_host(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode=FGF_SUB_
 
 
 def fgf_filter_host_input_bytes(batch, H, W, C_I, C_p, r, s, sub_mode=FGF_SUB_NEAREST,
-                              self_guided=False):
-    return int(_lib.fgf_filter_host_input_bytes(batch, H, W, C_I, C_p, r, s, sub_mode,
-                                              1 if self_guided else 0))
+                                dtype=FGF_F32, self_guided=False):
+    return int(_lib.fgf_filter_host_input_bytes(batch, H, W, C_I, C_p, r, s, sub_mode, dtype,
+                                                1 if self_guided else 0))
+
+
+def fgf_filter_host_ex(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, dtype, device=0,
+                       check=True):
+    rc = _lib.fgf_filter_host_ex(_addr(I), _addr(p), _addr(q), batch, H, W, C_I, C_p, r,
+                                 float(eps), s, sub_mode, dtype, device)
+    if check:
+        _check(rc, "fgf_filter_host_ex")
+    return rc
 
 
 def fgf_coefficients(I, p, mean_ab, batch, H, W, C_I, C_p, r, eps, s, sub_mode, workspace,

@@ -1250,36 +1250,47 @@ int fgf_upsample_output_rows(const float* I, const float* mean_ab, float* q, int
 // fgf_filter_host copies only the sample rows of p when the subsampling is nearest (s > 1) and
 // the rows are long enough (>= 2 KB) for the copy engine's 2-D transfers to run at link rate.
 static bool host_p_sample_rows(const Plan& P) {
-    return P.s > 1 && P.sub == FGF_SUB_NEAREST && (size_t)P.W * 4 >= 2048;
+    return P.s > 1 && P.sub == FGF_SUB_NEAREST && (size_t)P.W * P.esize >= 2048;
 }
 
 size_t fgf_filter_host_input_bytes(int batch, int H, int W, int C_I, int C_p, int r, int s,
-                                 int sub_mode, int self_guided) {
+                                   int sub_mode, int dtype, int self_guided) {
     Plan P;
-    if (make_plan(P, batch, H, W, C_I, C_p, r, 0.01, s, sub_mode)) return 0;
+    if (make_plan(P, batch, H, W, C_I, C_p, r, 0.01, s, sub_mode) || set_dtype(P, dtype)) return 0;
     const bool self = self_guided && C_I == 1 && C_p == 1;
-    size_t b = (size_t)batch * C_I * P.N * 4;
+    size_t b = (size_t)batch * C_I * P.N * P.esize;
     if (!self)
-        b += (size_t)batch * C_p * 4 * (host_p_sample_rows(P) ? (size_t)P.h * P.W : P.N);
+        b += (size_t)batch * C_p * P.esize * (host_p_sample_rows(P) ? (size_t)P.h * P.W : P.N);
     return b;
 }
 
-int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
-                    int C_p, int r, double eps, int s, int sub_mode, int device) {
+int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, int W, int C_I,
+                       int C_p, int r, double eps, int s, int sub_mode, int dtype, int device) {
     g_last_launches = 0;
     Plan P;
     int rc = make_plan(P, batch, H, W, C_I, C_p, r, eps, s, sub_mode);
     if (rc) return rc;
+    if ((rc = set_dtype(P, dtype))) return rc;
+    if (dtype != FGF_F32 && !(C_I * 10 + C_p == 11 || C_I * 10 + C_p == 31 || C_I * 10 + C_p == 33))
+        return FGF_ERR_UNSUPPORTED;
     if ((rc = check_pointers(I, p, q, P, false))) return rc;
     if (cudaSetDevice(device) != cudaSuccess) return FGF_ERR_CUDA;
     const bool self = (I == p) && C_I == 1 && C_p == 1;
+    const size_t es = P.esize;
+    const char* Ih = static_cast<const char*>(I);
+    const char* ph = static_cast<const char*>(p);
+    char* qh = static_cast<char*>(q);
 
-    // Sub-batch per pipeline slot: ~256 MB of I+p+q, at least one image.
-    const size_t img_floats = (size_t)(C_I + (self ? 0 : C_p) + C_p) * P.N;
-    const int sb = (int)std::max<size_t>(1, std::min<size_t>(batch, (256u << 20) / (img_floats * 4)));
+    // Sub-batch per pipeline slot: ~256 MB of I+p+q, at least one image; the I, p and q parts
+    // of a slot start on 256-byte boundaries.
+    const size_t img_bytes = (size_t)(C_I + (self ? 0 : C_p) + C_p) * P.N * es;
+    const int sb = (int)std::max<size_t>(1, std::min<size_t>(batch, (256u << 20) / img_bytes));
     Plan Psub;
     make_plan(Psub, sb, H, W, C_I, C_p, r, eps, s, sub_mode);
-    const size_t slot_bytes = align_up(img_floats * sb * 4);
+    set_dtype(Psub, dtype);
+    const size_t partI = align_up((size_t)sb * C_I * P.N * es);
+    const size_t partP = self ? 0 : align_up((size_t)sb * C_p * P.N * es);
+    const size_t slot_bytes = partI + partP + align_up((size_t)sb * C_p * P.N * es);
     const size_t need_ws = plan_ws(Psub, true);
 
     std::lock_guard<std::mutex> lk(g_host_mu);
@@ -1338,16 +1349,16 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
     for (int b0 = 0; b0 < batch; b0 += sb, ++k) {
         const int nb = std::min(sb, batch - b0);
         const int slot = k & 1;
-        float* dI = hp.dbuf[slot];
-        float* dp = self ? dI : dI + (size_t)nb * C_I * P.N;
-        float* dq = dI + (size_t)nb * (C_I + (self ? 0 : C_p)) * P.N;
+        char* dI = reinterpret_cast<char*>(hp.dbuf[slot]);
+        char* dp = self ? dI : dI + partI;
+        char* dq = dI + partI + partP;
         // The slot is free once the D2H of chunk k-2 has finished.
         if (k >= 2 && cudaStreamWaitEvent(hp.s_h2d, hp.ev_free[slot], 0)) return drain(FGF_ERR_CUDA);
-        if (cudaMemcpyAsync(dI, I + (size_t)b0 * C_I * P.N, (size_t)nb * C_I * P.N * 4,
+        if (cudaMemcpyAsync(dI, Ih + (size_t)b0 * C_I * P.N * es, (size_t)nb * C_I * P.N * es,
                             cudaMemcpyHostToDevice, hp.s_h2d))
             return drain(FGF_ERR_CUDA);
         if (!self && !host_p_sample_rows(P)) {
-            if (cudaMemcpyAsync(dp, p + (size_t)b0 * C_p * P.N, (size_t)nb * C_p * P.N * 4,
+            if (cudaMemcpyAsync(dp, ph + (size_t)b0 * C_p * P.N * es, (size_t)nb * C_p * P.N * es,
                                 cudaMemcpyHostToDevice, hp.s_h2d))
                 return drain(FGF_ERR_CUDA);
         } else if (!self) {
@@ -1355,16 +1366,16 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
             // mean_b needs I alone at full resolution), and every engine addresses p
             // through the row stride s W -- only rows y s cross the host link.  The device
             // plane keeps its full geometry; its other rows are never read.
-            const size_t pitch = (size_t)s * W * 4, width = (size_t)W * 4;
-            const float* ph = p + (size_t)b0 * C_p * P.N;
+            const size_t pitch = (size_t)s * W * es, width = (size_t)W * es;
+            const char* pc = ph + (size_t)b0 * C_p * P.N * es;
             if (H % s == 0) {   // one pitch across the chunk's planes
-                if (cudaMemcpy2DAsync(dp, pitch, ph, pitch, width, (size_t)nb * C_p * P.h,
+                if (cudaMemcpy2DAsync(dp, pitch, pc, pitch, width, (size_t)nb * C_p * P.h,
                                       cudaMemcpyHostToDevice, hp.s_h2d))
                     return drain(FGF_ERR_CUDA);
             } else {
                 for (int j = 0; j < nb * C_p; ++j)
-                    if (cudaMemcpy2DAsync(dp + (size_t)j * P.N, pitch, ph + (size_t)j * P.N, pitch,
-                                          width, P.h, cudaMemcpyHostToDevice, hp.s_h2d))
+                    if (cudaMemcpy2DAsync(dp + (size_t)j * P.N * es, pitch, pc + (size_t)j * P.N * es,
+                                          pitch, width, P.h, cudaMemcpyHostToDevice, hp.s_h2d))
                         return drain(FGF_ERR_CUDA);
             }
         }
@@ -1373,13 +1384,14 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
             return drain(FGF_ERR_CUDA);
         Plan Pc;
         if ((rc = make_plan(Pc, nb, H, W, C_I, C_p, r, eps, s, sub_mode))) return drain(rc);
+        if ((rc = set_dtype(Pc, dtype))) return drain(rc);
         if ((rc = run_all(dI, dp, dq, Pc, hp.ws, hp.wsbytes, hp.s_comp))) return drain(rc);
         launches += g_last_launches;
         g_last_launches = 0;
         if (cudaEventRecord(hp.ev_done[slot], hp.s_comp) ||
             cudaStreamWaitEvent(hp.s_d2h, hp.ev_done[slot], 0))
             return drain(FGF_ERR_CUDA);
-        if (cudaMemcpyAsync(q + (size_t)b0 * C_p * P.N, dq, (size_t)nb * C_p * P.N * 4,
+        if (cudaMemcpyAsync(qh + (size_t)b0 * C_p * P.N * es, dq, (size_t)nb * C_p * P.N * es,
                             cudaMemcpyDeviceToHost, hp.s_d2h))
             return drain(FGF_ERR_CUDA);
         if (cudaEventRecord(hp.ev_free[slot], hp.s_d2h)) return drain(FGF_ERR_CUDA);
@@ -1387,6 +1399,11 @@ int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, 
     if ((rc = drain(FGF_OK))) return rc;
     g_last_launches = launches;
     return FGF_OK;
+}
+
+int fgf_filter_host(const float* I, const float* p, float* q, int batch, int H, int W, int C_I,
+                    int C_p, int r, double eps, int s, int sub_mode, int device) {
+    return fgf_filter_host_ex(I, p, q, batch, H, W, C_I, C_p, r, eps, s, sub_mode, FGF_F32, device);
 }
 
 }  // extern "C"

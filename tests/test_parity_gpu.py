@@ -253,7 +253,37 @@ def test_host_entry_point_reads_only_sample_rows_of_p(B, C_I, C_p, H, W, r, s):
     assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, s, 1) == 4 * B * (C_I + C_p) * H * W
     assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, 1, 0) == 4 * B * (C_I + C_p) * H * W
     assert fgf.fgf_filter_host_input_bytes(1, 64, 64, 1, 1, 8, 4, 0) == 4 * 2 * 64 * 64
-    assert fgf.fgf_filter_host_input_bytes(1, 64, 64, 1, 1, 8, 4, 0, True) == 4 * 64 * 64
+    assert fgf.fgf_filter_host_input_bytes(1, 64, 64, 1, 1, 8, 4, 0, self_guided=True) == 4 * 64 * 64
+
+
+@pytest.mark.parametrize("dt,B,C_I,C_p,H,W,r,s,sub", [
+    ("u8", 3, 1, 1, 540, 2048, 16, 4, 0),     # 8-bit frames, sample rows of p only (2 KB rows)
+    ("u8", 2, 1, 1, 301, 403, 8, 4, 0),       # odd plane sizes, narrow rows: dense copy of p
+    ("f16", 2, 1, 1, 540, 1920, 16, 4, 0),
+    ("bf16", 1, 3, 3, 270, 1024, 8, 2, 1),    # colour, block means: dense copy
+    ("u8", 2, 3, 1, 300, 2048, 12, 3, 0),     # colour guidance, odd s
+])
+def test_host_entry_point_reduced_precision(dt, B, C_I, C_p, H, W, r, s, sub):
+    """fgf_filter_host_ex: host buffers of 8-bit codes / 16-bit floats through the same
+    pipeline -- bit-identical to the device entry point on the same values."""
+    tdt = {"u8": torch.uint8, "f16": torch.float16, "bf16": torch.bfloat16}[dt]
+    code = {"u8": fgf.FGF_U8, "f16": fgf.FGF_F16, "bf16": fgf.FGF_BF16}[dt]
+    g = torch.Generator(device="cuda").manual_seed(H + W + s)
+    def mk(C):
+        t = torch.rand((B, C, H, W), device="cuda", generator=g)
+        return (t * 255).round().to(torch.uint8) if dt == "u8" else t.to(tdt)
+    I, p = mk(C_I), mk(C_p)
+    qd = fgf.filter(I, p, r, 0.01, s, sub)
+    torch.cuda.synchronize()
+    assert qd.dtype == tdt
+    Ih, ph = I.cpu().pin_memory(), p.cpu().pin_memory()
+    qh = torch.empty(qd.shape, dtype=tdt).pin_memory()
+    fgf.fgf_filter_host_ex(Ih, ph, qh, B, H, W, C_I, C_p, r, 0.01, s, sub, code, 0)
+    assert torch.equal(qh, qd.cpu())
+    es = 1 if dt == "u8" else 2
+    rows = -(-H // s) if (sub == 0 and s > 1 and W * es >= 2048) else H
+    assert fgf.fgf_filter_host_input_bytes(B, H, W, C_I, C_p, r, s, sub, code) == \
+        es * B * (C_I * H * W + C_p * rows * W)
 
 
 def test_default_stream_entry_point():
