@@ -118,3 +118,39 @@ def test_fuzz_band_loopback(seed):
     assert float((q - q_whole).abs().max()) <= 1e-5, (seed, H, W, CI, CP, r, s, sub, mode, nranks)
     ref = oracle.fast_guided_filter(I.cpu().numpy(), p.cpu().numpy(), r, eps, s, sub)
     assert float(np.abs(q.double().cpu().numpy() - ref).max()) <= 1e-4
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FGF_FUZZ_HOST_SEEDS", "40"))))
+def test_fuzz_host_entry_point_equals_device(seed):
+    """fgf_filter_host_ex on random geometries (the same generator, widths up to 2080 so that
+    both the sample-row copy of p and the dense copy occur, H a multiple of s or not, pinned or
+    pageable buffers): q is bit-identical to the device entry point on the same values, with
+    NaN / 255 planted in the rows of p the method does not read."""
+    B, H, W, CI, CP, r, eps, s, sub, dtype, self_guided = _case(seed + 5000)
+    rng = np.random.default_rng(seed + 77)
+    W = int(rng.choice([W, 512, 1024, 2080]))
+    if s > 1 and s >= min(H, W):
+        s = 1
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    I = _store(torch.rand((B, CI, H, W), device="cuda", generator=g), dtype)
+    p = I if self_guided else _store(torch.rand((B, CP, H, W), device="cuda", generator=g), dtype)
+    qd = fgf.filter(I, p, r, eps, s, sub)
+    torch.cuda.synchronize()
+    code = {torch.float32: fgf.FGF_F32, torch.float16: fgf.FGF_F16, torch.bfloat16: fgf.FGF_BF16,
+            torch.uint8: fgf.FGF_U8}[dtype]
+    pin = bool(rng.integers(0, 2))
+    Ih = I.cpu()
+    ph = Ih if self_guided else p.cpu()
+    sparse = fgf.fgf_filter_host_input_bytes(B, H, W, CI, CP, r, s, sub, code, self_guided) < \
+        I.element_size() * B * (CI + (0 if self_guided else CP)) * H * W
+    if sparse:   # the rows between the sample rows are not read: poison them
+        mask = torch.ones(H, dtype=torch.bool)
+        mask[::s] = False
+        ph[:, :, mask, :] = 255 if dtype == torch.uint8 else float("nan")
+    if pin:
+        Ih = Ih.pin_memory()
+        ph = Ih if self_guided else ph.pin_memory()
+    qh = torch.empty(qd.shape, dtype=dtype)
+    qh = qh.pin_memory() if pin else qh
+    fgf.fgf_filter_host_ex(Ih, ph, qh, B, H, W, CI, CP, r, eps, s, sub, code, 0)
+    assert torch.equal(qh, qd.cpu()), (B, H, W, CI, CP, r, eps, s, sub, dtype, self_guided, sparse)
