@@ -427,6 +427,7 @@ std::mutex g_ws_mu;
 std::vector<DevWs> g_ws;
 
 // Host-buffer pipeline state (fgf_filter_host), one per device.
+constexpr int kHostBands = 8;
 struct HostPipe {
     float* dbuf[2] = {nullptr, nullptr};
     size_t dbytes = 0;
@@ -434,6 +435,7 @@ struct HostPipe {
     size_t wsbytes = 0;
     cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_in[2], ev_done[2], ev_free[2];
+    cudaEvent_t ev_bin[kHostBands], ev_bout[kHostBands];   // single-frame row-band pipeline
     bool init = false;
 };
 std::mutex g_host_mu;
@@ -1309,6 +1311,10 @@ int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, 
                 cudaEventCreateWithFlags(&hp.ev_free[k], cudaEventDisableTiming))
                 return FGF_ERR_CUDA;
         }
+        for (int k = 0; k < kHostBands; ++k)
+            if (cudaEventCreateWithFlags(&hp.ev_bin[k], cudaEventDisableTiming) ||
+                cudaEventCreateWithFlags(&hp.ev_bout[k], cudaEventDisableTiming))
+                return FGF_ERR_CUDA;
         hp.init = true;
     }
     if (hp.dbytes < slot_bytes) {
@@ -1347,6 +1353,65 @@ int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, 
         return status != FGF_OK ? status : (ok ? FGF_OK : FGF_ERR_CUDA);
     };
     int launches = 0;
+    // ONE gray fp32 frame, nearest samples: whole-image chunks cannot overlap anything, so the
+    // frame is pipelined by rows instead.  The sample rows of I and p go first and the low-res
+    // chain (steps 1-5) runs on them while the other rows of I follow in kHostBands bands; each
+    // band's output pass (steps 6-7, global vertical map) starts when its rows have arrived
+    // and its q rows leave while the next band is still coming in.
+    const bool frame_bands = batch == 1 && C_I == 1 && C_p == 1 && dtype == FGF_F32 &&
+                             host_p_sample_rows(P) && !P.fused_out && P.h >= 4 * kHostBands &&
+                             dev_env("FGF_HOST_NOBANDS") == nullptr;
+    if (frame_bands) {
+        char* dI = reinterpret_cast<char*>(hp.dbuf[0]);
+        char* dp = self ? dI : dI + partI;
+        char* dq = dI + partI + partP;
+        const size_t rowb = (size_t)W * es, pitch = (size_t)s * rowb;
+        if (cudaMemcpy2DAsync(dI, pitch, Ih, pitch, rowb, P.h, cudaMemcpyHostToDevice, hp.s_h2d))
+            return drain(FGF_ERR_CUDA);
+        if (!self && cudaMemcpy2DAsync(dp, pitch, ph, pitch, rowb, P.h, cudaMemcpyHostToDevice, hp.s_h2d))
+            return drain(FGF_ERR_CUDA);
+        if (cudaEventRecord(hp.ev_in[0], hp.s_h2d) || cudaStreamWaitEvent(hp.s_comp, hp.ev_in[0], 0))
+            return drain(FGF_ERR_CUDA);
+        float* mean = reinterpret_cast<float*>(static_cast<char*>(hp.ws) + mean_off(P));
+        if ((rc = run_lowres(dI, dp, mean, 0, 1, P, static_cast<char*>(hp.ws), hp.s_comp)))
+            return drain(rc);
+        launches += g_last_launches;
+        g_last_launches = 0;
+        const int hb = (P.h + kHostBands - 1) / kHostBands;   // low-res rows per band
+        for (int k = 0; k * hb < P.h; ++k) {
+            const int Y0 = k * hb * s, Y1 = std::min(H, (k + 1) * hb * s), rows = Y1 - Y0;
+            // rows y s + 1 .. y s + s - 1 of the band's full groups, then a partial last group
+            const int groups = rows / s, rem = rows - groups * s;
+            const size_t o = (size_t)Y0 * rowb;
+            if (groups > 0 && cudaMemcpy2DAsync(dI + o + rowb, pitch, Ih + o + rowb, pitch,
+                                                (size_t)(s - 1) * rowb, groups,
+                                                cudaMemcpyHostToDevice, hp.s_h2d))
+                return drain(FGF_ERR_CUDA);
+            if (rem > 1 && cudaMemcpyAsync(dI + o + (size_t)groups * pitch + rowb,
+                                           Ih + o + (size_t)groups * pitch + rowb,
+                                           (size_t)(rem - 1) * rowb, cudaMemcpyHostToDevice, hp.s_h2d))
+                return drain(FGF_ERR_CUDA);
+            if (cudaEventRecord(hp.ev_bin[k], hp.s_h2d) ||
+                cudaStreamWaitEvent(hp.s_comp, hp.ev_bin[k], 0))
+                return drain(FGF_ERR_CUDA);
+            Plan Pr{};
+            Pr.batch = 1; Pr.H = rows; Pr.W = W; Pr.CI = 1; Pr.CP = 1; Pr.NC = P.NC;
+            Pr.h = P.h; Pr.w = P.w; Pr.N = (size_t)rows * W; Pr.n = P.n; Pr.TR = 32;
+            Pr.s = s; Pr.sub = sub_mode; Pr.r = r; Pr.R = P.R; Pr.eps = eps;
+            const Band band{H, P.h, Y0, 0, P.h};
+            if ((rc = launch_output(dI + o, mean, dq + o, 1, Pr, hp.s_comp, &band))) return drain(rc);
+            launches += g_last_launches;
+            g_last_launches = 0;
+            if (cudaEventRecord(hp.ev_bout[k], hp.s_comp) ||
+                cudaStreamWaitEvent(hp.s_d2h, hp.ev_bout[k], 0))
+                return drain(FGF_ERR_CUDA);
+            if (cudaMemcpyAsync(qh + o, dq + o, (size_t)rows * rowb, cudaMemcpyDeviceToHost, hp.s_d2h))
+                return drain(FGF_ERR_CUDA);
+        }
+        if ((rc = drain(FGF_OK))) return rc;
+        g_last_launches = launches;
+        return FGF_OK;
+    }
     int k = 0;
     for (int b0 = 0; b0 < batch; b0 += sb, ++k) {
         const int nb = std::min(sb, batch - b0);

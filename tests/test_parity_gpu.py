@@ -228,6 +228,9 @@ def test_host_entry_point_matches_device():
     (2, 1, 2, 541, 962, 8, 4),       # ragged H: one 2-D copy per plane; two p channels
     (2, 3, 1, 300, 1024, 12, 3),     # colour guidance (strip engine), odd s
     (1, 1, 1, 2050, 8192, 64, 2),    # r' = 32: K5 reading the samples in place; several chunks' worth
+    (1, 1, 1, 1083, 1030, 8, 4),     # ONE gray frame: the row-band pipeline; partial last group (3 rows)
+    (1, 1, 1, 1081, 2052, 16, 4),    # ... a last group of the sample row alone
+    (1, 1, 1, 999, 1200, 9, 3),      # ... odd s, H a multiple of s
 ])
 def test_host_entry_point_reads_only_sample_rows_of_p(B, C_I, C_p, H, W, r, s):
     """With nearest samples Alg. 2 reads p only at p[y s][x s]:
