@@ -1286,9 +1286,16 @@ int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, 
     // Sub-batch per pipeline slot: ~256 MB of I+p+q, at least one image; the I, p and q parts
     // of a slot start on 256-byte boundaries.
     const size_t img_bytes = (size_t)(C_I + (self ? 0 : C_p) + C_p) * P.N * es;
+    // ... and at least four chunks when the batch has four images, so that a small batch still
+    // overlaps its copies with the filter (the development knob sets the slot size alone).
     size_t slot_target = 256u << 20;
-    if (const char* e = dev_env("FGF_HOST_CHUNK_MB")) slot_target = (size_t)std::max(1, atoi(e)) << 20;
-    const int sb = (int)std::max<size_t>(1, std::min<size_t>(batch, slot_target / img_bytes));
+    int sb_cap = std::max(1, (batch + 3) / 4);
+    if (const char* e = dev_env("FGF_HOST_CHUNK_MB")) {
+        slot_target = (size_t)std::max(1, atoi(e)) << 20;
+        sb_cap = batch;
+    }
+    const int sb = (int)std::max<size_t>(
+        1, std::min<size_t>(std::min(batch, sb_cap), slot_target / img_bytes));
     Plan Psub;
     make_plan(Psub, sb, H, W, C_I, C_p, r, eps, s, sub_mode);
     set_dtype(Psub, dtype);
