@@ -124,7 +124,7 @@ int fgf_filter_ws(const float* I, const float* p, float* q, int batch, int H, in
  * With FGF_SUB_NEAREST and s > 1 the method reads p only at its sample sites p[y s][x s]
  * (the output step P:84-86 uses I alone at full resolution), so only rows y s of p are
  * copied to the device (rows of >= 2 KB; the other rows of the host buffer are not read).
- * One gray fp32 frame (batch 1) with nearest samples is pipelined by rows: the sample rows
+ * One gray frame (batch 1, any element type) with nearest samples is pipelined by rows: the sample rows
  * first, the low-res chain on them while the other rows of I arrive in 8 bands, each band's
  * output rows computed and copied back as soon as its rows are on the device.
  * fgf_filter_host_ex: the same on host buffers of element type dtype (FGF_F32 / FGF_F16 /

@@ -1360,12 +1360,12 @@ int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, 
         return status != FGF_OK ? status : (ok ? FGF_OK : FGF_ERR_CUDA);
     };
     int launches = 0;
-    // ONE gray fp32 frame, nearest samples: whole-image chunks cannot overlap anything, so the
+    // ONE gray frame (any element type), nearest samples: whole-image chunks cannot overlap anything, so the
     // frame is pipelined by rows instead.  The sample rows of I and p go first and the low-res
     // chain (steps 1-5) runs on them while the other rows of I follow in kHostBands bands; each
     // band's output pass (steps 6-7, global vertical map) starts when its rows have arrived
     // and its q rows leave while the next band is still coming in.
-    const bool frame_bands = batch == 1 && C_I == 1 && C_p == 1 && dtype == FGF_F32 &&
+    const bool frame_bands = batch == 1 && C_I == 1 && C_p == 1 &&
                              host_p_sample_rows(P) && !P.fused_out && P.h >= 4 * kHostBands &&
                              dev_env("FGF_HOST_NOBANDS") == nullptr;
     if (frame_bands) {
@@ -1405,6 +1405,7 @@ int fgf_filter_host_ex(const void* I, const void* p, void* q, int batch, int H, 
             Pr.batch = 1; Pr.H = rows; Pr.W = W; Pr.CI = 1; Pr.CP = 1; Pr.NC = P.NC;
             Pr.h = P.h; Pr.w = P.w; Pr.N = (size_t)rows * W; Pr.n = P.n; Pr.TR = 32;
             Pr.s = s; Pr.sub = sub_mode; Pr.r = r; Pr.R = P.R; Pr.eps = eps;
+            Pr.dtype = dtype; Pr.esize = (int)es;
             const Band band{H, P.h, Y0, 0, P.h};
             if ((rc = launch_output(dI + o, mean, dq + o, 1, Pr, hp.s_comp, &band))) return drain(rc);
             launches += g_last_launches;

@@ -265,6 +265,9 @@ def test_host_entry_point_reads_only_sample_rows_of_p(B, C_I, C_p, H, W, r, s):
     ("f16", 2, 1, 1, 540, 1920, 16, 4, 0),
     ("bf16", 1, 3, 3, 270, 1024, 8, 2, 1),    # colour, block means: dense copy
     ("u8", 2, 3, 1, 300, 2048, 12, 3, 0),     # colour guidance, odd s
+    ("u8", 1, 1, 1, 1083, 2051, 16, 4, 0),    # ONE 8-bit frame: the row-band pipeline, odd row bytes
+    ("f16", 1, 1, 1, 1081, 1026, 8, 4, 0),    # ... 16-bit, a last group of the sample row alone
+    ("bf16", 1, 1, 1, 720, 1280, 12, 3, 0),
 ])
 def test_host_entry_point_reduced_precision(dt, B, C_I, C_p, H, W, r, s, sub):
     """fgf_filter_host_ex: host buffers of 8-bit codes / 16-bit floats through the same
